@@ -1,0 +1,1164 @@
+// pm_capi.cu — device context and the C-ABI entry points of include/pm_b200.h.
+//
+// Host C++ drives hand-written sm_100a kernels (pm_kernels.cuh) on one CUDA stream.  Nothing here
+// computes any part of the path on the CPU: the host samples projection plans (the reference's
+// PRNG stream, pm_host.cpp), turns them into constant-memory extraction programs, launches the
+// kernels and scans the per-trial summaries in ascending trial order exactly like the
+// reduction of driver.hpp:195-208.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "pm_internal.hpp"
+#include "pm_kernels.cuh"
+
+using namespace pm;
+
+namespace {
+
+#define PM_CUDA(call)                                                                                  \
+    do {                                                                                               \
+        const cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess) {                                                                       \
+            return set_error(e_ == cudaErrorMemoryAllocation ? PM_ERR_OUT_OF_MEMORY : PM_ERR_CUDA,     \
+                             std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+        }                                                                                              \
+    } while (0)
+
+#define PM_TRY(call)                  \
+    do {                              \
+        const int rc_ = (call);       \
+        if (rc_ != PM_OK) return rc_; \
+    } while (0)
+
+// grow-only device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+enum Slot {
+    S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
+    S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
+    S_SCAL, S_MEMBERS, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
+};
+
+}  // namespace
+
+struct pm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    int64_t launches = 0;
+    // sequence set
+    int t = 0;
+    std::vector<int64_t> offs, word_off;
+    std::vector<int32_t> seq_len;
+    int64_t total_bases = 0, total_words = 0;
+    uint64_t* d_words = nullptr;
+    int64_t* d_word_off = nullptr;
+    int32_t* d_seq_len = nullptr;
+    unsigned int* d_seq_sym = nullptr;
+    unsigned long long* d_tot_sym = nullptr;  // [0..3] symbol totals, [4] first bad byte
+    unsigned long long tot_sym[4] = {0, 0, 0, 0};
+    // window index space for the current l
+    int win_l = 0;
+    std::vector<int64_t> win_off;
+    int64_t* d_win_off = nullptr;
+    int64_t x = 0, uniform_w = 0;
+    DevBuf buf[S_COUNT_];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+template <typename T>
+int get_buf(pm_ctx* c, Slot s, size_t n, T** out) {
+    DevBuf& b = c->buf[s];
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    if (bytes > b.cap) {
+        if (b.p != nullptr) {
+            PM_CUDA(cudaStreamSynchronize(c->stream));
+            PM_CUDA(cudaFree(b.p));
+            b.p = nullptr;
+            b.cap = 0;
+        }
+        const size_t want = bytes + bytes / 4;  // a little headroom so growing batches do not thrash
+        PM_CUDA(cudaMalloc(&b.p, want));
+        b.cap = want;
+    }
+    *out = static_cast<T*>(b.p);
+    return PM_OK;
+}
+
+int check_launch(pm_ctx* c, const char* what) {
+    ++c->launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(PM_ERR_CUDA, std::string(what) + " launch: " + cudaGetErrorString(e));
+    return PM_OK;
+}
+
+int need_sequences(const pm_ctx* c) {
+    if (c == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null context");
+    if (c->t < 1) return set_error(PM_ERR_INVALID_PARAMS, "no sequence set loaded: call pm_ctx_set_sequences first");
+    return PM_OK;
+}
+
+// (seq, offset) index space for motif length l (sequence.hpp:103-132)
+int prepare_windows(pm_ctx* c, int l) {
+    if (l < 1) return set_error(PM_ERR_INVALID_PARAMS, "motif length l must be positive");
+    if (l > PM_MAX_L) {
+        return set_error(PM_ERR_UNSUPPORTED, "l=" + std::to_string(l) + " exceeds this build's limit of " +
+                                                 std::to_string(PM_MAX_L) + " (one 64-bit word per l-mer)");
+    }
+    if (c->win_l == l) return PM_OK;
+    c->win_off.assign(static_cast<size_t>(c->t) + 1, 0);
+    bool uniform = true;
+    for (int i = 0; i < c->t; ++i) {
+        const int64_t w = c->seq_len[static_cast<size_t>(i)] - l + 1;
+        if (w < 1) {
+            return set_error(PM_ERR_INVALID_PARAMS, "sequence 'seq" + std::to_string(i + 1) + "' of length " +
+                                                        std::to_string(c->seq_len[static_cast<size_t>(i)]) +
+                                                        " has no l-mer of length " + std::to_string(l));
+        }
+        c->win_off[static_cast<size_t>(i) + 1] = c->win_off[static_cast<size_t>(i)] + w;
+        uniform = uniform && c->seq_len[static_cast<size_t>(i)] == c->seq_len[0];
+    }
+    c->x = c->win_off[static_cast<size_t>(c->t)];
+    if (c->x > static_cast<int64_t>(std::numeric_limits<uint32_t>::max())) {
+        return set_error(PM_ERR_INVALID_PARAMS, "sort-and-group hashing supports at most 2^32-1 l-mers");  // projection.hpp:284-287
+    }
+    c->uniform_w = uniform ? c->seq_len[0] - l + 1 : 0;
+    PM_CUDA(cudaMemcpyAsync(c->d_win_off, c->win_off.data(), sizeof(int64_t) * (static_cast<size_t>(c->t) + 1),
+                            cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    c->win_l = l;
+    return PM_OK;
+}
+
+// kept positions (1-based, validated) -> constant-memory extraction program
+k::PlanProg make_prog(const int32_t* kept, int kk) {
+    k::PlanProg pp;
+    std::memset(&pp, 0, sizeof(pp));
+    pp.keybits = static_cast<uint8_t>(2 * kk);
+    int i = 0;
+    while (i < kk) {
+        int j = i;
+        while (j + 1 < kk && kept[j + 1] == kept[j] + 1) ++j;
+        const int width = j - i + 1;
+        pp.rshift[pp.nruns] = static_cast<uint8_t>(64 - 2 * kept[j]);  // last digit of the run, 0-based kept[j]-1
+        pp.nbits[pp.nruns] = static_cast<uint8_t>(2 * width);
+        ++pp.nruns;
+        i = j + 1;
+    }
+    return pp;
+}
+
+// ---------------------------------------------------------------------------------------------
+// stable segmented radix sort driver: sorts key bits [0, keybits) of every segment; on return
+// *ko/*io point at the buffers holding the result.
+// ---------------------------------------------------------------------------------------------
+template <typename KeyT>
+int sort_segments(pm_ctx* c, KeyT* ka, KeyT* kb, unsigned int* ia, unsigned int* ib, int nseg, int64_t stride,
+                  int64_t len, const unsigned int* len_dev, int keybits, KeyT** ko, unsigned int** io) {
+    const int64_t span = len_dev ? stride : len;
+    const int tiles = static_cast<int>((span + k::kSortTile - 1) / k::kSortTile);
+    unsigned int* counts = nullptr;
+    PM_TRY(get_buf(c, S_COUNTS, static_cast<size_t>(nseg) * 256 * static_cast<size_t>(std::max(tiles, 1)), &counts));
+    const int passes = (keybits + 7) / 8;
+    KeyT* kin = ka;
+    KeyT* kout = kb;
+    unsigned int* iin = ia;
+    unsigned int* iout = ib;
+    bool first = true;
+    if (tiles == 0 || nseg == 0) {
+        *ko = ka;
+        *io = ia;
+        return PM_OK;
+    }
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = 8 * pass;
+        const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nseg));
+        k::radix_hist_kernel<KeyT><<<grid, k::kSortWarps * 32, 0, c->stream>>>(kin, stride, len, len_dev, tiles, shift, counts);
+        PM_TRY(check_launch(c, "radix_hist"));
+        k::radix_scan_kernel<<<nseg, 256, 0, c->stream>>>(counts, tiles);
+        PM_TRY(check_launch(c, "radix_scan"));
+        if (first) {
+            k::radix_scatter_kernel<KeyT, true><<<grid, k::kSortWarps * 32, 0, c->stream>>>(
+                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts);
+        } else {
+            k::radix_scatter_kernel<KeyT, false><<<grid, k::kSortWarps * 32, 0, c->stream>>>(
+                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts);
+        }
+        PM_TRY(check_launch(c, "radix_scatter"));
+        first = false;
+        std::swap(kin, kout);
+        std::swap(iin, iout);
+    }
+    *ko = kin;
+    *io = iin;
+    return PM_OK;
+}
+
+// keys of n_trials plans -> sorted (key, flat index) per trial
+template <typename KeyT>
+struct Sorted {
+    KeyT* keys = nullptr;
+    unsigned int* idx = nullptr;
+};
+
+template <typename KeyT>
+int project_keys(pm_ctx* c, const std::vector<k::PlanProg>& progs, KeyT* keys) {
+    const int n = static_cast<int>(progs.size());
+    for (int base = 0; base < n; base += k::kMaxConstPlans) {
+        const int cnt = std::min(k::kMaxConstPlans, n - base);
+        PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
+                                        0, cudaMemcpyHostToDevice, c->stream));
+        const unsigned gx = static_cast<unsigned>(std::min<int64_t>((c->x + 255) / 256, 4096));
+        const dim3 grid(std::max(gx, 1u), static_cast<unsigned>(cnt));
+        k::project_keys_kernel<KeyT><<<grid, 256, 0, c->stream>>>(c->d_words, c->d_word_off, c->d_win_off, c->t, c->x,
+                                                                c->uniform_w, base, cnt, keys);
+        PM_TRY(check_launch(c, "project_keys"));
+    }
+    return PM_OK;
+}
+
+template <typename KeyT>
+int hash_and_sort(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keybits, Sorted<KeyT>* out) {
+    const size_t n = progs.size() * static_cast<size_t>(c->x);
+    KeyT *ka, *kb;
+    unsigned int *ia, *ib;
+    PM_TRY(get_buf(c, S_KEYS_A, n, &ka));
+    PM_TRY(get_buf(c, S_KEYS_B, n, &kb));
+    PM_TRY(get_buf(c, S_IDX_A, n, &ia));
+    PM_TRY(get_buf(c, S_IDX_B, n, &ib));
+    PM_TRY(project_keys<KeyT>(c, progs, ka));
+    return sort_segments<KeyT>(c, ka, kb, ia, ib, static_cast<int>(progs.size()), c->x, c->x, nullptr, keybits,
+                               &out->keys, &out->idx);
+}
+
+struct Records {
+    uint64_t* key = nullptr;
+    unsigned int* start = nullptr;
+    unsigned int* size = nullptr;
+    unsigned int* n_rec = nullptr;
+    int64_t cap_e = 0;
+};
+
+template <typename KeyT>
+int find_enriched(pm_ctx* c, const Sorted<KeyT>& s, int n_trials, int thr, Records* r) {
+    r->cap_e = std::max<int64_t>(1, c->x / thr);
+    const size_t n = static_cast<size_t>(n_trials) * static_cast<size_t>(r->cap_e);
+    PM_TRY(get_buf(c, S_REC_KEY, n, &r->key));
+    PM_TRY(get_buf(c, S_REC_START, n, &r->start));
+    PM_TRY(get_buf(c, S_REC_SIZE, n, &r->size));
+    PM_TRY(get_buf(c, S_NREC, static_cast<size_t>(n_trials) + 1, &r->n_rec));
+    k::enrich_kernel<KeyT><<<n_trials, 1024, 0, c->stream>>>(s.keys, c->x, thr, r->cap_e, r->key, r->start, r->size, r->n_rec);
+    return check_launch(c, "enrich");
+}
+
+// ---------------------------------------------------------------------------------------------
+// EM launcher
+// ---------------------------------------------------------------------------------------------
+using EmKernel = void (*)(const k::EmParams);
+
+template <int G>
+EmKernel em_for() { return k::em_refine_kernel<G>; }
+
+EmKernel em_kernel_for(int l) {
+    switch ((l + 1) / 2) {
+        case 1: return em_for<1>();
+        case 2: return em_for<2>();
+        case 3: return em_for<3>();
+        case 4: return em_for<4>();
+        case 5: return em_for<5>();
+        case 6: return em_for<6>();
+        case 7: return em_for<7>();
+        case 8: return em_for<8>();
+        case 9: return em_for<9>();
+        case 10: return em_for<10>();
+        case 11: return em_for<11>();
+        case 12: return em_for<12>();
+        case 13: return em_for<13>();
+        case 14: return em_for<14>();
+        case 15: return em_for<15>();
+        default: return em_for<16>();
+    }
+}
+
+size_t em_smem_bytes(int nwarps) {
+    size_t b = 0;
+    b += 128 * 4;                          // th
+    b += 256 * 4;                          // T
+    b += static_cast<size_t>(nwarps) * 128 * 4;  // part
+    b += 128 * 4;                          // rawm
+    b += static_cast<size_t>(nwarps) * 8;  // llpart
+    b += 8 * 8;                            // dscal
+    b += static_cast<size_t>(nwarps) * k::kCandCap * 8;  // cand_v
+    b += static_cast<size_t>(nwarps) * k::kCandCap * 4;  // cand_w
+    b += 128 * 4;                          // prof
+    b += 4 * 4;                            // iscal
+    b += 8;                                // cons_bits
+    return b + 16;
+}
+
+int em_warps_for(int t) {
+    if (t >= 64) return 8;
+    if (t % 5 == 0 && t % 4 != 0) return 5;
+    return 4;
+}
+
+struct EmOut {
+    int32_t* score = nullptr;
+    int32_t* iters = nullptr;
+    double* expct = nullptr;
+    uint64_t* cons = nullptr;
+    int32_t* pos = nullptr;
+    float* theta = nullptr;
+    double* ll = nullptr;
+};
+
+// scalars on the device: [0] iter_total (u64) [1] error flag (u32 in the low half)
+int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k::WorkDesc* work,
+              const unsigned int* n_work_dev, unsigned int n_work_host, unsigned int n_work_bound,
+              const unsigned int* members, const EmOut& o, unsigned long long* d_scal) {
+    k::EmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.seq_len = c->d_seq_len;
+    p.win_off = c->d_win_off;
+    p.seq_sym = c->d_seq_sym;
+    for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
+    p.tot_bases = static_cast<double>(c->total_bases);
+    p.t = c->t;
+    p.l = l;
+    p.max_iters = max_iters;
+    p.tol = tol;
+    const double eps = z_eps < 0.0 ? 9.313225746154785e-10 /* 2^-30 */ : z_eps;
+    p.z_eps = static_cast<float>(eps);
+    p.log_z_eps = eps > 0.0 ? static_cast<float>(std::log(eps)) : -INFINITY;
+    p.work = work;
+    p.n_work_dev = n_work_dev;
+    p.n_work = n_work_host;
+    p.members = members;
+    p.out_score = o.score;
+    p.out_iters = o.iters;
+    p.out_exp = o.expct;
+    p.out_cons = o.cons;
+    p.out_pos = o.pos;
+    p.out_theta = o.theta;
+    p.out_ll = o.ll;
+    p.iter_total = d_scal;
+    p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
+
+    const int nwarps = em_warps_for(c->t);
+    const int threads = nwarps * 32;
+    const size_t smem = em_smem_bytes(nwarps);
+    EmKernel kern = em_kernel_for(l);
+    int per_sm = 0;
+    PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    per_sm = std::max(per_sm, 1);
+    const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
+    const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
+    kern<<<grid, threads, smem, c->stream>>>(p);
+    return check_launch(c, "em_refine");
+}
+
+void unpack_consensus(uint64_t bits, int l, char* out) {
+    static const char sym[4] = {'A', 'C', 'T', 'G'};
+    for (int c = 0; c < l; ++c) out[c] = sym[(bits >> (62 - 2 * c)) & 3];
+    out[l] = '\0';
+}
+
+int pack_lmer(const char* v, int l, uint64_t* out) {
+    uint64_t bits = 0;
+    for (int c = 0; c < l; ++c) {
+        int r;
+        switch (v[c]) {
+            case 'A': r = 0; break;
+            case 'C': r = 1; break;
+            case 'T': r = 2; break;
+            case 'G': r = 3; break;
+            default:
+                return set_error(PM_ERR_UNKNOWN_SYMBOL, std::string("symbol '") + v[c] + "' is not in alphabet \"ACTG\"");
+        }
+        bits |= static_cast<uint64_t>(r) << (62 - 2 * c);
+    }
+    *out = bits;
+    return PM_OK;
+}
+
+int check_backend(int backend, int kk, uint64_t dense_cap) {
+    // projection.hpp:341-351: an explicit dense request above the cap is an error; results are
+    // otherwise backend-independent, and this build always sorts.
+    if (backend == PM_BACKEND_DENSE && pow4(kk) > dense_cap) {
+        return set_error(PM_ERR_DENSE_TABLE_TOO_LARGE, "dense backend would allocate " + std::to_string(pow4(kk)) +
+                                                           " buckets, above the cap of " + std::to_string(dense_cap) +
+                                                           "; use the grouped backend");
+    }
+    return PM_OK;
+}
+
+int check_plan_for_hash(pm_ctx* c, int l, const int32_t* kept, int kk) {
+    PM_TRY(need_sequences(c));
+    PM_TRY(validate_plan(l, kept, kk));
+    if (kk > 31) {
+        return set_error(PM_ERR_KMER_TOO_LONG, "projection width " + std::to_string(kk) +
+                                                   " exceeds the encodable k-mer length 31");  // projection.hpp:327-330
+    }
+    return prepare_windows(c, l);
+}
+
+struct StageTimer {
+    pm_ctx* c;
+    bool on;
+    double* acc;
+    cudaEvent_t a = nullptr, b = nullptr;
+    StageTimer(pm_ctx* ctx, bool enable, double* into) : c(ctx), on(enable), acc(into) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    void stop() {
+        if (on && a) {
+            cudaEventRecord(b, c->stream);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            *acc += ms;
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+            a = b = nullptr;
+        }
+    }
+    ~StageTimer() { stop(); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int pm_ctx_create(int device, void* stream, pm_ctx** out) {
+    clear_error();
+    if (out == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null output pointer");
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count < 1) {
+        return set_error(PM_ERR_NO_DEVICE, std::string("no CUDA device available (") +
+                                               (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0") +
+                                               "); libpm_b200 has no CPU fallback");
+    }
+    if (device < 0 || device >= count) return set_error(PM_ERR_NO_DEVICE, "CUDA device ordinal out of range");
+    cudaDeviceProp prop;
+    PM_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        return set_error(PM_ERR_NO_DEVICE, std::string("device '") + prop.name + "' is sm_" + std::to_string(prop.major) +
+                                               std::to_string(prop.minor) + "; this library is built for sm_100a only");
+    }
+    PM_CUDA(cudaSetDevice(device));
+    pm_ctx* c = new pm_ctx();
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->sm_count = prop.multiProcessorCount;
+    *out = c;
+    return PM_OK;
+}
+
+void pm_ctx_destroy(pm_ctx* c) {
+    if (c == nullptr) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf& b : c->buf) {
+        if (b.p) cudaFree(b.p);
+    }
+    cudaFree(c->d_words);
+    cudaFree(c->d_word_off);
+    cudaFree(c->d_seq_len);
+    cudaFree(c->d_seq_sym);
+    cudaFree(c->d_tot_sym);
+    cudaFree(c->d_win_off);
+    delete c;
+}
+
+int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t) {
+    clear_error();
+    if (c == nullptr || bases == nullptr || offs == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    if (t < 1) return set_error(PM_ERR_INVALID_PARAMS, "a sequence set needs at least one sequence");
+    for (int i = 0; i < t; ++i) {
+        if (offs[i + 1] <= offs[i]) return set_error(PM_ERR_INVALID_PARAMS, "sequence 'seq" + std::to_string(i + 1) + "' is empty");
+        if (offs[i + 1] - offs[i] > INT32_MAX) return set_error(PM_ERR_UNSUPPORTED, "sequence longer than 2^31-1 bases");
+    }
+    PM_CUDA(cudaSetDevice(c->device));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_words);
+    cudaFree(c->d_word_off);
+    cudaFree(c->d_seq_len);
+    cudaFree(c->d_seq_sym);
+    cudaFree(c->d_tot_sym);
+    cudaFree(c->d_win_off);
+    c->d_words = nullptr;
+    c->d_word_off = nullptr;
+    c->d_seq_len = nullptr;
+    c->d_seq_sym = nullptr;
+    c->d_tot_sym = nullptr;
+    c->d_win_off = nullptr;
+    c->t = 0;
+    c->win_l = 0;
+
+    const int64_t base0 = offs[0];
+    std::vector<int64_t> rel(static_cast<size_t>(t) + 1), word_off(static_cast<size_t>(t) + 1, 0);
+    std::vector<int32_t> len(static_cast<size_t>(t));
+    int64_t max_words = 0;
+    for (int i = 0; i <= t; ++i) rel[static_cast<size_t>(i)] = offs[i] - base0;
+    for (int i = 0; i < t; ++i) {
+        const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
+        len[static_cast<size_t>(i)] = static_cast<int32_t>(n);
+        const int64_t nw = (n + 31) / 32 + 1;  // +1 zero pad word: word a+1 of any window exists
+        word_off[static_cast<size_t>(i) + 1] = word_off[static_cast<size_t>(i)] + nw;
+        max_words = std::max(max_words, nw);
+    }
+    const int64_t total_bases = rel[static_cast<size_t>(t)];
+    const int64_t total_words = word_off[static_cast<size_t>(t)] + 2;
+
+    char* d_ascii = nullptr;
+    int64_t* d_offs = nullptr;
+    PM_TRY(get_buf(c, S_ASCII, static_cast<size_t>(total_bases), &d_ascii));
+    PM_TRY(get_buf(c, S_OFFS, static_cast<size_t>(t) + 1, &d_offs));
+    PM_CUDA(cudaMalloc(&c->d_words, sizeof(uint64_t) * static_cast<size_t>(total_words)));
+    PM_CUDA(cudaMalloc(&c->d_word_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
+    PM_CUDA(cudaMalloc(&c->d_seq_len, sizeof(int32_t) * static_cast<size_t>(t)));
+    PM_CUDA(cudaMalloc(&c->d_seq_sym, sizeof(unsigned int) * 4 * static_cast<size_t>(t)));
+    PM_CUDA(cudaMalloc(&c->d_tot_sym, sizeof(unsigned long long) * 8));
+    PM_CUDA(cudaMalloc(&c->d_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
+    PM_CUDA(cudaMemcpyAsync(d_ascii, bases + base0, static_cast<size_t>(total_bases), cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemcpyAsync(d_offs, rel.data(), sizeof(int64_t) * rel.size(), cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemcpyAsync(c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size(), cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemcpyAsync(c->d_seq_len, len.data(), sizeof(int32_t) * len.size(), cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * static_cast<size_t>(total_words), c->stream));
+    PM_CUDA(cudaMemsetAsync(c->d_seq_sym, 0, sizeof(unsigned int) * 4 * static_cast<size_t>(t), c->stream));
+    PM_CUDA(cudaMemsetAsync(c->d_tot_sym, 0, sizeof(unsigned long long) * 4, c->stream));
+    PM_CUDA(cudaMemsetAsync(c->d_tot_sym + 4, 0xFF, sizeof(unsigned long long), c->stream));
+
+    const int warps_per_block = 8;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((max_words + warps_per_block - 1) / warps_per_block, 65535)),
+                    static_cast<unsigned>(std::min(t, 65535)));
+    k::encode_kernel<<<grid, warps_per_block * 32, 0, c->stream>>>(d_ascii, d_offs, c->d_word_off, t, c->d_words,
+                                                                 c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
+    PM_TRY(check_launch(c, "encode"));
+    unsigned long long host_tot[5];
+    PM_CUDA(cudaMemcpyAsync(host_tot, c->d_tot_sym, sizeof(host_tot), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    if (host_tot[4] != ULLONG_MAX) {
+        const int64_t bad = static_cast<int64_t>(host_tot[4]);
+        int seq = 0;
+        while (seq + 1 < t && rel[static_cast<size_t>(seq) + 1] <= bad) ++seq;
+        return set_error(PM_ERR_UNKNOWN_SYMBOL, std::string("symbol '") + bases[base0 + bad] + "' in sequence 'seq" +
+                                                    std::to_string(seq + 1) + "' is not in alphabet \"ACTG\"");
+    }
+    for (int r = 0; r < 4; ++r) c->tot_sym[r] = host_tot[r];
+    c->t = t;
+    c->offs = rel;
+    c->word_off = word_off;
+    c->seq_len = len;
+    c->total_bases = total_bases;
+    c->total_words = total_words;
+    return PM_OK;
+}
+
+int pm_ctx_num_sequences(const pm_ctx* c) { return c ? c->t : 0; }
+
+int64_t pm_ctx_total_lmers(const pm_ctx* c, int l) {
+    if (c == nullptr || c->t < 1) return -1;
+    int64_t x = 0;
+    for (int i = 0; i < c->t; ++i) {
+        const int64_t w = c->seq_len[static_cast<size_t>(i)] - l + 1;
+        if (l < 1 || w < 1) return -1;
+        x += w;
+    }
+    return x;
+}
+
+int pm_ctx_packed_words(pm_ctx* c, uint64_t* words_out, int64_t* word_off_out, int64_t cap_words) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    const int64_t n = c->word_off[static_cast<size_t>(c->t)];
+    if (cap_words < n) return set_error(PM_ERR_INVALID_PARAMS, "output buffer too small for the packed words");
+    PM_CUDA(cudaSetDevice(c->device));
+    PM_CUDA(cudaMemcpyAsync(words_out, c->d_words, sizeof(uint64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    std::memcpy(word_off_out, c->word_off.data(), sizeof(int64_t) * c->word_off.size());
+    return PM_OK;
+}
+
+int pm_ctx_symbol_counts(pm_ctx* c, int64_t* counts4) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    for (int r = 0; r < 4; ++r) counts4[r] = static_cast<int64_t>(c->tot_sym[r]);
+    return PM_OK;
+}
+
+int pm_ctx_synchronize(pm_ctx* c) {
+    clear_error();
+    if (c == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null context");
+    PM_CUDA(cudaSetDevice(c->device));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    return PM_OK;
+}
+
+int64_t pm_ctx_launch_count(const pm_ctx* c) { return c ? c->launches : 0; }
+
+// ------------------------------------------------------------------------------------------------
+// stage entry points
+// ------------------------------------------------------------------------------------------------
+int pm_hash_keys(pm_ctx* c, int l, const int32_t* kept, int kk, uint64_t* keys_out) {
+    clear_error();
+    PM_TRY(check_plan_for_hash(c, l, kept, kk));
+    PM_CUDA(cudaSetDevice(c->device));
+    const std::vector<k::PlanProg> progs(1, make_prog(kept, kk));
+    uint64_t* keys = nullptr;
+    PM_TRY(get_buf(c, S_KEYS_A, static_cast<size_t>(c->x), &keys));
+    PM_TRY(project_keys<uint64_t>(c, progs, keys));
+    PM_CUDA(cudaMemcpyAsync(keys_out, keys, sizeof(uint64_t) * static_cast<size_t>(c->x), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    return PM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// hash_trial + bucket listing for one plan.  thr = 1 lists every bucket (hash_trial); order_by_size
+// additionally applies the enriched_buckets ordering on the device.
+template <typename KeyT>
+int stage_buckets(pm_ctx* c, const int32_t* kept, int kk, int thr, bool order_by_size, std::vector<uint64_t>* keys,
+                  std::vector<uint32_t>* starts, std::vector<uint32_t>* sizes, std::vector<uint32_t>* sorted_idx) {
+    const std::vector<k::PlanProg> progs(1, make_prog(kept, kk));
+    Sorted<KeyT> srt;
+    PM_TRY(hash_and_sort<KeyT>(c, progs, 2 * kk, &srt));
+    Records rec;
+    PM_TRY(find_enriched<KeyT>(c, srt, 1, thr, &rec));
+    unsigned int n_rec = 0;
+    PM_CUDA(cudaMemcpyAsync(&n_rec, rec.n_rec, sizeof(n_rec), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    const size_t ne = n_rec;
+    std::vector<uint32_t> order(ne);
+    for (size_t i = 0; i < ne; ++i) order[i] = static_cast<uint32_t>(i);
+    if (order_by_size && ne > 1) {
+        // stable sort of the records by (x - size): equal sizes keep their ascending-key order
+        unsigned int *ka, *kb, *ia, *ib;
+        PM_TRY(get_buf(c, S_TMP_A, static_cast<size_t>(rec.cap_e), &ka));
+        PM_TRY(get_buf(c, S_TMP_B, static_cast<size_t>(rec.cap_e), &kb));
+        PM_TRY(get_buf(c, S_TMP_C, static_cast<size_t>(rec.cap_e), &ia));
+        PM_TRY(get_buf(c, S_TMP_D, static_cast<size_t>(rec.cap_e), &ib));
+        const unsigned gx = static_cast<unsigned>(std::min<int64_t>((rec.cap_e + 255) / 256, 1024));
+        k::size_keys_kernel<<<dim3(gx, 1), 256, 0, c->stream>>>(rec.size, rec.n_rec, rec.cap_e,
+                                                              static_cast<unsigned int>(c->x), 1, ka);
+        PM_TRY(check_launch(c, "size_keys"));
+        int bits = 1;
+        while ((static_cast<uint64_t>(c->x) >> bits) != 0) ++bits;
+        unsigned int* ko;
+        unsigned int* io;
+        PM_TRY((sort_segments<unsigned int>(c, ka, kb, ia, ib, 1, rec.cap_e, rec.cap_e, rec.n_rec, bits, &ko, &io)));
+        PM_CUDA(cudaMemcpyAsync(order.data(), io, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<uint64_t> hk(ne);
+    std::vector<uint32_t> hs(ne), hz(ne);
+    sorted_idx->resize(static_cast<size_t>(c->x));
+    PM_CUDA(cudaMemcpyAsync(hk.data(), rec.key, sizeof(uint64_t) * ne, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(hs.data(), rec.start, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(hz.data(), rec.size, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(sorted_idx->data(), srt.idx, sizeof(uint32_t) * static_cast<size_t>(c->x), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    keys->resize(ne);
+    starts->resize(ne);
+    sizes->resize(ne);
+    for (size_t i = 0; i < ne; ++i) {
+        (*keys)[i] = hk[order[i]];
+        (*starts)[i] = hs[order[i]];
+        (*sizes)[i] = hz[order[i]];
+    }
+    return PM_OK;
+}
+
+int stage_buckets_any(pm_ctx* c, const int32_t* kept, int kk, int thr, bool order_by_size, std::vector<uint64_t>* keys,
+                      std::vector<uint32_t>* starts, std::vector<uint32_t>* sizes, std::vector<uint32_t>* sorted_idx) {
+    if (2 * kk <= 32) return stage_buckets<uint32_t>(c, kept, kk, thr, order_by_size, keys, starts, sizes, sorted_idx);
+    return stage_buckets<uint64_t>(c, kept, kk, thr, order_by_size, keys, starts, sizes, sorted_idx);
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_hash_trial(pm_ctx* c, int l, const int32_t* kept, int kk, int backend, uint64_t dense_table_cap,
+                  int64_t* n_buckets, uint64_t* bucket_keys, int32_t* bucket_sizes, int32_t* members) {
+    clear_error();
+    PM_TRY(check_plan_for_hash(c, l, kept, kk));
+    PM_TRY(check_backend(backend, kk, dense_table_cap));
+    PM_CUDA(cudaSetDevice(c->device));
+    std::vector<uint64_t> keys;
+    std::vector<uint32_t> starts, sizes, idx;
+    PM_TRY(stage_buckets_any(c, kept, kk, 1, false, &keys, &starts, &sizes, &idx));
+    *n_buckets = static_cast<int64_t>(keys.size());
+    for (size_t b = 0; b < keys.size(); ++b) {
+        bucket_keys[b] = keys[b];
+        bucket_sizes[b] = static_cast<int32_t>(sizes[b]);
+    }
+    for (size_t i = 0; i < idx.size(); ++i) members[i] = static_cast<int32_t>(idx[i]);
+    return PM_OK;
+}
+
+int pm_enriched_buckets(pm_ctx* c, int l, const int32_t* kept, int kk, int s, int r_cap, int64_t* n_enriched,
+                        uint64_t* keys_out, int32_t* sizes_pre, int32_t* overflowed, int64_t* mem_off, int32_t* members) {
+    clear_error();
+    PM_TRY(check_plan_for_hash(c, l, kept, kk));
+    if (s < 1 || r_cap < s) return set_error(PM_ERR_INVALID_PARAMS, "enriched buckets need s >= 1 and r_cap >= s");
+    PM_CUDA(cudaSetDevice(c->device));
+    std::vector<uint64_t> keys;
+    std::vector<uint32_t> starts, sizes, idx;
+    PM_TRY(stage_buckets_any(c, kept, kk, s, true, &keys, &starts, &sizes, &idx));
+    *n_enriched = static_cast<int64_t>(keys.size());
+    int64_t pos = 0;
+    for (size_t b = 0; b < keys.size(); ++b) {
+        keys_out[b] = keys[b];
+        sizes_pre[b] = static_cast<int32_t>(sizes[b]);
+        overflowed[b] = sizes[b] > static_cast<uint32_t>(r_cap) ? 1 : 0;
+        const uint32_t take = std::min(sizes[b], static_cast<uint32_t>(r_cap));
+        mem_off[b] = pos;
+        for (uint32_t m = 0; m < take; ++m) members[pos++] = static_cast<int32_t>(idx[starts[b] + m]);
+    }
+    mem_off[keys.size()] = pos;
+    return PM_OK;
+}
+
+int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
+              double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
+              int32_t* iterations, float* theta, double* ll_trace) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    PM_TRY(prepare_windows(c, l));
+    if (max_iters < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one EM iteration");
+    if (n_buckets < 1) return PM_OK;
+    PM_CUDA(cudaSetDevice(c->device));
+    const int64_t n_mem = mem_off[n_buckets];
+    std::vector<k::WorkDesc> work(static_cast<size_t>(n_buckets));
+    for (int b = 0; b < n_buckets; ++b) {
+        const int64_t cnt = mem_off[b + 1] - mem_off[b];
+        if (cnt < 1) return set_error(PM_ERR_EMPTY_BUCKET, "cannot build a motif model from an empty bucket");
+        work[static_cast<size_t>(b)].mem_begin = mem_off[b];
+        work[static_cast<size_t>(b)].key = 0;
+        work[static_cast<size_t>(b)].count = static_cast<unsigned int>(cnt);
+        work[static_cast<size_t>(b)].trial = b;
+    }
+    for (int64_t i = 0; i < n_mem; ++i) {
+        if (members[i] < 0 || members[i] >= c->x) return set_error(PM_ERR_INDEX_OUT_OF_RANGE, "member l-mer index out of range");
+    }
+    const size_t nb = static_cast<size_t>(n_buckets);
+    unsigned int* d_mem;
+    k::WorkDesc* d_work;
+    unsigned long long* d_scal;
+    EmOut o;
+    PM_TRY(get_buf(c, S_MEMBERS, static_cast<size_t>(n_mem), &d_mem));
+    PM_TRY(get_buf(c, S_WORK, nb, &d_work));
+    PM_TRY(get_buf(c, S_SCAL, 4, &d_scal));
+    PM_TRY(get_buf(c, S_OUT_SCORE, nb, &o.score));
+    PM_TRY(get_buf(c, S_OUT_ITERS, nb, &o.iters));
+    PM_TRY(get_buf(c, S_OUT_EXP, nb, &o.expct));
+    PM_TRY(get_buf(c, S_OUT_CONS, nb, &o.cons));
+    PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
+    if (theta) PM_TRY(get_buf(c, S_OUT_THETA, nb * 4 * static_cast<size_t>(l + 1), &o.theta));
+    if (ll_trace) {
+        PM_TRY(get_buf(c, S_OUT_LL, nb * static_cast<size_t>(max_iters), &o.ll));
+        std::vector<double> nan_fill(nb * static_cast<size_t>(max_iters), std::numeric_limits<double>::quiet_NaN());
+        PM_CUDA(cudaMemcpyAsync(o.ll, nan_fill.data(), sizeof(double) * nan_fill.size(), cudaMemcpyHostToDevice, c->stream));
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    PM_CUDA(cudaMemcpyAsync(d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem), cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(k::WorkDesc) * nb, cudaMemcpyHostToDevice, c->stream));
+    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
+    PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
+                     static_cast<unsigned int>(n_buckets), d_mem, o, d_scal));
+    std::vector<int32_t> hs(nb), hi(nb);
+    std::vector<double> he(nb);
+    std::vector<uint64_t> hc(nb);
+    unsigned long long scal[2];
+    PM_CUDA(cudaMemcpyAsync(hs.data(), o.score, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(hi.data(), o.iters, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(he.data(), o.expct, sizeof(double) * nb, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(hc.data(), o.cons, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaMemcpyAsync(scal, d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c->stream));
+    if (positions) PM_CUDA(cudaMemcpyAsync(positions, o.pos, sizeof(int32_t) * nb * static_cast<size_t>(c->t), cudaMemcpyDeviceToHost, c->stream));
+    if (theta) PM_CUDA(cudaMemcpyAsync(theta, o.theta, sizeof(float) * nb * 4 * static_cast<size_t>(l + 1), cudaMemcpyDeviceToHost, c->stream));
+    if (ll_trace) PM_CUDA(cudaMemcpyAsync(ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    if ((scal[1] & 0xFFFFFFFFULL) != 0) {
+        return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
+    }
+    for (size_t b = 0; b < nb; ++b) {
+        if (score) score[b] = hs[b];
+        if (iterations) iterations[b] = hi[b];
+        if (expectation) expectation[b] = he[b];
+        if (consensus) unpack_consensus(hc[b], l, consensus + 32 * b);
+    }
+    return PM_OK;
+}
+
+int pm_score(pm_ctx* c, int l, const int32_t* starts, int* score, char* consensus) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    PM_TRY(prepare_windows(c, l));
+    std::vector<int32_t> s0(static_cast<size_t>(c->t));
+    for (int i = 0; i < c->t; ++i) {
+        if (starts[i] < 1 || starts[i] + l - 1 > c->seq_len[static_cast<size_t>(i)]) {
+            return set_error(PM_ERR_INDEX_OUT_OF_RANGE, "l-mer (i=" + std::to_string(i + 1) + ", j=" + std::to_string(starts[i]) +
+                                                            ", l=" + std::to_string(l) + ") is out of range");
+        }
+        s0[static_cast<size_t>(i)] = starts[i] - 1;
+    }
+    PM_CUDA(cudaSetDevice(c->device));
+    int32_t* d_starts;
+    unsigned long long* d_out;
+    PM_TRY(get_buf(c, S_TMP_A, static_cast<size_t>(c->t), &d_starts));
+    PM_TRY(get_buf(c, S_SCAL, 4, &d_out));
+    PM_CUDA(cudaMemcpyAsync(d_starts, s0.data(), sizeof(int32_t) * s0.size(), cudaMemcpyHostToDevice, c->stream));
+    k::score_kernel<<<1, 256, 0, c->stream>>>(c->d_words, c->d_word_off, c->t, l, d_starts,
+                                            reinterpret_cast<int32_t*>(d_out), reinterpret_cast<uint64_t*>(d_out + 1));
+    PM_TRY(check_launch(c, "score"));
+    unsigned long long h[2];
+    PM_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    *score = static_cast<int>(h[0] & 0xFFFFFFFFULL);
+    unpack_consensus(h[1], l, consensus);
+    return PM_OK;
+}
+
+int pm_hamming_scan(pm_ctx* c, const char* v, int l, int d, int32_t* per_seq_min, int* total_distance, int* within_d) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    PM_TRY(prepare_windows(c, l));
+    uint64_t cand = 0;
+    PM_TRY(pack_lmer(v, l, &cand));
+    PM_CUDA(cudaSetDevice(c->device));
+    int32_t* d_min;
+    PM_TRY(get_buf(c, S_TMP_A, static_cast<size_t>(c->t), &d_min));
+    const int threads = 256;
+    const int blocks = std::max(1, std::min((c->t * 32 + threads - 1) / threads, c->sm_count * 8));
+    k::hamming_scan_kernel<<<blocks, threads, 0, c->stream>>>(c->d_words, c->d_word_off, c->d_seq_len, c->t, l, cand, d_min);
+    PM_TRY(check_launch(c, "hamming_scan"));
+    std::vector<int32_t> h(static_cast<size_t>(c->t));
+    PM_CUDA(cudaMemcpyAsync(h.data(), d_min, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    int tot = 0, within = 0;
+    for (int i = 0; i < c->t; ++i) {
+        tot += h[static_cast<size_t>(i)];
+        within += h[static_cast<size_t>(i)] <= d ? 1 : 0;
+        if (per_seq_min) per_seq_min[i] = h[static_cast<size_t>(i)];
+    }
+    if (total_distance) *total_distance = tot;
+    if (within_d) *within_d = within;
+    return PM_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// run(), driver.hpp:145-220
+// ------------------------------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+struct TrialSummary {  // device layout of S_TB: parallel arrays would need 6 copies; one struct, one copy
+    int32_t work;      // -1 when the trial has no enriched bucket
+    int32_t score;
+    int32_t iters;
+    int32_t pad;
+    double expct;
+    uint64_t key;
+    uint64_t cons;
+};
+
+__global__ void summarize_kernel(const int32_t* __restrict__ best_work, const k::WorkDesc* __restrict__ work,
+                                 const int32_t* __restrict__ score, const int32_t* __restrict__ iters,
+                                 const double* __restrict__ expct, const uint64_t* __restrict__ cons, int n_trials,
+                                 TrialSummary* __restrict__ out) {
+    const int tr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tr >= n_trials) return;
+    TrialSummary s;
+    s.work = best_work[tr];
+    s.pad = 0;
+    if (s.work >= 0) {
+        s.score = score[s.work];
+        s.iters = iters[s.work];
+        s.expct = expct[s.work];
+        s.key = work[s.work].key;
+        s.cons = cons[s.work];
+    } else {
+        s.score = -1;
+        s.iters = 0;
+        s.expct = 0.0;
+        s.key = 0;
+        s.cons = 0;
+    }
+    out[tr] = s;
+}
+
+struct RunState {
+    bool have_best = false;
+    TrialSummary best{};
+    int64_t best_trial = 0;
+    std::vector<int32_t> positions;
+};
+
+template <typename KeyT>
+int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
+              int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
+              int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key, int64_t out_base) {
+    const int n_trials = static_cast<int>(progs.size());
+    const int l = cfg->l;
+    const bool prof = cfg->profile != 0;
+    const int r_cap = c->t * params.s;
+    Sorted<KeyT> srt;
+    Records rec;
+    {
+        StageTimer tk(c, prof, &out->stage_ms[0]);
+        const size_t n = progs.size() * static_cast<size_t>(c->x);
+        KeyT *ka, *kb;
+        unsigned int *ia, *ib;
+        PM_TRY(get_buf(c, S_KEYS_A, n, &ka));
+        PM_TRY(get_buf(c, S_KEYS_B, n, &kb));
+        PM_TRY(get_buf(c, S_IDX_A, n, &ia));
+        PM_TRY(get_buf(c, S_IDX_B, n, &ib));
+        PM_TRY(project_keys<KeyT>(c, progs, ka));
+        tk.stop();
+        StageTimer ts(c, prof, &out->stage_ms[1]);
+        PM_TRY((sort_segments<KeyT>(c, ka, kb, ia, ib, n_trials, c->x, c->x, nullptr, 2 * params.k, &srt.keys, &srt.idx)));
+    }
+    unsigned int* work_off;
+    k::WorkDesc* work;
+    {
+        StageTimer te(c, prof, &out->stage_ms[2]);
+        PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
+        PM_TRY(get_buf(c, S_WORK_OFF, static_cast<size_t>(n_trials) + 1, &work_off));
+        PM_TRY(get_buf(c, S_WORK, static_cast<size_t>(n_trials) * static_cast<size_t>(rec.cap_e), &work));
+        k::work_scan_kernel<<<1, 1024, 0, c->stream>>>(rec.n_rec, n_trials, work_off);
+        PM_TRY(check_launch(c, "work_scan"));
+        const unsigned gx = static_cast<unsigned>(std::min<int64_t>((rec.cap_e + 127) / 128, 64));
+        k::build_work_kernel<<<dim3(std::max(gx, 1u), static_cast<unsigned>(n_trials)), 128, 0, c->stream>>>(
+            rec.n_rec, work_off, rec.key, rec.start, rec.size, c->x, rec.cap_e, r_cap, n_trials, work);
+        PM_TRY(check_launch(c, "build_work"));
+    }
+    const size_t nb = static_cast<size_t>(n_trials) * static_cast<size_t>(rec.cap_e);
+    EmOut o;
+    unsigned long long* d_scal;
+    int32_t* best_work;
+    TrialSummary* d_tb;
+    PM_TRY(get_buf(c, S_OUT_SCORE, nb, &o.score));
+    PM_TRY(get_buf(c, S_OUT_ITERS, nb, &o.iters));
+    PM_TRY(get_buf(c, S_OUT_EXP, nb, &o.expct));
+    PM_TRY(get_buf(c, S_OUT_CONS, nb, &o.cons));
+    PM_TRY(get_buf(c, S_SCAL, 4, &d_scal));
+    PM_TRY(get_buf(c, S_BEST, static_cast<size_t>(n_trials), &best_work));
+    PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
+    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
+    {
+        StageTimer tm(c, prof, &out->stage_ms[3]);
+        PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work, work_off + n_trials, 0,
+                         static_cast<unsigned int>(std::min<size_t>(nb, 1u << 30)), srt.idx, o, d_scal));
+    }
+    std::vector<TrialSummary> tb(static_cast<size_t>(n_trials));
+    std::vector<unsigned int> n_rec(static_cast<size_t>(n_trials));
+    unsigned long long scal[2];
+    {
+        StageTimer tr(c, prof, &out->stage_ms[4]);
+        const int warps_per_block = 8;
+        k::trial_best_kernel<<<(n_trials + warps_per_block - 1) / warps_per_block, warps_per_block * 32, 0, c->stream>>>(
+            work_off, work, o.score, o.expct, n_trials, best_work);
+        PM_TRY(check_launch(c, "trial_best"));
+        summarize_kernel<<<(n_trials + 127) / 128, 128, 0, c->stream>>>(best_work, work, o.score, o.iters, o.expct, o.cons,
+                                                                      n_trials, d_tb);
+        PM_TRY(check_launch(c, "summarize"));
+    }
+    {
+        StageTimer td(c, prof, &out->stage_ms[7]);
+        PM_CUDA(cudaMemcpyAsync(tb.data(), d_tb, sizeof(TrialSummary) * tb.size(), cudaMemcpyDeviceToHost, c->stream));
+        PM_CUDA(cudaMemcpyAsync(n_rec.data(), rec.n_rec, sizeof(unsigned int) * n_rec.size(), cudaMemcpyDeviceToHost, c->stream));
+        PM_CUDA(cudaMemcpyAsync(scal, d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c->stream));
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if ((scal[1] & 0xFFFFFFFFULL) != 0) {
+        return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
+    }
+    out->em_lookup_adds += static_cast<int64_t>(scal[0]) * c->x * l;
+
+    // Ascending-trial reduction, driver.hpp:195-208.
+    const int perfect = l * c->t;
+    int32_t new_best_work = -1;
+    for (int i = 0; i < n_trials; ++i) {
+        const int64_t trial = first_trial + i;
+        const TrialSummary& s = tb[static_cast<size_t>(i)];
+        out->trials_run = trial;
+        out->buckets_enriched += n_rec[static_cast<size_t>(i)];
+        const size_t oi = static_cast<size_t>(out_base + i);
+        if (trial_buckets) trial_buckets[oi] = n_rec[static_cast<size_t>(i)];
+        if (trial_best_score) trial_best_score[oi] = s.score;
+        if (trial_best_expectation) trial_best_expectation[oi] = s.expct;
+        if (trial_best_key) trial_best_key[oi] = s.key;
+        if (s.work >= 0 && (!st->have_best || pm_candidate_improves(s.score, s.expct, s.key, st->best.score,
+                                                                    st->best.expct, st->best.key))) {
+            st->have_best = true;
+            st->best = s;
+            st->best_trial = trial;
+            new_best_work = s.work;
+        }
+        if (cfg->early_stop && st->have_best && st->best.score == perfect) {
+            *stop = true;
+            break;
+        }
+    }
+    if (new_best_work >= 0) {
+        // Positions of the new incumbent: re-run its bucket alone with the position output on.
+        // Same kernel, same launch shape per CTA, deterministic => identical candidate.
+        EmOut o1;
+        PM_TRY(get_buf(c, S_TMP_A, 16, &o1.score));
+        o1.iters = o1.score + 4;
+        PM_TRY(get_buf(c, S_TMP_B, 4, &o1.expct));
+        PM_TRY(get_buf(c, S_TMP_C, 4, &o1.cons));
+        PM_TRY(get_buf(c, S_OUT_POS, static_cast<size_t>(c->t), &o1.pos));
+        unsigned long long* d_scal2;
+        PM_TRY(get_buf(c, S_TMP_D, 4, &d_scal2));
+        PM_CUDA(cudaMemsetAsync(d_scal2, 0, sizeof(unsigned long long) * 4, c->stream));
+        PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work + new_best_work, nullptr, 1, 1, srt.idx,
+                         o1, d_scal2));
+        st->positions.resize(static_cast<size_t>(c->t));
+        PM_CUDA(cudaMemcpyAsync(st->positions.data(), o1.pos, sizeof(int32_t) * static_cast<size_t>(c->t), cudaMemcpyDeviceToHost, c->stream));
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return PM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* positions, int64_t* trial_buckets,
+           int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key) {
+    const auto t0 = std::chrono::steady_clock::now();
+    clear_error();
+    if (cfg == nullptr || out == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    PM_TRY(need_sequences(c));
+    std::memset(out, 0, sizeof(*out));
+    PM_TRY(pm_resolve_params(cfg, c->offs.data(), c->t, out));
+    const pm_run_result params = *out;
+    PM_TRY(prepare_windows(c, cfg->l));
+    if (params.k > 31) {
+        return set_error(PM_ERR_KMER_TOO_LONG, "projection width " + std::to_string(params.k) +
+                                                   " exceeds the encodable k-mer length 31");
+    }
+    PM_TRY(check_backend(cfg->backend, params.k, cfg->dense_table_cap));
+    if (cfg->max_em_iters < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one EM iteration");
+    const int64_t r_cap = static_cast<int64_t>(c->t) * params.s;
+    if (r_cap > INT32_MAX) return set_error(PM_ERR_UNSUPPORTED, "t*s exceeds 2^31-1");
+    PM_CUDA(cudaSetDevice(c->device));
+    const int64_t launches0 = c->launches;
+
+    int64_t tb = cfg->trial_begin, te = cfg->trial_end;
+    if (tb == 0 && te == 0) {
+        tb = 1;
+        te = params.m;
+    }
+    if (tb < 1 || te > params.m || tb > te + 1) return set_error(PM_ERR_INVALID_PARAMS, "trial range must lie within 1..m");
+
+    // batch size: bounded by a workspace budget (worst-case per-trial footprint)
+    const int key_bytes = 2 * params.k <= 32 ? 4 : 8;
+    const int64_t cap_e = std::max<int64_t>(1, c->x / params.s);
+    const int64_t tiles = (c->x + k::kSortTile - 1) / k::kSortTile;
+    const double per_trial = static_cast<double>(c->x) * (2.0 * key_bytes + 8.0) + 1024.0 * static_cast<double>(tiles) +
+                             static_cast<double>(cap_e) * (16.0 + sizeof(k::WorkDesc) + 24.0) + 64.0;
+    int64_t batch = cfg->batch_trials > 0 ? cfg->batch_trials
+                                          : static_cast<int64_t>(std::max(1.0, std::floor(3.0e9 / per_trial)));
+    batch = std::max<int64_t>(1, std::min<int64_t>(batch, 32768));
+
+    RunState st;
+    bool stop = false;
+    std::vector<int32_t> kept(static_cast<size_t>(params.k));
+    for (int64_t first = tb; first <= te && !stop; first += batch) {
+        const int64_t last = std::min(te, first + batch - 1);
+        std::vector<k::PlanProg> progs;
+        progs.reserve(static_cast<size_t>(last - first + 1));
+        for (int64_t trial = first; trial <= last; ++trial) {
+            const int32_t* plan;
+            if (cfg->forced_kept != nullptr) {
+                plan = cfg->forced_kept;
+            } else if (cfg->plans != nullptr) {
+                plan = cfg->plans + (trial - 1) * params.k;
+                PM_TRY(validate_plan(cfg->l, plan, params.k));
+            } else {
+                PM_TRY(pm_trial_plan(cfg->l, params.k, cfg->seed, trial, kept.data()));
+                plan = kept.data();
+            }
+            progs.push_back(make_prog(plan, params.k));
+        }
+        const int rc = key_bytes == 4
+                           ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
+                                                 trial_best_expectation, trial_best_key, first - tb)
+                           : run_batch<uint64_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
+                                                 trial_best_expectation, trial_best_key, first - tb);
+        if (rc != PM_OK) return rc;
+    }
+
+    out->gpu_launches = c->launches - launches0;
+    out->found = st.have_best ? 1 : 0;
+    if (!st.have_best) {
+        out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return set_error(PM_ERR_NO_ENRICHED_BUCKETS, "no bucket reached s=" + std::to_string(params.s) + " in " +
+                                                         std::to_string(out->trials_run) + " trials; lower s or raise m");
+    }
+    unpack_consensus(st.best.cons, cfg->l, out->consensus);
+    out->score = st.best.score;
+    out->iterations = st.best.iters;
+    out->expectation = st.best.expct;
+    out->source_bucket = st.best.key;
+    out->best_trial = st.best_trial;
+    if (positions) std::memcpy(positions, st.positions.data(), sizeof(int32_t) * static_cast<size_t>(c->t));
+    {
+        // XOR/popcount scoring of the reported consensus (north_star "Scoring")
+        StageTimer tsc(c, cfg->profile != 0, &out->stage_ms[5]);
+        int tot = 0, within = 0;
+        PM_TRY(pm_hamming_scan(c, out->consensus, cfg->l, cfg->d, nullptr, &tot, &within));
+        out->total_distance = tot;
+        out->within_d = within;
+    }
+    out->gpu_launches = c->launches - launches0;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return PM_OK;
+}
+
+int pm_run_host(pm_ctx* c, const pm_run_config* cfg, const char* bases, const int64_t* offs, int t, pm_run_result* out,
+                int32_t* positions) {
+    const auto t0 = std::chrono::steady_clock::now();
+    double up_ms = 0.0;
+    {
+        const auto a = std::chrono::steady_clock::now();
+        PM_TRY(pm_ctx_set_sequences(c, bases, offs, t));
+        up_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+    }
+    const int64_t launches0 = c->launches - 1;
+    const int rc = pm_run(c, cfg, out, positions, nullptr, nullptr, nullptr, nullptr);
+    out->stage_ms[6] = up_ms;
+    out->gpu_launches = c->launches - launches0;
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+}  // extern "C"

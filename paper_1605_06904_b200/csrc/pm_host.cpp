@@ -1,0 +1,352 @@
+// pm_host.cpp — host-side logic of libpm_b200.so that never touches the GPU:
+// status/error plumbing, the projection-plan PRNG stream, the parameter formulas,
+// resolve_params and the multi-GPU result merge.  (SURVEY.md §8a rows 3, 13, 14.)
+//
+// The plan stream must be bit-exact with the reference, so it uses the same standard engine
+// (std::mt19937_64, rng.hpp:32) and the same rejection rule (rng.hpp:37-50); plans are sampled on
+// the host and shipped to the device as constant-memory extraction programs (paper: "RNG on
+// host").
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "pm_internal.hpp"
+
+namespace pm {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+void clear_error() { g_last_error.clear(); }
+
+uint64_t pow4(int k) {
+    if (k >= 32) return std::numeric_limits<uint64_t>::max();
+    return 1ULL << (2 * k);
+}
+
+int validate_plan(int l, const int32_t* kept, int k) {
+    if (l < 1) return set_error(PM_ERR_INVALID_PARAMS, "projection source length must be positive, got " + std::to_string(l));
+    if (k < 1 || k > l || kept == nullptr) {
+        return set_error(PM_ERR_INVALID_PARAMS, "projection must keep between 1 and l positions, got " +
+                                                    std::to_string(k) + " of l=" + std::to_string(l));
+    }
+    int prev = 0;
+    for (int i = 0; i < k; ++i) {
+        if (kept[i] <= prev || kept[i] > l) {
+            return set_error(PM_ERR_INVALID_PARAMS,
+                             "kept positions must be strictly increasing within [1," + std::to_string(l) + "]");
+        }
+        prev = kept[i];
+    }
+    return PM_OK;
+}
+
+namespace {
+
+// Unbiased draw below n by rejecting the low tail 2^64 mod n (rng.hpp:37-50).
+uint64_t draw_below(std::mt19937_64& eng, uint64_t n) {
+    if (n == 1) return 0;
+    const uint64_t low_tail = (0 - n) % n;
+    uint64_t x = eng();
+    while (x < low_tail) x = eng();
+    return x % n;
+}
+
+// sample_plan (projection.hpp:210-226): draw l-k distinct excluded positions by a partial
+// Fisher-Yates over 1..l (rng.hpp:62-73); the plan is the sorted complement.
+int plan_from_engine(int l, int k, std::mt19937_64& eng, int32_t* kept) {
+    if (k < 1 || k > l) {
+        return set_error(PM_ERR_INVALID_PARAMS,
+                         "plan needs 1 <= k <= l, got k=" + std::to_string(k) + ", l=" + std::to_string(l));
+    }
+    std::vector<int> pool(static_cast<size_t>(l));
+    for (int i = 0; i < l; ++i) pool[static_cast<size_t>(i)] = i + 1;
+    const int drop = l - k;
+    for (int i = 0; i < drop; ++i) {
+        const int j = i + static_cast<int>(draw_below(eng, static_cast<uint64_t>(l - i)));
+        std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+    }
+    std::vector<char> dropped(static_cast<size_t>(l) + 1, 0);
+    for (int i = 0; i < drop; ++i) dropped[static_cast<size_t>(pool[static_cast<size_t>(i)])] = 1;
+    int n = 0;
+    for (int p = 1; p <= l; ++p) {
+        if (!dropped[static_cast<size_t>(p)]) kept[n++] = p;
+    }
+    return PM_OK;
+}
+
+int64_t total_windows(const int64_t* offs, int t, int l) {
+    int64_t x = 0;
+    for (int i = 0; i < t; ++i) {
+        const int64_t w = (offs[i + 1] - offs[i]) - l + 1;
+        if (l < 1 || w < 1) return -1;
+        x += w;
+    }
+    return x;
+}
+
+}  // namespace
+}  // namespace pm
+
+using namespace pm;
+
+extern "C" {
+
+const char* pm_version(void) { return "pm_b200 0.1 (sm_100a)"; }
+const char* pm_last_error(void) { return g_last_error.c_str(); }
+
+void pm_default_config(pm_run_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->q = 0.95;
+    cfg->workers = 1;
+    cfg->backend = PM_BACKEND_AUTO;
+    cfg->max_em_iters = 5;
+    cfg->em_tol = 1e-6;
+    cfg->s_floor = 3;
+    cfg->dense_table_cap = 65536;
+    cfg->early_stop = 1;
+    cfg->z_epsilon = -1.0;
+}
+
+uint64_t pm_splitmix64(uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+uint64_t pm_derive_seed(uint64_t master, uint64_t index) {
+    return pm_splitmix64(master + 0x9E3779B97F4A7C15ULL * (index + 1));
+}
+
+int pm_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept) {
+    clear_error();
+    std::mt19937_64 eng(rng_seed);
+    return plan_from_engine(l, k, eng, kept);
+}
+
+int pm_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept) {
+    return pm_sample_plan(l, k, pm_derive_seed(master, static_cast<uint64_t>(trial)), kept);
+}
+
+int pm_validate_plan(int l, const int32_t* kept, int k) {
+    clear_error();
+    return validate_plan(l, kept, k);
+}
+
+int pm_optimal_k(int l, int d, int* k) {
+    clear_error();
+    if (l - d - 1 < 1) {
+        return set_error(PM_ERR_INVALID_PARAMS, "no valid projection width: l-d-1 = " + std::to_string(l - d - 1) +
+                                                    " (l=" + std::to_string(l) + ", d=" + std::to_string(d) + ")");
+    }
+    *k = l - d - 1;
+    return PM_OK;
+}
+
+int pm_p_hat(int l, int d, int k, double* out) {
+    clear_error();
+    if (l < 1 || d < 0 || d >= l || k < 0 || k > l) {
+        return set_error(PM_ERR_INVALID_PARAMS, "p_hat needs 0 <= d < l and 0 <= k <= l");
+    }
+    double p = 0.0;
+    if (k <= l - d) {
+        // C(l-d,k)/C(l,k) as a running product of ratios <= 1, i ascending (same order as the
+        // reference so the double result is identical).
+        p = 1.0;
+        for (int i = 0; i < k; ++i) p *= static_cast<double>(l - d - i) / static_cast<double>(l - i);
+    }
+    *out = p;
+    return PM_OK;
+}
+
+int pm_binomial_lt(int t_hat, double p, int s, double* out) {
+    clear_error();
+    if (t_hat < 1 || s < 0 || p < 0.0 || p > 1.0) {
+        return set_error(PM_ERR_INVALID_PARAMS, "binomial_lt needs t_hat >= 1, s >= 0, p in [0,1]");
+    }
+    double result;
+    if (s == 0) {
+        result = 0.0;
+    } else if (s > t_hat || p <= 0.0) {
+        result = 1.0;
+    } else if (p >= 1.0) {
+        result = 0.0;
+    } else {
+        // pmf terms built incrementally from (1-p)^t_hat, summed for i = 0 .. s-1
+        const double odds = p / (1.0 - p);
+        double term = std::pow(1.0 - p, t_hat);
+        double acc = term;
+        const int last = std::min(s - 1, t_hat);
+        for (int i = 0; i < last; ++i) {
+            term *= static_cast<double>(t_hat - i) / static_cast<double>(i + 1) * odds;
+            acc += term;
+        }
+        result = std::min(1.0, std::max(0.0, acc));
+    }
+    *out = result;
+    return PM_OK;
+}
+
+int pm_trials_for_tail(double q, double miss, int64_t* m_out) {
+    clear_error();
+    if (!(q > 0.0 && q < 1.0)) return set_error(PM_ERR_INVALID_PARAMS, "q must lie strictly between 0 and 1");
+    if (miss >= 1.0) {
+        return set_error(PM_ERR_UNREACHABLE, "bucket threshold unattainable: per-trial miss probability is 1");
+    }
+    if (miss <= 0.0) {
+        *m_out = 1;
+        return PM_OK;
+    }
+    // smallest m with miss^m <= 1-q: closed form, then nudged both ways in double arithmetic
+    const double target = 1.0 - q;
+    const double closed = std::ceil(std::log(target) / std::log(miss));
+    int64_t m = closed < 1.0 ? 1 : static_cast<int64_t>(closed);
+    while (std::pow(miss, static_cast<double>(m)) > target) ++m;
+    while (m > 1 && std::pow(miss, static_cast<double>(m - 1)) <= target) --m;
+    *m_out = m;
+    return PM_OK;
+}
+
+int pm_num_trials(double q, int t_hat, double p, int s, int64_t* m) {
+    double miss = 0.0;
+    const int rc = pm_binomial_lt(t_hat, p, s, &miss);
+    if (rc != PM_OK) return rc;
+    return pm_trials_for_tail(q, miss, m);
+}
+
+int pm_bucket_threshold_for_windows(uint64_t windows, int k, int floor_, int* s) {
+    clear_error();
+    if (k < 1 || floor_ < 1) return set_error(PM_ERR_INVALID_PARAMS, "bucket threshold needs k >= 1 and floor >= 1");
+    long double buckets = 1.0L;
+    for (int i = 0; i < k; ++i) buckets *= 4.0L;
+    const long double twice_mean = std::ceil(2.0L * static_cast<long double>(windows) / buckets);
+    *s = twice_mean <= static_cast<long double>(floor_) ? floor_ : static_cast<int>(twice_mean);
+    return PM_OK;
+}
+
+int pm_resolve_params(const pm_run_config* cfg, const int64_t* offs, int t, pm_run_result* params) {
+    clear_error();
+    if (t < 1) return set_error(PM_ERR_INVALID_PARAMS, "a sequence set needs at least one sequence");
+    if (cfg->l < 1) return set_error(PM_ERR_INVALID_PARAMS, "motif length l must be positive");
+    if (cfg->d < 0 || cfg->d >= cfg->l) {
+        return set_error(PM_ERR_INVALID_PARAMS,
+                         "need 0 <= d < l, got d=" + std::to_string(cfg->d) + ", l=" + std::to_string(cfg->l));
+    }
+    const int64_t windows = total_windows(offs, t, cfg->l);
+    if (windows < 0) {
+        return set_error(PM_ERR_INVALID_PARAMS, "a sequence has no l-mer of length " + std::to_string(cfg->l));
+    }
+    params->t_hat = cfg->t_hat != 0 ? cfg->t_hat : t;
+    if (params->t_hat < 1 || params->t_hat > t) return set_error(PM_ERR_INVALID_PARAMS, "t_hat must lie in [1, t]");
+    if (!(cfg->q > 0.0 && cfg->q < 1.0)) return set_error(PM_ERR_INVALID_PARAMS, "q must lie strictly between 0 and 1");
+    params->q = cfg->q;
+
+    int rc;
+    if (cfg->forced_kept != nullptr) {
+        if ((rc = validate_plan(cfg->l, cfg->forced_kept, cfg->n_forced)) != PM_OK) return rc;
+        params->k = cfg->n_forced;
+        if (cfg->k != 0 && cfg->k != params->k) {
+            return set_error(PM_ERR_INVALID_PARAMS, "k override conflicts with the forced projection plan");
+        }
+    } else if (cfg->k != 0) {
+        if (cfg->k < 1 || cfg->k > cfg->l) return set_error(PM_ERR_INVALID_PARAMS, "k override must lie in [1, l]");
+        params->k = cfg->k;
+    } else if ((rc = pm_optimal_k(cfg->l, cfg->d, &params->k)) != PM_OK) {
+        return rc;
+    }
+
+    if (cfg->s != 0) {
+        if (cfg->s < 1) return set_error(PM_ERR_INVALID_PARAMS, "s override must be at least 1");
+        params->s = cfg->s;
+    } else {
+        if (cfg->s_floor < 1) return set_error(PM_ERR_INVALID_PARAMS, "s floor must be at least 1");
+        rc = pm_bucket_threshold_for_windows(static_cast<uint64_t>(windows), params->k, cfg->s_floor, &params->s);
+        if (rc != PM_OK) return rc;
+    }
+
+    if (cfg->m != 0) {
+        if (cfg->m < 1) return set_error(PM_ERR_INVALID_PARAMS, "m override must be at least 1");
+        params->m = cfg->m;
+    } else if (cfg->forced_kept != nullptr) {
+        params->m = 1;  // a pinned plan makes repeated trials identical (driver.hpp:110-112)
+    } else {
+        double ph = 0.0;
+        if ((rc = pm_p_hat(cfg->l, cfg->d, params->k, &ph)) != PM_OK) return rc;
+        rc = pm_num_trials(params->q, params->t_hat, ph, params->s, &params->m);
+        if (rc == PM_ERR_UNREACHABLE) {
+            return set_error(rc, g_last_error + "; lower s or k, or pass an explicit m");
+        }
+        if (rc != PM_OK) return rc;
+    }
+    return PM_OK;
+}
+
+int pm_candidate_improves(int score_a, double exp_a, uint64_t key_a, int score_b, double exp_b, uint64_t key_b) {
+    if (score_a != score_b) return score_a > score_b;
+    if (exp_a != exp_b) return exp_a > exp_b;
+    return key_a < key_b;
+}
+
+int pm_merge_results(const pm_run_result* parts, const int32_t* const* parts_positions, int n_parts, int t, int l,
+                     int early_stop, pm_run_result* out, int32_t* positions_out) {
+    clear_error();
+    if (n_parts < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one partial result");
+    // Parts are contiguous trial shards in ascending trial order, so scanning parts in order and
+    // replacing only on a strict improvement reproduces the ascending-trial scan of
+    // driver.hpp:195-203.  A shard that reached the perfect score ends the scan (driver.hpp:204-207):
+    // each shard already truncated itself at its own first perfect trial.
+    const int perfect = l * t;
+    int winner = -1;
+    pm_run_result acc;
+    std::memset(&acc, 0, sizeof(acc));
+    acc.k = parts[0].k;
+    acc.s = parts[0].s;
+    acc.m = parts[0].m;
+    acc.q = parts[0].q;
+    acc.t_hat = parts[0].t_hat;
+    for (int i = 0; i < n_parts; ++i) {
+        const pm_run_result& p = parts[i];
+        acc.trials_run = std::max(acc.trials_run, p.trials_run);
+        acc.buckets_enriched += p.buckets_enriched;
+        acc.wall_ms = std::max(acc.wall_ms, p.wall_ms);
+        acc.gpu_launches += p.gpu_launches;
+        acc.em_lookup_adds += p.em_lookup_adds;
+        for (int j = 0; j < 8; ++j) acc.stage_ms[j] = std::max(acc.stage_ms[j], p.stage_ms[j]);
+        if (p.found && (winner < 0 || pm_candidate_improves(p.score, p.expectation, p.source_bucket, acc.score,
+                                                            acc.expectation, acc.source_bucket))) {
+            winner = i;
+            std::memcpy(acc.consensus, p.consensus, sizeof(acc.consensus));
+            acc.score = p.score;
+            acc.iterations = p.iterations;
+            acc.expectation = p.expectation;
+            acc.source_bucket = p.source_bucket;
+            acc.best_trial = p.best_trial;
+            acc.within_d = p.within_d;
+            acc.total_distance = p.total_distance;
+            acc.found = 1;
+        }
+        if (early_stop && acc.found && acc.score == perfect) {
+            acc.trials_run = p.trials_run;
+            break;
+        }
+    }
+    *out = acc;
+    if (winner < 0) {
+        return set_error(PM_ERR_NO_ENRICHED_BUCKETS, "no bucket reached s=" + std::to_string(acc.s) + " in " +
+                                                         std::to_string(acc.trials_run) +
+                                                         " trials; lower s or raise m");
+    }
+    if (positions_out != nullptr && parts_positions != nullptr && parts_positions[winner] != nullptr) {
+        std::memcpy(positions_out, parts_positions[winner], sizeof(int32_t) * static_cast<size_t>(t));
+    }
+    return PM_OK;
+}
+
+}  // extern "C"
