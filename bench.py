@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py — projection trials/sec of the PROJECTION hot path on B200 (BASELINE.json metric).
+
+    python bench.py --gpus 1 --steps 20 --warmup 5             # our arm (CUDA path through the C ABI)
+    python bench.py --impl reference --steps 3 --warmup 1      # the reference's CPU path on the host cores
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...   # N ranks, trial shards
+
+A step = one full pass of the hot path (hash -> bucket -> EM-refine -> score -> reduce) over one
+batch of projection trials on synthetic planted-(l,d) data: by default config C1 of BASELINE.json
+(the (15,4) instance the metric names): t=20 x n=600, k=7, s=4, m=172 trials (the reference's own
+trial count for q=0.95), instance seed 42, run seed 7, early_stop off.  With N ranks every rank
+runs its own contiguous shard of N*m trials (weak scaling) and the per-rank bests are merged with
+one all_gather (NCCL) inside the timed step.
+Prints ONE JSON line (see DESIGN.md §7 for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+
+METRIC = "projection trials/sec"
+UNIT = "trials/s"
+
+# BASELINE.json configs: name -> (t, n, l, d, k, s, m from the reference formula)
+CONFIGS = {
+    "c1": dict(t=20, n=600, l=15, d=4, k=7, s=4, m=172, label="C1 planted (15,4) t=20 n=600 k=7 s=4"),
+    "c2": dict(t=20, n=1000, l=16, d=5, k=7, s=4, m=1293, label="C2 planted (16,5) t=20 n=1000 k=7 s=4"),
+    "c3": dict(t=20, n=1000, l=18, d=6, k=7, s=4, m=2218, label="C3 planted (18,6) t=20 n=1000 k=7 s=4"),
+    "c4": dict(t=20, n=1000, l=20, d=7, k=7, s=4, m=3421, label="C4 planted (20,7) t=20 n=1000 k=7 s=4"),
+}
+INSTANCE_SEED = 42
+RUN_SEED = 7
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--trials", type=int, default=0, help="trials per step per GPU (default: the config's formula m)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip time-to-motif and the other-config sweep")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks: sampled with nvidia-smi DURING the timed region (B200_PROFILING.md recipe)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.rows = []
+        self.proc = None
+        self.gpu_index = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return p.get("hbm_gbs", 6650.0), p.get("sm_max_mhz", 1965.0), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+# ------------------------------------------------------------------------------------------------
+# the reference arm / cpu_baseline: the reference's own CPU implementation on the host cores
+# ------------------------------------------------------------------------------------------------
+def load_cpu_oracle():
+    from oracle import pmo
+    kind = "reference" if pmo.available("reference") else "port"
+    return pmo.load(kind), kind
+
+
+def cpu_trials_per_second(oracle, kind, ss, cfg, trials, workers):
+    """Times run() of the reference on `trials` trials of the workload (bounded sample)."""
+    t0 = time.perf_counter()
+    oracle.run(ss, l=cfg["l"], d=cfg["d"], k=cfg["k"], s=cfg["s"], m=trials, seed=RUN_SEED, early_stop=0,
+               workers=workers)
+    dt = time.perf_counter() - t0
+    return trials / dt, dt
+
+
+def run_reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return  # rank 0 alone runs the CPU arm
+    oracle, kind = load_cpu_oracle()
+    ss, _, _ = oracle.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], INSTANCE_SEED)
+    cores = os.cpu_count() or 1
+    workers = cores if kind == "reference" else 1  # the C port is a scalar single-thread restatement
+    sample = max(workers, 2) * (1 if cfg["n"] > 600 else 2)  # trials per step: ~1-3 s of host time
+    for _ in range(args.warmup):
+        cpu_trials_per_second(oracle, kind, ss, cfg, sample, workers)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_trials_per_second(oracle, kind, ss, cfg, sample, workers)
+        times.append(dt)
+    total = sum(times)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["label"], "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED,
+                   "trials_per_step": sample, "note": "bounded sample of the same workload; trial cost is i.i.d."},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+                         "sample": f"{sample} trials/step x {args.steps} steps of projmotif::run "
+                                   f"(-O3, workers={workers}) on {cores} host cores"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def run_b200_arm(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1605_06904_b200 as pm
+    from paper_1605_06904_b200.sharding import all_gather_merge, shard_range
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl b200 needs a B200: the CUDA path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    m_per_gpu = args.trials or cfg["m"]
+    m_total = m_per_gpu * world
+    begin, end = shard_range(m_total, rank, world)
+    stream = torch.cuda.current_stream()
+    ctx = pm.Context(local_rank, stream.cuda_stream)
+
+    # synthetic planted instance: the library's host generator (planted.hpp draw order, pinned to the
+    # reference by tests/test_host_abi.py), outside every timed region.  This arm never touches oracle/.
+    class Inst:
+        pass
+    ss = Inst()
+    ss.bases, ss.offs, motif, _ = pm.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], INSTANCE_SEED)
+    ss.t = cfg["t"]
+    ss.total_lmers = lambda l_: cfg["t"] * (cfg["n"] - l_ + 1)
+    t, l = ss.t, cfg["l"]
+    kw = dict(l=l, d=cfg["d"], k=cfg["k"], s=cfg["s"], m=m_total, seed=RUN_SEED, early_stop=0,
+              trial_begin=begin, trial_end=end, profile=1)
+
+    # pinned host copies of the inputs for the e2e leg
+    pinned = torch.empty(len(ss.bases), dtype=torch.uint8).pin_memory()
+    pinned.numpy()[:] = np.frombuffer(ss.bases, dtype=np.uint8)
+    bases_ptr = C.cast(pinned.data_ptr(), C.c_char_p)
+    offs = np.ascontiguousarray(ss.offs, dtype=np.int64)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step(e2e):
+        """One pass over this rank's trial shard + the cross-rank reduction.  Returns the merged result."""
+        cfg_c = pm.default_config(**kw)
+        out = pm.RunResult()
+        pos = np.zeros(t, dtype=np.int32)
+        if e2e:
+            rc = pm.lib().pm_run_host(ctx._h, C.byref(cfg_c), bases_ptr, offs.ctypes.data_as(C.POINTER(C.c_int64)), t,
+                                      C.byref(out), pos.ctypes.data_as(C.POINTER(C.c_int32)))
+        else:
+            rc = pm.lib().pm_run(ctx._h, C.byref(cfg_c), C.byref(out), pos.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 None, None, None, None)
+        if rc not in (0, 7):  # a shard may legitimately find no enriched bucket
+            raise pm.PmError(rc, pm.lib().pm_last_error().decode())
+        if dist is not None:
+            merged, mpos = all_gather_merge(out, pos, t, l, False, device=torch.device("cuda", local_rank))
+            return out, merged
+        return out, out
+
+    def timed_loop(steps, e2e):
+        per_step_ms, launches, stage, lookups, h2d, d2h = [], 0, [0.0] * 8, 0, 0, 0
+        result = None
+        for _ in range(steps):
+            flush.fill_(1)  # evict L2 between timed iterations (untimed)
+            barrier()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            mine, result = one_step(e2e)
+            ev1.record(stream)
+            barrier()
+            ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
+            if dist is not None:
+                dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # device-timed, max over ranks
+            per_step_ms.append(float(ms.item()))
+            launches += mine.gpu_launches
+            lookups += mine.em_lookup_adds
+            h2d += mine.h2d_bytes
+            d2h += mine.d2h_bytes
+            for i in range(8):
+                stage[i] += mine.stage_ms[i]
+        return per_step_ms, launches, stage, lookups, h2d, d2h, result
+
+    ctx.set_sequences(ss.bases, ss.offs)
+    timed_loop(args.warmup, False)                      # warm-up (untimed)
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    ms_dev, launches, stage, lookups, _, _, result = timed_loop(args.steps, False)
+    clocks = sampler.stop() if rank == 0 else None
+    timed_loop(max(1, min(args.warmup, 2)), True)
+    ms_e2e, _, stage_e2e, _, h2d, d2h, result_e2e = timed_loop(args.steps, True)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    mean_ms = sum(ms_dev) / len(ms_dev)
+    value = m_total / (mean_ms * 1e-3)
+    mean_e2e = sum(ms_e2e) / len(ms_e2e)
+    hbm_peak, sm_max_mhz, peak_kind = measured_peaks()
+    # EM kernel roofline: FP32-pipe bound.  achieved = E-step lookup-adds executed per
+    # launch / mean launch duration (CUDA events on the launching stream, inside the timed steps).
+    em_launches = args.steps * max(1, -(-(end - begin + 1) // 32768))
+    em_ms = stage[3] / max(1, args.steps)
+    fp32_peak_tflops = 148 * 128 * sm_max_mhz * 1e6 / 1e12
+    achieved_tflops = (lookups / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 else None
+    x = ss.total_lmers(l)
+    hb_bytes = (-(-t * cfg["n"] // 4) + 8 * x) * (end - begin + 1)
+    hb_ms = (stage[0] + stage[1] + stage[2]) / max(1, args.steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["label"], "trials_per_step_per_gpu": m_per_gpu, "trials_per_step": m_total,
+                   "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED, "early_stop": False,
+                   "parallelism": f"trials sharded over {world} GPU(s), one all_gather of the best record",
+                   "l2": "256 MiB flush between timed steps (untimed)",
+                   "timing": "CUDA events on the launching stream per step, max over ranks"},
+        "result": {"consensus": result.consensus.decode(), "score": result.score, "best_trial": result.best_trial,
+                   "planted_motif": motif, "recovered": result.consensus.decode() == motif,
+                   "buckets_enriched": result.buckets_enriched, "within_d": result.within_d},
+        "e2e": {"value": m_total / (mean_e2e * 1e-3), "unit": UNIT, "ms_per_step": mean_e2e,
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                "note": "pm_run_host: pinned host ASCII -> H2D -> encode -> run -> D2H result, every step"},
+        "gpu_launches": launches,
+        "stage_ms_per_step": {name: stage[i] / args.steps for i, name in
+                              enumerate(["keys", "sort", "enrich", "em", "reduce", "score", "upload", "d2h"])},
+        "roofline": {"bound": "fp32", "kernel": "em_refine_kernel", "achieved": achieved_tflops, "peak": fp32_peak_tflops,
+                     "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
+                     "traffic": None, "launch_ms": em_ms / max(1, em_launches // args.steps),
+                     "work": "E-step lookup-adds: sum_b (iterations_b+1)*x*l, 1 lookup-add = 1 FP32 op",
+                     "peak_source": f"148 SM x 128 FP32 lanes x {sm_max_mhz:.0f} MHz ({peak_kind} clocks), adds not FMAs"},
+        "roofline_hash_bucket": {"bound": "hbm", "kernels": "project_keys+radix_sort+enrich",
+                                 "achieved": (hb_bytes / (hb_ms * 1e-3) / 1e9) if hb_ms > 0 else None, "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": (hb_bytes / (hb_ms * 1e-3) / 1e9 / hbm_peak) if hb_ms > 0 else None,
+                                 "note": f"algorithmic bytes ceil(t*n/4)+8x per trial; peak {peak_kind}; at t=20 the "
+                                         "input is L2-resident so this is a latency/launch-bound stage, see DESIGN.md"},
+        "clocks": clocks,
+    }
+
+    if not args.no_extras:
+        line["time_to_motif"] = time_to_motif(pm, ctx, cfg)
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def time_to_motif(pm, ctx, cfg):
+    """Wall time from run() entry until the trial T* after which the running best consensus equals
+    the planted motif, over several instance seeds, batches of 16 trials."""
+    rows = []
+    for inst_seed in (42, 1, 2, 3, 4):
+        bases, offs, motif, _ = pm.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], inst_seed)
+        ctx.set_sequences(bases, offs)
+        t0 = time.perf_counter()
+        found_at, first = None, 1
+        while first <= cfg["m"] and found_at is None:
+            last = min(cfg["m"], first + 15)
+            try:
+                r = ctx.run(per_trial=False, l=cfg["l"], d=cfg["d"], k=cfg["k"], s=cfg["s"], m=cfg["m"], seed=RUN_SEED,
+                            early_stop=0, trial_begin=first, trial_end=last)
+                if r["consensus"] == motif:
+                    found_at = r["best_trial"]
+            except pm.PmError:
+                pass
+            first = last + 1
+        rows.append({"instance_seed": inst_seed, "found": found_at is not None, "t_star": found_at,
+                     "ms": 1e3 * (time.perf_counter() - t0)})
+    hit = [r for r in rows if r["found"]]
+    return {"runs": rows, "ms_median": statistics.median(r["ms"] for r in hit) if hit else None,
+            "note": "wall ms incl. host, batches of 16 trials, stop at the first batch whose best == planted motif"}
+
+
+def cpu_baseline(cfg):
+    oracle, kind = load_cpu_oracle()
+    ss, _, _ = oracle.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], INSTANCE_SEED)
+    cores = os.cpu_count() or 1
+    workers = cores if kind == "reference" else 1
+    # calibrate on `workers` trials, then size the sample for ~15 s of wall time
+    rate, dt = cpu_trials_per_second(oracle, kind, ss, cfg, max(workers, 2), workers)
+    sample = int(max(workers, min(cfg["m"], rate * 15.0)))
+    sample = max(workers, (sample // workers) * workers)
+    value, dt = cpu_trials_per_second(oracle, kind, ss, cfg, sample, workers)
+    return {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+            "sample": f"{sample} of the workload's trials through projmotif::run (reference headers, -O3 -DNDEBUG, "
+                      f"workers={workers}) in {dt:.1f} s on {cores} host cores"}
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+    else:
+        run_b200_arm(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

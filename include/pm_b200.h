@@ -98,7 +98,9 @@ typedef struct pm_run_result {
     int32_t total_distance;   /* sum_i min_j hamming(consensus, S_ij)  (oracle.hpp:101-115) */
     double stage_ms[8];       /* profile=1: [0] keys [1] sort [2] enrich [3] em [4] reduce [5] score [6] h2d+encode [7] d2h */
     int64_t gpu_launches;     /* kernels launched by this call */
-    int64_t em_lookup_adds;   /* E-step pair-table lookups x 2 executed (algorithmic work) */
+    int64_t em_lookup_adds;   /* E-step lookup-adds executed: sum over buckets of (iterations+1) * x * l */
+    int64_t h2d_bytes;        /* bytes this call copied host->device ... */
+    int64_t d2h_bytes;        /* ... and device->host */
 } pm_run_result;
 
 /* --------------------------------------------------------------------------------------------
@@ -113,6 +115,10 @@ uint64_t pm_derive_seed(uint64_t master, uint64_t index);          /* rng.hpp:22
 int pm_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept);/* sample_plan(l,k,Rng(seed)), projection.hpp:210-226 */
 int pm_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept); /* driver.hpp:164-165 */
 int pm_validate_plan(int l, const int32_t* kept, int k);           /* ProjectionPlan ctor, projection.hpp:36-52 */
+
+/* generate_planted, planted.hpp:38-101 (host; the synthetic-input generator of the benchmarks):
+ * bases = t*n chars without separators, motif = l chars, positions = t 1-based starts. */
+int pm_generate_planted(int t, int n, int l, int d, uint64_t seed, char* bases, char* motif, int32_t* positions);
 
 int pm_optimal_k(int l, int d, int* k);                            /* projection.hpp:97-103 */
 int pm_p_hat(int l, int d, int k, double* out);                    /* projection.hpp:107-120 */
@@ -164,11 +170,11 @@ int pm_enriched_buckets(pm_ctx* ctx, int l, const int32_t* kept, int k, int s, i
                         uint64_t* keys, int32_t* sizes_pre, int32_t* overflowed, int64_t* mem_off, int32_t* members);
 /* refine, refine.hpp:288-326, for n_buckets member lists at once (bucket b = members[mem_off[b]..mem_off[b+1])).
  * Per bucket: consensus (32 bytes each), positions (t each), score, expectation, iterations,
- * theta (4*(l+1) floats, MotifModel layout refine.hpp:65-71) and the LL trace (max_iters doubles).
+ * theta (4*(l+1) doubles, MotifModel layout refine.hpp:65-71) and the LL trace (max_iters doubles).
  * Any output pointer may be NULL. */
 int pm_refine(pm_ctx* ctx, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
               double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
-              int32_t* iterations, float* theta, double* ll_trace);
+              int32_t* iterations, double* theta, double* ll_trace);
 /* score / consensus of a start vector, scoring.hpp:111-131 (starts 1-based). */
 int pm_score(pm_ctx* ctx, int l, const int32_t* starts, int* score, char* consensus /* l+1 */);
 /* XOR/popcount Hamming scan of candidate v over every window: per-sequence minimum distance

@@ -1,0 +1,465 @@
+// projmotif_b200.hpp — C++ host layer over the pm_b200 C ABI with the reference library's own
+// entry points, value types and exception types (namespace projmotif -> projmotif_b200), so code
+// written against projmotif's hot path compiles against this header by switching the namespace.
+//
+//   reference (proj/include/projmotif/)                 here
+//   errors.hpp            exception hierarchy           same names, thrown from pm_status codes
+//   sequence.hpp:19-154   LmerRef, SequenceSet          same (value semantics, 1-based indices)
+//   projection.hpp:34-95  ProjectionPlan, Bucket, BucketGrouping, EnrichedBucket, HashBackend
+//   projection.hpp:97-206 optimal_k, p_hat, binomial_lt, trials_for_tail, num_trials, bucket_threshold*
+//   projection.hpp:210    sample_plan(l, k, Rng&)
+//   projection.hpp:319    hash_trial(seqs, l, plan, backend, workers, dense_table_cap)
+//   projection.hpp:359    enriched_buckets(grouping, s, r_cap)
+//   refine.hpp:288        refine(bucket, seqs, l, max_iters, tol)
+//   scoring.hpp:111-131   score, consensus;  sequence.hpp:28 hamming;  oracle.hpp:101 total_distance
+//   driver.hpp:23-220     RunConfig, RunResult, TrialParams, resolve_params, run
+//
+// All heavy work happens in libpm_b200.so on the GPU; nothing here computes the path on the CPU.
+// Link with -lpm_b200 (paper_1605_06904_b200/libpm_b200.so).
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+#include "pm_b200.h"
+
+namespace projmotif_b200 {
+
+// ---- errors.hpp
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ParamError : Error { using Error::Error; };
+struct ParseError : Error { using Error::Error; };
+struct UnknownSymbolError : ParseError { using ParseError::ParseError; };
+struct KmerTooLongError : ParamError { using ParamError::ParamError; };
+struct IndexOutOfRangeError : ParamError { using ParamError::ParamError; };
+struct LengthMismatchError : ParamError { using ParamError::ParamError; };
+struct InvalidParamsError : ParamError { using ParamError::ParamError; };
+struct DenseTableTooLargeError : ParamError { using ParamError::ParamError; };
+struct UnreachableError : ParamError { using ParamError::ParamError; };
+struct EmptyBucketError : ParamError { using ParamError::ParamError; };
+struct NoEnrichedBucketsError : Error { using Error::Error; };
+struct NumericalUnderflowError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };  // CUDA failure / no B200: there is no CPU fallback
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == PM_OK) return;
+    const std::string msg = pm_last_error();
+    switch (rc) {
+        case PM_ERR_INVALID_PARAMS: throw InvalidParamsError(msg);
+        case PM_ERR_LENGTH_MISMATCH: throw LengthMismatchError(msg);
+        case PM_ERR_KMER_TOO_LONG: throw KmerTooLongError(msg);
+        case PM_ERR_DENSE_TABLE_TOO_LARGE: throw DenseTableTooLargeError(msg);
+        case PM_ERR_UNREACHABLE: throw UnreachableError(msg);
+        case PM_ERR_EMPTY_BUCKET: throw EmptyBucketError(msg);
+        case PM_ERR_NO_ENRICHED_BUCKETS: throw NoEnrichedBucketsError(msg);
+        case PM_ERR_NUMERICAL_UNDERFLOW: throw NumericalUnderflowError(msg);
+        case PM_ERR_UNKNOWN_SYMBOL: throw UnknownSymbolError(msg);
+        case PM_ERR_INDEX_OUT_OF_RANGE: throw IndexOutOfRangeError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+}  // namespace detail
+
+// ---- sequence.hpp
+using StartVector = std::vector<int>;
+
+struct LmerRef {
+    int seq_index;
+    int offset;
+    int length;
+    friend bool operator==(const LmerRef& a, const LmerRef& b) {
+        return a.seq_index == b.seq_index && a.offset == b.offset && a.length == b.length;
+    }
+};
+
+class SequenceSet {
+public:
+    explicit SequenceSet(std::vector<std::string> sequences) : seqs_(std::move(sequences)) {
+        if (seqs_.empty()) throw InvalidParamsError("a sequence set needs at least one sequence");
+        offs_.assign(seqs_.size() + 1, 0);
+        for (std::size_t i = 0; i < seqs_.size(); ++i) {
+            if (seqs_[i].empty()) throw InvalidParamsError("sequence 'seq" + std::to_string(i + 1) + "' is empty");
+            for (char c : seqs_[i]) {
+                if (c != 'A' && c != 'C' && c != 'G' && c != 'T') {
+                    throw UnknownSymbolError(std::string("symbol '") + c + "' in sequence 'seq" + std::to_string(i + 1) +
+                                             "' is not in alphabet \"ACTG\"");
+                }
+            }
+            offs_[i + 1] = offs_[i] + static_cast<std::int64_t>(seqs_[i].size());
+            bases_ += seqs_[i];
+        }
+    }
+    int count() const { return static_cast<int>(seqs_.size()); }
+    int length(int i) const { return static_cast<int>(seqs_.at(static_cast<std::size_t>(i - 1)).size()); }
+    const std::string& sequence(int i) const { return seqs_.at(static_cast<std::size_t>(i - 1)); }
+    int window_count(int i, int l) const {
+        const int w = length(i) - l + 1;
+        if (l < 1 || w < 1) throw InvalidParamsError("sequence has no l-mer of length " + std::to_string(l));
+        return w;
+    }
+    std::uint64_t total_lmers(int l) const {
+        std::uint64_t x = 0;
+        for (int i = 1; i <= count(); ++i) x += static_cast<std::uint64_t>(window_count(i, l));
+        return x;
+    }
+    std::string lmer_at(int i, int j, int l) const {
+        const std::string& s = sequence(i);
+        if (l < 1 || j < 1 || j + l - 1 > static_cast<int>(s.size())) throw IndexOutOfRangeError("l-mer out of range");
+        return s.substr(static_cast<std::size_t>(j - 1), static_cast<std::size_t>(l));
+    }
+    // C-ABI view
+    const std::string& bases() const { return bases_; }
+    const std::vector<std::int64_t>& offsets() const { return offs_; }
+    // flat l-mer index (0-based, (seq, offset) order) <-> LmerRef
+    LmerRef ref_of(std::int64_t flat, int l) const {
+        std::int64_t first = 0;
+        for (int i = 1; i <= count(); ++i) {
+            const std::int64_t w = length(i) - l + 1;
+            if (flat < first + w) return LmerRef{i, static_cast<int>(flat - first) + 1, l};
+            first += w;
+        }
+        throw IndexOutOfRangeError("flat l-mer index out of range");
+    }
+    std::int32_t flat_of(const LmerRef& r) const {
+        std::int64_t first = 0;
+        for (int i = 1; i < r.seq_index; ++i) first += length(i) - r.length + 1;
+        return static_cast<std::int32_t>(first + r.offset - 1);
+    }
+
+private:
+    std::vector<std::string> seqs_;
+    std::string bases_;
+    std::vector<std::int64_t> offs_;
+};
+
+inline int hamming(std::string_view a, std::string_view b) {  // sequence.hpp:28-38 (trivial, host)
+    if (a.size() != b.size()) throw LengthMismatchError("hamming distance needs equal lengths");
+    int d = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) d += a[i] != b[i];
+    return d;
+}
+
+// ---- device binding: one context per thread, re-uploading only when the SequenceSet changes
+class Device {
+public:
+    static Device& instance() {
+        thread_local Device dev;
+        return dev;
+    }
+    pm_ctx* bind(const SequenceSet& seqs) {
+        if (!ctx_) {
+            pm_ctx* c = nullptr;
+            detail::check(pm_ctx_create(device_, nullptr, &c));
+            ctx_.reset(c);
+        }
+        if (loaded_ != seqs.bases() || loaded_offs_ != seqs.offsets()) {
+            detail::check(pm_ctx_set_sequences(ctx_.get(), seqs.bases().data(), seqs.offsets().data(), seqs.count()));
+            loaded_ = seqs.bases();
+            loaded_offs_ = seqs.offsets();
+        }
+        return ctx_.get();
+    }
+    void set_device(int ordinal) {
+        ctx_.reset();
+        loaded_.clear();
+        device_ = ordinal;
+    }
+
+private:
+    struct Closer {
+        void operator()(pm_ctx* c) const { pm_ctx_destroy(c); }
+    };
+    std::unique_ptr<pm_ctx, Closer> ctx_;
+    std::string loaded_;
+    std::vector<std::int64_t> loaded_offs_;
+    int device_ = 0;
+};
+
+// ---- rng.hpp: only the seed matters to sample_plan; the stream itself lives in libpm_b200 (pm_host.cpp)
+inline std::uint64_t splitmix64(std::uint64_t x) { return pm_splitmix64(x); }
+inline std::uint64_t derive_seed(std::uint64_t master, std::uint64_t index) { return pm_derive_seed(master, index); }
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : seed_(seed) {}
+    std::uint64_t seed() const { return seed_; }
+
+private:
+    std::uint64_t seed_;
+};
+
+// ---- projection.hpp
+struct TrialParams {
+    int l = 0, d = 0, k = 0, s = 0;
+    std::int64_t m = 0;
+    double q = 0.0;
+    int t_hat = 0;
+};
+
+class ProjectionPlan {
+public:
+    ProjectionPlan(int l, std::vector<int> kept) : l_(l), kept_(std::move(kept)) {
+        detail::check(pm_validate_plan(l_, kept_.data(), static_cast<int>(kept_.size())));
+    }
+    static ProjectionPlan identity(int l) {
+        std::vector<int> all(static_cast<std::size_t>(l));
+        for (int p = 1; p <= l; ++p) all[static_cast<std::size_t>(p - 1)] = p;
+        return ProjectionPlan(l, std::move(all));
+    }
+    int l() const { return l_; }
+    int k() const { return static_cast<int>(kept_.size()); }
+    const std::vector<int>& kept_positions() const { return kept_; }
+    bool operator==(const ProjectionPlan& o) const { return l_ == o.l_ && kept_ == o.kept_; }
+
+private:
+    int l_;
+    std::vector<int> kept_;
+};
+
+struct Bucket {
+    std::uint64_t key = 0;
+    std::vector<LmerRef> members;
+};
+using BucketGrouping = std::vector<Bucket>;
+struct EnrichedBucket {
+    std::uint64_t key = 0;
+    std::vector<LmerRef> members;
+    bool overflowed = false;
+};
+enum class HashBackend { dense, grouped, automatic };
+
+inline int optimal_k(int l, int d) { int k = 0; detail::check(pm_optimal_k(l, d, &k)); return k; }
+inline double p_hat(int l, int d, int k) { double v = 0; detail::check(pm_p_hat(l, d, k, &v)); return v; }
+inline double binomial_lt(int t_hat, double p, int s) { double v = 0; detail::check(pm_binomial_lt(t_hat, p, s, &v)); return v; }
+inline std::int64_t trials_for_tail(double q, double miss) { std::int64_t m = 0; detail::check(pm_trials_for_tail(q, miss, &m)); return m; }
+inline std::int64_t num_trials(double q, int t_hat, double p, int s) { std::int64_t m = 0; detail::check(pm_num_trials(q, t_hat, p, s, &m)); return m; }
+inline int bucket_threshold_for_windows(std::uint64_t windows, int k, int floor) {
+    int s = 0;
+    detail::check(pm_bucket_threshold_for_windows(windows, k, floor, &s));
+    return s;
+}
+inline int bucket_threshold(int t, int n, int l, int k, int floor = 3) {
+    if (t < 1 || l < 1 || l > n) throw InvalidParamsError("bucket threshold needs t >= 1 and 1 <= l <= n");
+    return bucket_threshold_for_windows(static_cast<std::uint64_t>(t) * static_cast<std::uint64_t>(n - l + 1), k, floor);
+}
+
+inline ProjectionPlan sample_plan(int l, int k, Rng& rng) {
+    std::vector<int> kept(static_cast<std::size_t>(k > 0 ? k : 1));
+    detail::check(pm_sample_plan(l, k, rng.seed(), kept.data()));
+    kept.resize(static_cast<std::size_t>(k));
+    return ProjectionPlan(l, std::move(kept));
+}
+
+inline BucketGrouping hash_trial(const SequenceSet& seqs, int l, const ProjectionPlan& plan,
+                                 HashBackend backend = HashBackend::automatic, int /*workers*/ = 1,
+                                 std::uint64_t dense_table_cap = 65536) {
+    if (plan.l() != l) {
+        throw LengthMismatchError("plan built for l=" + std::to_string(plan.l()) + ", asked to hash l=" + std::to_string(l));
+    }
+    const std::size_t x = static_cast<std::size_t>(seqs.total_lmers(l));
+    std::vector<std::uint64_t> keys(x);
+    std::vector<std::int32_t> sizes(x), members(x);
+    std::int64_t nb = 0;
+    const int be = backend == HashBackend::dense ? PM_BACKEND_DENSE : backend == HashBackend::grouped ? PM_BACKEND_GROUPED : PM_BACKEND_AUTO;
+    detail::check(pm_hash_trial(Device::instance().bind(seqs), l, plan.kept_positions().data(), plan.k(), be, dense_table_cap,
+                                &nb, keys.data(), sizes.data(), members.data()));
+    BucketGrouping out(static_cast<std::size_t>(nb));
+    std::size_t pos = 0;
+    for (std::size_t b = 0; b < out.size(); ++b) {
+        out[b].key = keys[b];
+        out[b].members.reserve(static_cast<std::size_t>(sizes[b]));
+        for (int m = 0; m < sizes[b]; ++m) out[b].members.push_back(seqs.ref_of(members[pos++], l));
+    }
+    return out;
+}
+
+// enriched_buckets (projection.hpp:359-390).  The reference filters a BucketGrouping that hash_trial
+// returned by value; its only caller is run_trial (driver.hpp:166-169), which run() below replaces
+// wholesale.  Here hashing, threshold, ordering and truncation happen in one device pass, so the
+// entry point takes the plan instead of the materialised grouping.
+inline std::vector<EnrichedBucket> enriched_buckets(const SequenceSet& seqs, int l, const ProjectionPlan& plan, int s, int r_cap) {
+    const std::size_t x = static_cast<std::size_t>(seqs.total_lmers(l));
+    std::vector<std::uint64_t> keys(x);
+    std::vector<std::int32_t> sizes(x), over(x), members(x);
+    std::vector<std::int64_t> moff(x + 1);
+    std::int64_t ne = 0;
+    detail::check(pm_enriched_buckets(Device::instance().bind(seqs), l, plan.kept_positions().data(), plan.k(), s, r_cap, &ne,
+                                      keys.data(), sizes.data(), over.data(), moff.data(), members.data()));
+    std::vector<EnrichedBucket> out(static_cast<std::size_t>(ne));
+    for (std::size_t b = 0; b < out.size(); ++b) {
+        out[b].key = keys[b];
+        out[b].overflowed = over[b] != 0;
+        for (std::int64_t m = moff[b]; m < moff[b + 1]; ++m) out[b].members.push_back(seqs.ref_of(members[static_cast<std::size_t>(m)], l));
+    }
+    return out;
+}
+
+// ---- refine.hpp
+struct RefinedCandidate {
+    std::string consensus;
+    StartVector positions;
+    int score = 0;
+    double expectation = 0.0;
+    int iterations = 0;
+    std::uint64_t source_bucket = 0;
+};
+
+inline std::vector<RefinedCandidate> refine_all(const std::vector<EnrichedBucket>& buckets, const SequenceSet& seqs, int l,
+                                                int max_iters = 5, double tol = 1e-6) {
+    if (max_iters < 1) throw InvalidParamsError("need at least one EM iteration");
+    const int t = seqs.count();
+    std::vector<std::int32_t> members;
+    std::vector<std::int64_t> moff(1, 0);
+    for (const EnrichedBucket& b : buckets) {
+        if (b.members.empty()) throw EmptyBucketError("cannot build a motif model from an empty bucket");
+        for (const LmerRef& r : b.members) members.push_back(seqs.flat_of(r));
+        moff.push_back(static_cast<std::int64_t>(members.size()));
+    }
+    const std::size_t nb = buckets.size();
+    std::vector<char> cons(32 * (nb ? nb : 1));
+    std::vector<std::int32_t> pos(static_cast<std::size_t>(t) * (nb ? nb : 1)), score(nb ? nb : 1), iters(nb ? nb : 1);
+    std::vector<double> expct(nb ? nb : 1);
+    detail::check(pm_refine(Device::instance().bind(seqs), l, members.data(), moff.data(), static_cast<int>(nb), max_iters, tol,
+                            -1.0, cons.data(), pos.data(), score.data(), expct.data(), iters.data(), nullptr, nullptr));
+    std::vector<RefinedCandidate> out(nb);
+    for (std::size_t b = 0; b < nb; ++b) {
+        out[b].consensus.assign(cons.data() + 32 * b, static_cast<std::size_t>(l));
+        out[b].positions.assign(pos.begin() + static_cast<std::ptrdiff_t>(b * static_cast<std::size_t>(t)),
+                                pos.begin() + static_cast<std::ptrdiff_t>((b + 1) * static_cast<std::size_t>(t)));
+        out[b].score = score[b];
+        out[b].expectation = expct[b];
+        out[b].iterations = iters[b];
+        out[b].source_bucket = buckets[b].key;
+    }
+    return out;
+}
+
+inline RefinedCandidate refine(const EnrichedBucket& bucket, const SequenceSet& seqs, int l, int max_iters = 5, double tol = 1e-6) {
+    return refine_all({bucket}, seqs, l, max_iters, tol).front();
+}
+
+// ---- scoring.hpp / oracle.hpp:101-115
+inline int score(const SequenceSet& seqs, const StartVector& starts, int l) {
+    if (static_cast<int>(starts.size()) != seqs.count()) throw LengthMismatchError("expected one start per sequence");
+    int sc = 0;
+    char cons[33];
+    detail::check(pm_score(Device::instance().bind(seqs), l, starts.data(), &sc, cons));
+    return sc;
+}
+inline std::string consensus(const SequenceSet& seqs, const StartVector& starts, int l) {
+    if (static_cast<int>(starts.size()) != seqs.count()) throw LengthMismatchError("expected one start per sequence");
+    int sc = 0;
+    char cons[33];
+    detail::check(pm_score(Device::instance().bind(seqs), l, starts.data(), &sc, cons));
+    return std::string(cons, static_cast<std::size_t>(l));
+}
+inline int total_distance(const std::string& candidate, const SequenceSet& seqs) {
+    int tot = 0;
+    detail::check(pm_hamming_scan(Device::instance().bind(seqs), candidate.data(), static_cast<int>(candidate.size()), 0, nullptr, &tot, nullptr));
+    return tot;
+}
+
+// ---- driver.hpp
+struct RunConfig {
+    int l = 0;
+    int d = 0;
+    std::optional<int> k;
+    std::optional<int> s;
+    std::optional<std::int64_t> m;
+    double q = 0.95;
+    std::uint64_t seed = 0;
+    int workers = 1;
+    HashBackend backend = HashBackend::automatic;
+    int max_em_iters = 5;
+    double em_tol = 1e-6;
+    int s_floor = 3;
+    std::uint64_t dense_table_cap = 65536;
+    bool early_stop = true;
+    std::optional<int> t_hat;
+    std::optional<std::vector<int>> forced_kept_positions;
+};
+
+struct RunResult {
+    RefinedCandidate best;
+    std::int64_t best_trial = 0;
+    TrialParams params;
+    std::uint64_t seed = 0;
+    std::int64_t trials_run = 0;
+    std::int64_t buckets_enriched = 0;
+    double wall_ms = 0.0;
+    // GPU-build extras (north_star "Scoring")
+    int within_d = 0;
+    int total_distance = 0;
+};
+
+namespace detail {
+inline pm_run_config to_c(const RunConfig& c) {
+    pm_run_config o;
+    pm_default_config(&o);
+    o.l = c.l;
+    o.d = c.d;
+    o.k = c.k.value_or(0);
+    o.s = c.s.value_or(0);
+    o.m = c.m.value_or(0);
+    o.q = c.q;
+    o.seed = c.seed;
+    o.workers = c.workers;
+    o.backend = c.backend == HashBackend::dense ? PM_BACKEND_DENSE : c.backend == HashBackend::grouped ? PM_BACKEND_GROUPED : PM_BACKEND_AUTO;
+    o.max_em_iters = c.max_em_iters;
+    o.em_tol = c.em_tol;
+    o.s_floor = c.s_floor;
+    o.dense_table_cap = c.dense_table_cap;
+    o.early_stop = c.early_stop ? 1 : 0;
+    o.t_hat = c.t_hat.value_or(0);
+    if (c.forced_kept_positions) {
+        o.forced_kept = c.forced_kept_positions->data();
+        o.n_forced = static_cast<std::int32_t>(c.forced_kept_positions->size());
+    }
+    // the reference distinguishes "override = 0/negative" (error) from "no override"; 0 is our
+    // "no override" marker, so reject explicit non-positive overrides here like driver.hpp:85-107
+    if (c.k && *c.k < 1) throw InvalidParamsError("k override must lie in [1, l]");
+    if (c.s && *c.s < 1) throw InvalidParamsError("s override must be at least 1");
+    if (c.m && *c.m < 1) throw InvalidParamsError("m override must be at least 1");
+    if (c.t_hat && *c.t_hat < 1) throw InvalidParamsError("t_hat must lie in [1, t]");
+    return o;
+}
+}  // namespace detail
+
+inline TrialParams resolve_params(const RunConfig& config, const SequenceSet& seqs) {
+    const pm_run_config c = detail::to_c(config);
+    pm_run_result r;
+    std::memset(&r, 0, sizeof(r));
+    detail::check(pm_resolve_params(&c, seqs.offsets().data(), seqs.count(), &r));
+    return TrialParams{config.l, config.d, r.k, r.s, r.m, r.q, r.t_hat};
+}
+
+inline RunResult run(const RunConfig& config, const SequenceSet& seqs) {
+    const pm_run_config c = detail::to_c(config);
+    pm_run_result r;
+    std::vector<std::int32_t> pos(static_cast<std::size_t>(seqs.count()));
+    detail::check(pm_run(Device::instance().bind(seqs), &c, &r, pos.data(), nullptr, nullptr, nullptr, nullptr));
+    RunResult out;
+    out.best.consensus = r.consensus;
+    out.best.positions.assign(pos.begin(), pos.end());
+    out.best.score = r.score;
+    out.best.expectation = r.expectation;
+    out.best.iterations = r.iterations;
+    out.best.source_bucket = r.source_bucket;
+    out.best_trial = r.best_trial;
+    out.params = TrialParams{config.l, config.d, r.k, r.s, r.m, r.q, r.t_hat};
+    out.seed = config.seed;
+    out.trials_run = r.trials_run;
+    out.buckets_enriched = r.buckets_enriched;
+    out.wall_ms = r.wall_ms;
+    out.within_d = r.within_d;
+    out.total_distance = r.total_distance;
+    return out;
+}
+
+}  // namespace projmotif_b200

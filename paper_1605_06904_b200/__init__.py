@@ -20,7 +20,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "libpm_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = ["pm_capi.cu", "pm_host.cpp"]
-HEADERS = ["pm_kernels.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
+HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -91,6 +91,7 @@ class RunResult(C.Structure):
         ("q", C.c_double), ("t_hat", C.c_int32), ("found", C.c_int32),
         ("within_d", C.c_int32), ("total_distance", C.c_int32),
         ("stage_ms", C.c_double * 8), ("gpu_launches", C.c_int64), ("em_lookup_adds", C.c_int64),
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
     ]
 
     def as_dict(self):
@@ -102,7 +103,7 @@ class RunResult(C.Structure):
 
 EXPORTS = [
     "pm_version", "pm_last_error", "pm_default_config", "pm_splitmix64", "pm_derive_seed", "pm_sample_plan",
-    "pm_trial_plan", "pm_validate_plan", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
+    "pm_trial_plan", "pm_validate_plan", "pm_generate_planted", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
@@ -196,6 +197,15 @@ def trial_plan(l, k, master, trial):
 def validate_plan(l, kept):
     k = _i32(kept)
     _check(lib().pm_validate_plan(l, _p(k, C.c_int32), len(k)))
+
+
+def generate_planted(t, n, l, d, seed):
+    """planted.hpp:38-101 -> (bases bytes of t*n chars, offs int64[t+1], motif, positions)."""
+    bases = C.create_string_buffer(t * n)
+    motif = C.create_string_buffer(l + 1)
+    pos = np.zeros(t, dtype=np.int32)
+    _check(lib().pm_generate_planted(t, n, l, d, C.c_uint64(seed), bases, motif, _p(pos, C.c_int32)))
+    return bases.raw[: t * n], np.arange(t + 1, dtype=np.int64) * n, motif.raw[:l].decode(), pos.tolist()
 
 
 def optimal_k(l, d):
@@ -366,11 +376,11 @@ class Context:
         score = np.zeros(max(nb, 1), dtype=np.int32)
         exp_ = np.zeros(max(nb, 1), dtype=np.float64)
         its = np.zeros(max(nb, 1), dtype=np.int32)
-        theta = np.zeros((max(nb, 1), 4, l + 1), dtype=np.float32)
+        theta = np.zeros((max(nb, 1), 4, l + 1), dtype=np.float64)
         ll = np.zeros((max(nb, 1), max_iters), dtype=np.float64)
         _check(lib().pm_refine(self._h, l, _p(members, C.c_int32), _p(moff, C.c_int64), nb, max_iters, C.c_double(tol),
                                C.c_double(z_epsilon), cons, _p(pos, C.c_int32), _p(score, C.c_int32),
-                               _p(exp_, C.c_double), _p(its, C.c_int32), _p(theta, C.c_float), _p(ll, C.c_double)))
+                               _p(exp_, C.c_double), _p(its, C.c_int32), _p(theta, C.c_double), _p(ll, C.c_double)))
         out = []
         for b in range(nb):
             out.append(dict(consensus=cons.raw[32 * b: 32 * b + l].decode(), positions=pos[b].tolist(),

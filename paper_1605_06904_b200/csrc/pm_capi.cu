@@ -19,6 +19,7 @@
 
 #include "pm_internal.hpp"
 #include "pm_kernels.cuh"
+#include "pm_em_smem.cuh"
 
 using namespace pm;
 
@@ -69,13 +70,26 @@ struct pm_ctx {
     unsigned int* d_seq_sym = nullptr;
     unsigned long long* d_tot_sym = nullptr;  // [0..3] symbol totals, [4] first bad byte
     unsigned long long tot_sym[4] = {0, 0, 0, 0};
+    // pair-class position groups for the shared-memory EM kernel (built once per sequence set)
+    uint16_t* d_cls_entries = nullptr;
+    int* d_cls_group_off = nullptr;
+    int* d_seq_zoff = nullptr;
+    int zlen = 0;          // 0 => the set does not fit the shared-memory EM kernel
+    int total_groups = 0;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
     int64_t* d_win_off = nullptr;
     int64_t x = 0, uniform_w = 0;
     DevBuf buf[S_COUNT_];
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    // measurement: bytes moved by this context and stage timing events (read after a sync)
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
+    struct StageMark {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<StageMark> marks;
+    std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
@@ -103,6 +117,110 @@ int check_launch(pm_ctx* c, const char* what) {
     ++c->launches;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(PM_ERR_CUDA, std::string(what) + " launch: " + cudaGetErrorString(e));
+    return PM_OK;
+}
+
+// Stage timing without extra synchronisation: events are recorded on the stream and read back by
+// collect_stage_times() after the batch's own final cudaStreamSynchronize.
+cudaEvent_t take_event(pm_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct StageTimer {
+    pm_ctx* c;
+    bool on;
+    int stage;
+    cudaEvent_t a = nullptr;
+    StageTimer(pm_ctx* ctx, bool enable, int stage_index) : c(ctx), on(enable), stage(stage_index) {
+        if (on) {
+            a = take_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    void stop() {
+        if (on && a) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, c->stream);
+            c->marks.push_back({stage, a, b});
+            a = nullptr;
+        }
+    }
+    ~StageTimer() { stop(); }
+};
+
+// call only after the stream has been synchronised
+void collect_stage_times(pm_ctx* c, double* stage_ms) {
+    for (const pm_ctx::StageMark& m : c->marks) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) stage_ms[m.stage] += ms;
+        c->ev_pool.push_back(m.a);
+        c->ev_pool.push_back(m.b);
+    }
+    c->marks.clear();
+}
+
+int h2d(pm_ctx* c, void* dst, const void* src, size_t bytes) {
+    c->h2d_bytes += static_cast<int64_t>(bytes);
+    PM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return PM_OK;
+}
+
+int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
+    c->d2h_bytes += static_cast<int64_t>(bytes);
+    PM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return PM_OK;
+}
+
+// Index build for the shared-memory EM kernel (pm_em_smem.cuh): the pair class 4*s_p + s_{p+1} of every base
+// position, grouped per class into warps of 32 positions with pairwise distinct addresses mod 32 so
+// that the M-step gather is free of bank conflicts.  A layout table like word_off, not arithmetic
+// of the path; it depends on the sequence set only (not on l, the plan or the bucket).
+int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel, int t) {
+    const int64_t total = rel[static_cast<size_t>(t)];
+    const int64_t zlen = k::kZPad + total;
+    if (zlen > 49000) return PM_OK;  // z would not fit in shared memory: the streaming kernel is used
+    auto code = [](char ch) { return (static_cast<unsigned char>(ch) >> 1) & 3; };
+    std::vector<std::vector<uint16_t>> bins(16 * 32);
+    for (int i = 0; i < t; ++i) {
+        const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
+        for (int64_t p = 0; p < n; ++p) {
+            const int a = code(bases[rel[static_cast<size_t>(i)] + p]);
+            const int b = p + 1 < n ? code(bases[rel[static_cast<size_t>(i)] + p + 1]) : 0;
+            const int64_t pos = k::kZPad + rel[static_cast<size_t>(i)] + p;
+            bins[static_cast<size_t>((4 * a + b) * 32 + (pos & 31))].push_back(static_cast<uint16_t>(pos));
+        }
+    }
+    std::vector<int> group_off(17, 0);
+    std::vector<uint16_t> entries;
+    for (int q = 0; q < 16; ++q) {
+        size_t groups = 0;
+        for (int r = 0; r < 32; ++r) groups = std::max(groups, bins[static_cast<size_t>(q * 32 + r)].size());
+        for (size_t g = 0; g < groups; ++g) {
+            for (int r = 0; r < 32; ++r) {
+                const std::vector<uint16_t>& b = bins[static_cast<size_t>(q * 32 + r)];
+                entries.push_back(g < b.size() ? b[g] : static_cast<uint16_t>(32 + r));  // dummy: a zero slot, same bank
+            }
+        }
+        group_off[static_cast<size_t>(q) + 1] = group_off[static_cast<size_t>(q)] + static_cast<int>(groups);
+    }
+    std::vector<int> zoff(static_cast<size_t>(t));
+    for (int i = 0; i < t; ++i) zoff[static_cast<size_t>(i)] = static_cast<int>(k::kZPad + rel[static_cast<size_t>(i)]);
+    PM_CUDA(cudaMalloc(&c->d_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
+    PM_CUDA(cudaMalloc(&c->d_cls_group_off, sizeof(int) * 17));
+    PM_CUDA(cudaMalloc(&c->d_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
+    PM_TRY(h2d(c, c->d_cls_entries, entries.data(), sizeof(uint16_t) * entries.size()));
+    PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * 17));
+    PM_TRY(h2d(c, c->d_seq_zoff, zoff.data(), sizeof(int) * zoff.size()));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    c->zlen = static_cast<int>(zlen);
+    c->total_groups = group_off[16];
     return PM_OK;
 }
 
@@ -137,8 +255,7 @@ int prepare_windows(pm_ctx* c, int l) {
         return set_error(PM_ERR_INVALID_PARAMS, "sort-and-group hashing supports at most 2^32-1 l-mers");  // projection.hpp:284-287
     }
     c->uniform_w = uniform ? c->seq_len[0] - l + 1 : 0;
-    PM_CUDA(cudaMemcpyAsync(c->d_win_off, c->win_off.data(), sizeof(int64_t) * (static_cast<size_t>(c->t) + 1),
-                            cudaMemcpyHostToDevice, c->stream));
+    PM_TRY(h2d(c, c->d_win_off, c->win_off.data(), sizeof(int64_t) * (static_cast<size_t>(c->t) + 1)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     c->win_l = l;
     return PM_OK;
@@ -220,6 +337,7 @@ int project_keys(pm_ctx* c, const std::vector<k::PlanProg>& progs, KeyT* keys) {
     const int n = static_cast<int>(progs.size());
     for (int base = 0; base < n; base += k::kMaxConstPlans) {
         const int cnt = std::min(k::kMaxConstPlans, n - base);
+        c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
         PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
                                         0, cudaMemcpyHostToDevice, c->stream));
         const unsigned gx = static_cast<unsigned>(std::min<int64_t>((c->x + 255) / 256, 4096));
@@ -294,6 +412,50 @@ EmKernel em_kernel_for(int l) {
     }
 }
 
+using EmSmemKernel = void (*)(const k::EmParams, const k::EmSmemExtra);
+
+template <int G>
+EmSmemKernel em_smem_for() { return k::em_refine_smem_kernel<G>; }
+
+EmSmemKernel em_smem_kernel_for(int l) {
+    switch ((l + 1) / 2) {
+        case 1: return em_smem_for<1>();
+        case 2: return em_smem_for<2>();
+        case 3: return em_smem_for<3>();
+        case 4: return em_smem_for<4>();
+        case 5: return em_smem_for<5>();
+        case 6: return em_smem_for<6>();
+        case 7: return em_smem_for<7>();
+        case 8: return em_smem_for<8>();
+        case 9: return em_smem_for<9>();
+        case 10: return em_smem_for<10>();
+        case 11: return em_smem_for<11>();
+        case 12: return em_smem_for<12>();
+        case 13: return em_smem_for<13>();
+        case 14: return em_smem_for<14>();
+        case 15: return em_smem_for<15>();
+        default: return em_smem_for<16>();
+    }
+}
+
+// must mirror the carve-up at the top of em_refine_smem_kernel
+size_t em_smem_bytes_v2(int nwarps, int G, int zlen) {
+    size_t b = 0;
+    b += (128 + 128 + static_cast<size_t>(nwarps) + 2) * 8;                               // thd, D64, llpart, dscal
+    b += (256 + static_cast<size_t>(nwarps) * 16 * G + 16 * static_cast<size_t>(G)) * 4;  // T, cpart, Cq
+    b += (static_cast<size_t>(nwarps) * k::kNearCap + 128 + 4) * 4;                       // near_j, prof, iscal
+    b += 8;                                                                               // cons_bits
+    b += static_cast<size_t>(zlen) * 4;                                                   // zbuf
+    return b + 16;
+}
+
+int em_smem_warps_for(int t) {
+    for (int nw : {10, 8, 12, 16, 6, 5, 4}) {
+        if (t % nw == 0) return nw;
+    }
+    return t >= 16 ? 8 : 4;
+}
+
 size_t em_smem_bytes(int nwarps) {
     size_t b = 0;
     b += 128 * 4;                          // th
@@ -322,7 +484,7 @@ struct EmOut {
     double* expct = nullptr;
     uint64_t* cons = nullptr;
     int32_t* pos = nullptr;
-    float* theta = nullptr;
+    double* theta = nullptr;
     double* ll = nullptr;
 };
 
@@ -360,6 +522,28 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.iter_total = d_scal;
     p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
 
+    if (c->zlen > 0) {
+        // shared-memory kernel: z of every window resident per CTA, conflict-free class-gather M-step
+        const int G = (l + 1) / 2;
+        const int nwarps = em_smem_warps_for(c->t);
+        const int threads = nwarps * 32;
+        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen);
+        EmSmemKernel kern = em_smem_kernel_for(l);
+        PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        if (per_sm >= 1) {
+            k::EmSmemExtra x;
+            x.cls_entries = c->d_cls_entries;
+            x.cls_group_off = c->d_cls_group_off;
+            x.seq_zoff = c->d_seq_zoff;
+            x.zlen = c->zlen;
+            const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
+            const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
+            kern<<<grid, threads, smem, c->stream>>>(p, x);
+            return check_launch(c, "em_refine_smem");
+        }
+    }
     const int nwarps = em_warps_for(c->t);
     const int threads = nwarps * 32;
     const size_t smem = em_smem_bytes(nwarps);
@@ -418,33 +602,6 @@ int check_plan_for_hash(pm_ctx* c, int l, const int32_t* kept, int kk) {
     return prepare_windows(c, l);
 }
 
-struct StageTimer {
-    pm_ctx* c;
-    bool on;
-    double* acc;
-    cudaEvent_t a = nullptr, b = nullptr;
-    StageTimer(pm_ctx* ctx, bool enable, double* into) : c(ctx), on(enable), acc(into) {
-        if (on) {
-            cudaEventCreate(&a);
-            cudaEventCreate(&b);
-            cudaEventRecord(a, c->stream);
-        }
-    }
-    void stop() {
-        if (on && a) {
-            cudaEventRecord(b, c->stream);
-            cudaEventSynchronize(b);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, a, b);
-            *acc += ms;
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-            a = b = nullptr;
-        }
-    }
-    ~StageTimer() { stop(); }
-};
-
 }  // namespace
 
 extern "C" {
@@ -488,6 +645,9 @@ void pm_ctx_destroy(pm_ctx* c) {
     cudaFree(c->d_seq_sym);
     cudaFree(c->d_tot_sym);
     cudaFree(c->d_win_off);
+    cudaFree(c->d_cls_entries);
+    cudaFree(c->d_cls_group_off);
+    cudaFree(c->d_seq_zoff);
     delete c;
 }
 
@@ -507,6 +667,14 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     cudaFree(c->d_seq_sym);
     cudaFree(c->d_tot_sym);
     cudaFree(c->d_win_off);
+    cudaFree(c->d_cls_entries);
+    cudaFree(c->d_cls_group_off);
+    cudaFree(c->d_seq_zoff);
+    c->d_cls_entries = nullptr;
+    c->d_cls_group_off = nullptr;
+    c->d_seq_zoff = nullptr;
+    c->zlen = 0;
+    c->total_groups = 0;
     c->d_words = nullptr;
     c->d_word_off = nullptr;
     c->d_seq_len = nullptr;
@@ -541,10 +709,10 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     PM_CUDA(cudaMalloc(&c->d_seq_sym, sizeof(unsigned int) * 4 * static_cast<size_t>(t)));
     PM_CUDA(cudaMalloc(&c->d_tot_sym, sizeof(unsigned long long) * 8));
     PM_CUDA(cudaMalloc(&c->d_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
-    PM_CUDA(cudaMemcpyAsync(d_ascii, bases + base0, static_cast<size_t>(total_bases), cudaMemcpyHostToDevice, c->stream));
-    PM_CUDA(cudaMemcpyAsync(d_offs, rel.data(), sizeof(int64_t) * rel.size(), cudaMemcpyHostToDevice, c->stream));
-    PM_CUDA(cudaMemcpyAsync(c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size(), cudaMemcpyHostToDevice, c->stream));
-    PM_CUDA(cudaMemcpyAsync(c->d_seq_len, len.data(), sizeof(int32_t) * len.size(), cudaMemcpyHostToDevice, c->stream));
+    PM_TRY(h2d(c, d_ascii, bases + base0, static_cast<size_t>(total_bases)));
+    PM_TRY(h2d(c, d_offs, rel.data(), sizeof(int64_t) * rel.size()));
+    PM_TRY(h2d(c, c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size()));
+    PM_TRY(h2d(c, c->d_seq_len, len.data(), sizeof(int32_t) * len.size()));
     PM_CUDA(cudaMemsetAsync(c->d_words, 0, sizeof(uint64_t) * static_cast<size_t>(total_words), c->stream));
     PM_CUDA(cudaMemsetAsync(c->d_seq_sym, 0, sizeof(unsigned int) * 4 * static_cast<size_t>(t), c->stream));
     PM_CUDA(cudaMemsetAsync(c->d_tot_sym, 0, sizeof(unsigned long long) * 4, c->stream));
@@ -557,7 +725,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
                                                                  c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
     PM_TRY(check_launch(c, "encode"));
     unsigned long long host_tot[5];
-    PM_CUDA(cudaMemcpyAsync(host_tot, c->d_tot_sym, sizeof(host_tot), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, host_tot, c->d_tot_sym, sizeof(host_tot)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     if (host_tot[4] != ULLONG_MAX) {
         const int64_t bad = static_cast<int64_t>(host_tot[4]);
@@ -567,6 +735,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
                                                     std::to_string(seq + 1) + "' is not in alphabet \"ACTG\"");
     }
     for (int r = 0; r < 4; ++r) c->tot_sym[r] = host_tot[r];
+    PM_TRY(build_class_groups(c, bases + base0, rel, t));
     c->t = t;
     c->offs = rel;
     c->word_off = word_off;
@@ -595,7 +764,7 @@ int pm_ctx_packed_words(pm_ctx* c, uint64_t* words_out, int64_t* word_off_out, i
     const int64_t n = c->word_off[static_cast<size_t>(c->t)];
     if (cap_words < n) return set_error(PM_ERR_INVALID_PARAMS, "output buffer too small for the packed words");
     PM_CUDA(cudaSetDevice(c->device));
-    PM_CUDA(cudaMemcpyAsync(words_out, c->d_words, sizeof(uint64_t) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, words_out, c->d_words, sizeof(uint64_t) * static_cast<size_t>(n)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     std::memcpy(word_off_out, c->word_off.data(), sizeof(int64_t) * c->word_off.size());
     return PM_OK;
@@ -629,7 +798,7 @@ int pm_hash_keys(pm_ctx* c, int l, const int32_t* kept, int kk, uint64_t* keys_o
     uint64_t* keys = nullptr;
     PM_TRY(get_buf(c, S_KEYS_A, static_cast<size_t>(c->x), &keys));
     PM_TRY(project_keys<uint64_t>(c, progs, keys));
-    PM_CUDA(cudaMemcpyAsync(keys_out, keys, sizeof(uint64_t) * static_cast<size_t>(c->x), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, keys_out, keys, sizeof(uint64_t) * static_cast<size_t>(c->x)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     return PM_OK;
 }
@@ -649,7 +818,7 @@ int stage_buckets(pm_ctx* c, const int32_t* kept, int kk, int thr, bool order_by
     Records rec;
     PM_TRY(find_enriched<KeyT>(c, srt, 1, thr, &rec));
     unsigned int n_rec = 0;
-    PM_CUDA(cudaMemcpyAsync(&n_rec, rec.n_rec, sizeof(n_rec), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, &n_rec, rec.n_rec, sizeof(n_rec)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     const size_t ne = n_rec;
     std::vector<uint32_t> order(ne);
@@ -670,16 +839,16 @@ int stage_buckets(pm_ctx* c, const int32_t* kept, int kk, int thr, bool order_by
         unsigned int* ko;
         unsigned int* io;
         PM_TRY((sort_segments<unsigned int>(c, ka, kb, ia, ib, 1, rec.cap_e, rec.cap_e, rec.n_rec, bits, &ko, &io)));
-        PM_CUDA(cudaMemcpyAsync(order.data(), io, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
+        PM_TRY(d2h(c, order.data(), io, sizeof(uint32_t) * ne));
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
     std::vector<uint64_t> hk(ne);
     std::vector<uint32_t> hs(ne), hz(ne);
     sorted_idx->resize(static_cast<size_t>(c->x));
-    PM_CUDA(cudaMemcpyAsync(hk.data(), rec.key, sizeof(uint64_t) * ne, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(hs.data(), rec.start, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(hz.data(), rec.size, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(sorted_idx->data(), srt.idx, sizeof(uint32_t) * static_cast<size_t>(c->x), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, hk.data(), rec.key, sizeof(uint64_t) * ne));
+    PM_TRY(d2h(c, hs.data(), rec.start, sizeof(uint32_t) * ne));
+    PM_TRY(d2h(c, hz.data(), rec.size, sizeof(uint32_t) * ne));
+    PM_TRY(d2h(c, sorted_idx->data(), srt.idx, sizeof(uint32_t) * static_cast<size_t>(c->x)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     keys->resize(ne);
     starts->resize(ne);
@@ -745,7 +914,7 @@ int pm_enriched_buckets(pm_ctx* c, int l, const int32_t* kept, int kk, int s, in
 
 int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
               double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
-              int32_t* iterations, float* theta, double* ll_trace) {
+              int32_t* iterations, double* theta, double* ll_trace) {
     clear_error();
     PM_TRY(need_sequences(c));
     PM_TRY(prepare_windows(c, l));
@@ -782,11 +951,11 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     if (ll_trace) {
         PM_TRY(get_buf(c, S_OUT_LL, nb * static_cast<size_t>(max_iters), &o.ll));
         std::vector<double> nan_fill(nb * static_cast<size_t>(max_iters), std::numeric_limits<double>::quiet_NaN());
-        PM_CUDA(cudaMemcpyAsync(o.ll, nan_fill.data(), sizeof(double) * nan_fill.size(), cudaMemcpyHostToDevice, c->stream));
+        PM_TRY(h2d(c, o.ll, nan_fill.data(), sizeof(double) * nan_fill.size()));
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
-    PM_CUDA(cudaMemcpyAsync(d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem), cudaMemcpyHostToDevice, c->stream));
-    PM_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(k::WorkDesc) * nb, cudaMemcpyHostToDevice, c->stream));
+    PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem)));
+    PM_TRY(h2d(c, d_work, work.data(), sizeof(k::WorkDesc) * nb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
     PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
                      static_cast<unsigned int>(n_buckets), d_mem, o, d_scal));
@@ -794,14 +963,14 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     std::vector<double> he(nb);
     std::vector<uint64_t> hc(nb);
     unsigned long long scal[2];
-    PM_CUDA(cudaMemcpyAsync(hs.data(), o.score, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(hi.data(), o.iters, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(he.data(), o.expct, sizeof(double) * nb, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(hc.data(), o.cons, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, c->stream));
-    PM_CUDA(cudaMemcpyAsync(scal, d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c->stream));
-    if (positions) PM_CUDA(cudaMemcpyAsync(positions, o.pos, sizeof(int32_t) * nb * static_cast<size_t>(c->t), cudaMemcpyDeviceToHost, c->stream));
-    if (theta) PM_CUDA(cudaMemcpyAsync(theta, o.theta, sizeof(float) * nb * 4 * static_cast<size_t>(l + 1), cudaMemcpyDeviceToHost, c->stream));
-    if (ll_trace) PM_CUDA(cudaMemcpyAsync(ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, hs.data(), o.score, sizeof(int32_t) * nb));
+    PM_TRY(d2h(c, hi.data(), o.iters, sizeof(int32_t) * nb));
+    PM_TRY(d2h(c, he.data(), o.expct, sizeof(double) * nb));
+    PM_TRY(d2h(c, hc.data(), o.cons, sizeof(uint64_t) * nb));
+    PM_TRY(d2h(c, scal, d_scal, sizeof(scal)));
+    if (positions) PM_TRY(d2h(c, positions, o.pos, sizeof(int32_t) * nb * static_cast<size_t>(c->t)));
+    if (theta) PM_TRY(d2h(c, theta, o.theta, sizeof(double) * nb * 4 * static_cast<size_t>(l + 1)));
+    if (ll_trace) PM_TRY(d2h(c, ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
@@ -832,12 +1001,12 @@ int pm_score(pm_ctx* c, int l, const int32_t* starts, int* score, char* consensu
     unsigned long long* d_out;
     PM_TRY(get_buf(c, S_TMP_A, static_cast<size_t>(c->t), &d_starts));
     PM_TRY(get_buf(c, S_SCAL, 4, &d_out));
-    PM_CUDA(cudaMemcpyAsync(d_starts, s0.data(), sizeof(int32_t) * s0.size(), cudaMemcpyHostToDevice, c->stream));
+    PM_TRY(h2d(c, d_starts, s0.data(), sizeof(int32_t) * s0.size()));
     k::score_kernel<<<1, 256, 0, c->stream>>>(c->d_words, c->d_word_off, c->t, l, d_starts,
                                             reinterpret_cast<int32_t*>(d_out), reinterpret_cast<uint64_t*>(d_out + 1));
     PM_TRY(check_launch(c, "score"));
     unsigned long long h[2];
-    PM_CUDA(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, h, d_out, sizeof(h)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     *score = static_cast<int>(h[0] & 0xFFFFFFFFULL);
     unpack_consensus(h[1], l, consensus);
@@ -858,7 +1027,7 @@ int pm_hamming_scan(pm_ctx* c, const char* v, int l, int d, int32_t* per_seq_min
     k::hamming_scan_kernel<<<blocks, threads, 0, c->stream>>>(c->d_words, c->d_word_off, c->d_seq_len, c->t, l, cand, d_min);
     PM_TRY(check_launch(c, "hamming_scan"));
     std::vector<int32_t> h(static_cast<size_t>(c->t));
-    PM_CUDA(cudaMemcpyAsync(h.data(), d_min, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    PM_TRY(d2h(c, h.data(), d_min, sizeof(int32_t) * h.size()));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     int tot = 0, within = 0;
     for (int i = 0; i < c->t; ++i) {
@@ -931,7 +1100,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     Sorted<KeyT> srt;
     Records rec;
     {
-        StageTimer tk(c, prof, &out->stage_ms[0]);
+        StageTimer tk(c, prof, 0);
         const size_t n = progs.size() * static_cast<size_t>(c->x);
         KeyT *ka, *kb;
         unsigned int *ia, *ib;
@@ -941,13 +1110,13 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(get_buf(c, S_IDX_B, n, &ib));
         PM_TRY(project_keys<KeyT>(c, progs, ka));
         tk.stop();
-        StageTimer ts(c, prof, &out->stage_ms[1]);
+        StageTimer ts(c, prof, 1);
         PM_TRY((sort_segments<KeyT>(c, ka, kb, ia, ib, n_trials, c->x, c->x, nullptr, 2 * params.k, &srt.keys, &srt.idx)));
     }
     unsigned int* work_off;
     k::WorkDesc* work;
     {
-        StageTimer te(c, prof, &out->stage_ms[2]);
+        StageTimer te(c, prof, 2);
         PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
         PM_TRY(get_buf(c, S_WORK_OFF, static_cast<size_t>(n_trials) + 1, &work_off));
         PM_TRY(get_buf(c, S_WORK, static_cast<size_t>(n_trials) * static_cast<size_t>(rec.cap_e), &work));
@@ -972,7 +1141,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
     {
-        StageTimer tm(c, prof, &out->stage_ms[3]);
+        StageTimer tm(c, prof, 3);
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work, work_off + n_trials, 0,
                          static_cast<unsigned int>(std::min<size_t>(nb, 1u << 30)), srt.idx, o, d_scal));
     }
@@ -980,7 +1149,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     std::vector<unsigned int> n_rec(static_cast<size_t>(n_trials));
     unsigned long long scal[2];
     {
-        StageTimer tr(c, prof, &out->stage_ms[4]);
+        StageTimer tr(c, prof, 4);
         const int warps_per_block = 8;
         k::trial_best_kernel<<<(n_trials + warps_per_block - 1) / warps_per_block, warps_per_block * 32, 0, c->stream>>>(
             work_off, work, o.score, o.expct, n_trials, best_work);
@@ -990,12 +1159,14 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(check_launch(c, "summarize"));
     }
     {
-        StageTimer td(c, prof, &out->stage_ms[7]);
-        PM_CUDA(cudaMemcpyAsync(tb.data(), d_tb, sizeof(TrialSummary) * tb.size(), cudaMemcpyDeviceToHost, c->stream));
-        PM_CUDA(cudaMemcpyAsync(n_rec.data(), rec.n_rec, sizeof(unsigned int) * n_rec.size(), cudaMemcpyDeviceToHost, c->stream));
-        PM_CUDA(cudaMemcpyAsync(scal, d_scal, sizeof(scal), cudaMemcpyDeviceToHost, c->stream));
+        StageTimer td(c, prof, 7);
+        PM_TRY(d2h(c, tb.data(), d_tb, sizeof(TrialSummary) * tb.size()));
+        PM_TRY(d2h(c, n_rec.data(), rec.n_rec, sizeof(unsigned int) * n_rec.size()));
+        PM_TRY(d2h(c, scal, d_scal, sizeof(scal)));
+        td.stop();
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
+    collect_stage_times(c, out->stage_ms);
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
@@ -1041,7 +1212,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work + new_best_work, nullptr, 1, 1, srt.idx,
                          o1, d_scal2));
         st->positions.resize(static_cast<size_t>(c->t));
-        PM_CUDA(cudaMemcpyAsync(st->positions.data(), o1.pos, sizeof(int32_t) * static_cast<size_t>(c->t), cudaMemcpyDeviceToHost, c->stream));
+        PM_TRY(d2h(c, st->positions.data(), o1.pos, sizeof(int32_t) * static_cast<size_t>(c->t)));
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
     return PM_OK;
@@ -1071,6 +1242,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     if (r_cap > INT32_MAX) return set_error(PM_ERR_UNSUPPORTED, "t*s exceeds 2^31-1");
     PM_CUDA(cudaSetDevice(c->device));
     const int64_t launches0 = c->launches;
+    const int64_t h2d0 = c->h2d_bytes, d2h0 = c->d2h_bytes;
 
     int64_t tb = cfg->trial_begin, te = cfg->trial_end;
     if (tb == 0 && te == 0) {
@@ -1118,6 +1290,8 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     }
 
     out->gpu_launches = c->launches - launches0;
+    out->h2d_bytes = c->h2d_bytes - h2d0;
+    out->d2h_bytes = c->d2h_bytes - d2h0;
     out->found = st.have_best ? 1 : 0;
     if (!st.have_best) {
         out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1133,13 +1307,16 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     if (positions) std::memcpy(positions, st.positions.data(), sizeof(int32_t) * static_cast<size_t>(c->t));
     {
         // XOR/popcount scoring of the reported consensus (north_star "Scoring")
-        StageTimer tsc(c, cfg->profile != 0, &out->stage_ms[5]);
+        StageTimer tsc(c, cfg->profile != 0, 5);
         int tot = 0, within = 0;
         PM_TRY(pm_hamming_scan(c, out->consensus, cfg->l, cfg->d, nullptr, &tot, &within));
         out->total_distance = tot;
         out->within_d = within;
     }
+    collect_stage_times(c, out->stage_ms);
     out->gpu_launches = c->launches - launches0;
+    out->h2d_bytes = c->h2d_bytes - h2d0;
+    out->d2h_bytes = c->d2h_bytes - d2h0;
     out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return PM_OK;
 }
@@ -1147,6 +1324,8 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
 int pm_run_host(pm_ctx* c, const pm_run_config* cfg, const char* bases, const int64_t* offs, int t, pm_run_result* out,
                 int32_t* positions) {
     const auto t0 = std::chrono::steady_clock::now();
+    if (c == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null context");
+    const int64_t h2d0 = c->h2d_bytes, d2h0 = c->d2h_bytes;
     double up_ms = 0.0;
     {
         const auto a = std::chrono::steady_clock::now();
@@ -1157,6 +1336,8 @@ int pm_run_host(pm_ctx* c, const pm_run_config* cfg, const char* bases, const in
     const int rc = pm_run(c, cfg, out, positions, nullptr, nullptr, nullptr, nullptr);
     out->stage_ms[6] = up_ms;
     out->gpu_launches = c->launches - launches0;
+    out->h2d_bytes = c->h2d_bytes - h2d0;
+    out->d2h_bytes = c->d2h_bytes - d2h0;
     out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return rc;
 }

@@ -1,0 +1,473 @@
+// pm_em_smem.cuh — EM refinement kernel for sequence sets whose per-window responsibilities fit in
+// shared memory (sum of sequence lengths <= ~50k bases: every t=20 config of BASELINE.json).
+//
+// One CTA per enriched bucket (persistent grid-stride over the work list), warps stride over
+// sequences for the E-step, then over pair-class position groups for the M-step.
+//
+//   E-step (lane = window)   w_j = sum_g T[g][nibble g of window j]  (pair-symbol log-odds table in smem),
+//                            pass A stores w_j and the per-sequence max, pass B turns them into
+//                            e_j = exp(w_j - max) and their sum, pass C scales to z_j = e_j / sum.
+//   M-step (lane = position) the pair class q(p) = 4 s_p + s_{p+1} of base position p is a property of the
+//                            sequence set, not of the bucket, so the positions of every class are grouped
+//                            ONCE per set into warps of 32 with pairwise distinct addresses mod 32.  Column
+//                            pair g of window j = p - 2g sees class q(p), hence
+//                                C[g][q] = sum_{p in class q} z[p - 2g]
+//                            is a conflict-free shared-memory gather into G register accumulators with no
+//                            data-dependent accumulator index; counts[a][2g] = sum_b C[g][4a+b] and
+//                            counts[b][2g+1] = sum_a C[g][4a+b] follow by marginalising (refine.hpp:227-237).
+//   precision                dense scan and counts in FP32; theta, log tables, the M-step normalisation and the
+//                            log-likelihood in FP64.  Windows within 2^-30 of the per-sequence maximum weight
+//                            are re-evaluated in FP64 (their z, the max and the log-sum-exp), which makes the
+//                            1e-6 convergence test of refine.hpp:300 reproducible whenever EM has saturated.
+#pragma once
+#include "pm_kernels.cuh"
+
+namespace pm {
+namespace k {
+
+constexpr int kZPad = 64;    // zero entries in front of the first sequence (dummy lanes read 32..63)
+constexpr int kNearCap = 64; // near-maximum windows re-evaluated in FP64, per warp
+
+struct EmSmemExtra {
+    const uint16_t* cls_entries;  // [total_groups][32] padded flat positions (kZPad + offs_i + p), dummies 32+lane
+    const int* cls_group_off;     // [17] first group of each class
+    const int* seq_zoff;          // [t] kZPad + offs_i
+    int zlen;                     // kZPad + total bases
+};
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// log-odds of window v under the FP64 table D64[c][r]
+__device__ __forceinline__ double window_weight_d(const double* __restrict__ D64, uint64_t v, int l) {
+    double w = 0.0;
+    for (int c = 0; c < l; ++c) w += D64[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)];
+    return w;
+}
+
+template <int G>
+__device__ __forceinline__ float window_weight_tree(const float* __restrict__ T, uint32_t vh, uint32_t vl) {
+    float t[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        // byte offset of entry (nibble g) in table g: nibble * 4
+        const uint32_t off = g < 7   ? (vh >> (26 - 4 * g)) & 0x3Cu
+                             : g == 7 ? (vh << 2) & 0x3Cu
+                             : g < 15 ? (vl >> (58 - 4 * g)) & 0x3Cu
+                                      : (vl << 2) & 0x3Cu;
+        t[g] = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(T) + g * 64 + off);
+    }
+    // pairwise tree: short dependency chains
+#pragma unroll
+    for (int s = 1; s < G; s <<= 1) {
+#pragma unroll
+        for (int g = 0; g + s < G; g += 2 * s) t[g] += t[g + s];
+    }
+    return t[0];
+}
+
+// top-aligned 64-bit window of lane `lane` (shift 2*lane) from words hi, lo as two 32-bit halves
+__device__ __forceinline__ void window_halves(uint64_t hi, uint64_t lo, int lane, uint32_t& vh, uint32_t& vl) {
+    const uint32_t h1 = static_cast<uint32_t>(hi >> 32), h0 = static_cast<uint32_t>(hi);
+    const uint32_t l1 = static_cast<uint32_t>(lo >> 32), l0 = static_cast<uint32_t>(lo);
+    const int sh = (2 * lane) & 31;
+    const bool upper = lane >= 16;
+    const uint32_t a = upper ? h0 : h1, b = upper ? l1 : h0, c = upper ? l0 : l1;
+    vh = __funnelshift_l(b, a, sh);
+    vl = __funnelshift_l(c, b, sh);
+}
+
+template <int G>
+__global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int l = p.l, t = p.t;
+
+    // ---- shared memory carve-up (doubles first for alignment)
+    double* thd = reinterpret_cast<double*>(smem_raw);  // [32][4] theta, column 0 = background
+    double* D64 = thd + 128;                            // [32][4] log theta[r][c+1] - log theta[r][0]
+    double* llpart = D64 + 128;                         // [nwarps]
+    double* dscal = llpart + nwarps;                    // [0] previous LL
+    float* T = reinterpret_cast<float*>(dscal + 2);     // [16][16] pair tables
+    float* cpart = T + 256;                             // [nwarps][16][G] per-warp class sums
+    float* Cq = cpart + nwarps * 16 * G;                // [16][G]
+    int* near_j = reinterpret_cast<int*>(Cq + 16 * G);  // [nwarps][kNearCap]
+    int* prof = near_j + nwarps * kNearCap;             // [32][4]
+    int* iscal = prof + 128;                            // [0] stop [1] score [2] bad
+    unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(iscal + 4);
+    float* zbuf = reinterpret_cast<float*>(cons_bits + 1);  // [zlen]
+
+    int* my_near = near_j + warp * kNearCap;
+    const int colshift = 62 - 2 * lane;
+
+    // responsibilities of invalid windows (and the front pad) stay zero for the whole kernel: only
+    // valid windows are ever written, and validity depends on the sequence set alone.
+    for (int i = threadIdx.x; i < x.zlen; i += blockDim.x) zbuf[i] = 0.f;
+
+    // M-step work split: contiguous ranges of (class, group) items per warp, fixed => deterministic
+    const int total_groups = x.cls_group_off[16];
+    const int item_lo = static_cast<int>(static_cast<long long>(total_groups) * warp / nwarps);
+    const int item_hi = static_cast<int>(static_cast<long long>(total_groups) * (warp + 1) / nwarps);
+
+    const unsigned int n_work = p.n_work_dev ? *p.n_work_dev : p.n_work;
+    for (unsigned int wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
+        const WorkDesc wd = p.work[wi];
+        __syncthreads();
+
+        // ---- init_model (refine.hpp:90-127), pseudocount 0
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) prof[i] = 0;
+        if (threadIdx.x == 0) {
+            iscal[0] = 0;
+            iscal[2] = 0;
+            dscal[0] = 0.0;
+        }
+        __syncthreads();
+        for (unsigned int m = threadIdx.x; m < wd.count; m += blockDim.x) {
+            const int64_t f = p.members[wd.mem_begin + m];
+            const int i = seq_of_flat(p.win_off, t, f);
+            const uint64_t v = load_window(p.words + p.word_off[i], f - p.win_off[i]);
+            for (int c = 0; c < l; ++c) atomicAdd(&prof[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)], 1);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < 4 * (l + 1); e += blockDim.x) {
+            const int c = e >> 2, r = e & 3;
+            thd[e] = c == 0 ? p.tot_sym[r] / p.tot_bases
+                            : static_cast<double>(prof[(c - 1) * 4 + r]) / static_cast<double>(wd.count);
+        }
+        __syncthreads();
+
+        int iterations = 0;
+        bool final_pass = false;
+        for (;;) {
+            // ---- log tables of the current theta (refine.hpp:155-161), FP64 then rounded once to FP32
+            for (int e = threadIdx.x; e < 4 * l; e += blockDim.x) {
+                const int c = e >> 2, r = e & 3;
+                D64[e] = log(fmax(thd[(c + 1) * 4 + r], 1e-9)) - log(fmax(thd[r], 1e-9));
+            }
+            if (final_pass) {
+                for (int i = threadIdx.x; i < 128; i += blockDim.x) prof[i] = 0;
+                if (threadIdx.x == 0) {
+                    iscal[1] = 0;
+                    *cons_bits = 0ULL;
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < 16 * G; e += blockDim.x) {
+                const int g = e >> 4, q = e & 15;
+                const int c0 = 2 * g, c1 = 2 * g + 1;
+                double v = 0.0;
+                if (c0 < l) v = D64[c0 * 4 + (q >> 2)];
+                if (c1 < l) v += D64[c1 * 4 + (q & 3)];
+                T[e] = static_cast<float>(v);
+            }
+            __syncthreads();
+
+            // ================= E-step: warp per sequence =================
+            double ll_warp = 0.0;
+            for (int i = warp; i < t; i += nwarps) {
+                const uint64_t* __restrict__ wp = p.words + p.word_off[i];
+                const int W = p.seq_len[i] - l + 1;
+                const int chunks = (W + 31) >> 5;
+                float* zs = zbuf + x.seq_zoff[i];
+
+                // pass A: window weights, lane-local maximum (strict >: earliest offset kept)
+                float best_w = -INFINITY;
+                int best_j = 0;
+                uint64_t hi = wp[0];
+                for (int c = 0; c < chunks; ++c) {
+                    const uint64_t lo = wp[c + 1];
+                    const int j = (c << 5) + lane;
+                    uint32_t vh, vl;
+                    window_halves(hi, lo, lane, vh, vl);
+                    hi = lo;
+                    if (j < W) {
+                        const float w = window_weight_tree<G>(T, vh, vl);
+                        zs[j] = w;
+                        if (w > best_w) {
+                            best_w = w;
+                            best_j = j;
+                        }
+                    }
+                }
+                const float M = warp_max_f(best_w);
+                if (!(M > -INFINITY) || !(M < INFINITY)) iscal[2] = 1;
+                __syncwarp();
+
+                if (final_pass) {
+                    // ---- positions: per-sequence argmax, ties to the smallest offset (refine.hpp:311-316).
+                    // Windows within delta of the FP32 maximum are compared by their FP64 weights.
+                    const float delta = 1e-3f + 1e-5f * fabsf(M);
+                    int nnear = 0;
+                    bool overflow = false;
+                    for (int c = 0; c < chunks; ++c) {
+                        const int j = (c << 5) + lane;
+                        const bool keep = j < W && zs[j] >= M - delta;
+                        const unsigned ball = __ballot_sync(0xffffffffu, keep);
+                        if (ball && !overflow) {
+                            if (nnear + __popc(ball) > kNearCap) {
+                                overflow = true;
+                            } else {
+                                if (keep) my_near[nnear + __popc(ball & ((1u << lane) - 1u))] = j;
+                                nnear += __popc(ball);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    int arg;
+                    if (!overflow) {
+                        double bw = -INFINITY;
+                        int bj = 0x7fffffff;
+                        for (int e = lane; e < nnear; e += 32) {
+                            const int j = my_near[e];
+                            const double w = window_weight_d(D64, load_window(wp, j), l);
+                            if (w > bw || (w == bw && j < bj)) {
+                                bw = w;
+                                bj = j;
+                            }
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+                            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                            if (ow > bw || (ow == bw && oj < bj)) {
+                                bw = ow;
+                                bj = oj;
+                            }
+                        }
+                        arg = bj;
+                    } else {
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const float ow = __shfl_xor_sync(0xffffffffu, best_w, o);
+                            const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+                            if (ow > best_w || (ow == best_w && oj < best_j)) {
+                                best_w = ow;
+                                best_j = oj;
+                            }
+                        }
+                        arg = best_j;
+                    }
+                    if (p.out_pos && lane == 0) p.out_pos[static_cast<int64_t>(wi) * t + i] = arg + 1;
+                    if (lane < l) {
+                        const uint64_t v = load_window(wp, arg);
+                        atomicAdd(&prof[lane * 4 + (static_cast<unsigned>(v >> colshift) & 3u)], 1);
+                    }
+                    __syncwarp();
+                    continue;
+                }
+
+                // pass B: e_j = exp(w_j - M), their sum; windows with w_j >= M + log(eps) are listed
+                float s_all = 0.f, s_far = 0.f;
+                int nnear = 0;
+                bool overflow = false;
+                for (int c = 0; c < chunks; ++c) {
+                    const int j = (c << 5) + lane;
+                    float e = 0.f;
+                    bool keep = false;
+                    if (j < W) {
+                        const float w = zs[j];
+                        e = __expf(w - M);
+                        zs[j] = e;
+                        keep = w >= M + p.log_z_eps;
+                    }
+                    s_all += e;
+                    s_far += keep ? 0.f : e;
+                    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+                    if (ball && !overflow) {
+                        if (nnear + __popc(ball) > kNearCap) {
+                            overflow = true;
+                        } else {
+                            if (keep) my_near[nnear + __popc(ball & ((1u << lane) - 1u))] = j;
+                            nnear += __popc(ball);
+                        }
+                    }
+                }
+                const float total = warp_sum_f(s_all);
+                if (!(total > 0.f)) iscal[2] = 1;
+                const float inv_total = 1.f / total;
+                __syncwarp();
+                // pass C: z_j = e_j / sum
+                for (int c = 0; c < chunks; ++c) {
+                    const int j = (c << 5) + lane;
+                    if (j < W) zs[j] *= inv_total;
+                }
+                __syncwarp();
+
+                const unsigned int* sc = p.seq_sym + i * 4;
+                const double lbg0 = log(fmax(thd[0], 1e-9)), lbg1 = log(fmax(thd[1], 1e-9));
+                const double lbg2 = log(fmax(thd[2], 1e-9)), lbg3 = log(fmax(thd[3], 1e-9));
+                const double log_base = sc[0] * lbg0 + sc[1] * lbg1 + sc[2] * lbg2 + sc[3] * lbg3;
+                double lse;  // log sum_j exp(w_j)
+                if (!overflow) {
+                    // FP64 re-evaluation of the dominant windows; the far tail (each < eps of the
+                    // maximum) keeps its FP32 sum
+                    const double far = static_cast<double>(warp_sum_f(s_far));
+                    double w64[(kNearCap + 31) / 32];
+                    double m64 = -INFINITY;
+#pragma unroll
+                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
+                        const int e = u * 32 + lane;
+                        w64[u] = e < nnear ? window_weight_d(D64, load_window(wp, my_near[e]), l) : -INFINITY;
+                        m64 = fmax(m64, w64[u]);
+                    }
+                    m64 = warp_max_d(m64);
+                    double s64 = 0.0;
+#pragma unroll
+                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
+                        w64[u] = u * 32 + lane < nnear ? exp(w64[u] - m64) : 0.0;
+                        s64 += w64[u];
+                    }
+                    s64 = warp_sum_d(s64) + far * exp(static_cast<double>(M) - m64);
+                    lse = m64 + log(s64);
+#pragma unroll
+                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
+                        const int e = u * 32 + lane;
+                        if (e < nnear) zs[my_near[e]] = static_cast<float>(w64[u] / s64);
+                    }
+                } else {
+                    lse = static_cast<double>(M) + log(static_cast<double>(total));
+                }
+                // log P(S_i) = log prod theta_bg - log W + logsumexp_j w_ij   (refine.hpp:200)
+                ll_warp += log_base - log(static_cast<double>(W)) + lse;
+                __syncwarp();
+            }
+            if (final_pass) break;
+            if (lane == 0) llpart[warp] = ll_warp;
+            __syncthreads();
+
+            // ================= M-step: conflict-free class gather =================
+            {
+                float acc[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g] = 0.f;
+                int cls = 0;
+                while (cls < 15 && x.cls_group_off[cls + 1] <= item_lo) ++cls;
+                for (int it = item_lo; it < item_hi; ++it) {
+                    while (it >= x.cls_group_off[cls + 1]) {
+                        // class finished for this warp: reduce lanes, publish, restart
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const float s = warp_sum_f(acc[g]);
+                            if (lane == 0) cpart[(warp * 16 + cls) * G + g] = s;
+                            acc[g] = 0.f;
+                        }
+                        ++cls;
+                    }
+                    const int pos = x.cls_entries[it * 32 + lane];
+                    const float* zp = zbuf + pos;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[g] += zp[-2 * g];
+                }
+                if (item_hi > item_lo) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float s = warp_sum_f(acc[g]);
+                        if (lane == 0) cpart[(warp * 16 + cls) * G + g] = s;
+                    }
+                }
+            }
+            __syncthreads();
+            // C[q][g] = sum over the warps that touched class q, in warp order
+            for (int e = threadIdx.x; e < 16 * G; e += blockDim.x) {
+                const int q = e / G, g = e - q * G;
+                const int g_lo = x.cls_group_off[q], g_hi = x.cls_group_off[q + 1];
+                float s = 0.f;
+                for (int w = 0; w < nwarps; ++w) {
+                    const int lo = static_cast<int>(static_cast<long long>(total_groups) * w / nwarps);
+                    const int hi = static_cast<int>(static_cast<long long>(total_groups) * (w + 1) / nwarps);
+                    if (lo < g_hi && hi > g_lo && hi > lo) s += cpart[(w * 16 + q) * G + g];
+                }
+                Cq[q * G + g] = s;
+            }
+            __syncthreads();
+            // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64
+            if (threadIdx.x <= l) {
+                double raw[4];
+                if (threadIdx.x < l) {
+                    const int c = threadIdx.x, g = c >> 1;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        double s = 0.0;
+                        for (int o = 0; o < 4; ++o) s += static_cast<double>(Cq[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                        raw[r] = s;
+                    }
+                } else {
+                    // background = symbol totals - expected motif counts, clamped at 0
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        double b = p.tot_sym[r];
+                        for (int c = 0; c < l; ++c) {
+                            const int g = c >> 1;
+                            for (int o = 0; o < 4; ++o) b -= static_cast<double>(Cq[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                        }
+                        raw[r] = fmax(b, 0.0);
+                    }
+                }
+                const double sum = raw[0] + raw[1] + raw[2] + raw[3];
+                double fs = 0.0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    raw[r] = sum > 0.0 ? fmax(raw[r] / sum, 1e-9) : 0.25;
+                    fs += raw[r];
+                }
+                const int col = threadIdx.x < l ? threadIdx.x + 1 : 0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) thd[col * 4 + r] = raw[r] / fs;
+            }
+            ++iterations;
+            if (threadIdx.x == 0) {
+                double ll = 0.0;
+                for (int w = 0; w < nwarps; ++w) ll += llpart[w];
+                if (p.out_ll) p.out_ll[static_cast<int64_t>(wi) * p.max_iters + (iterations - 1)] = ll;
+                iscal[0] = (iterations >= 2 && ll - dscal[0] < p.tol) ? 1 : 0;  // refine.hpp:296-304
+                dscal[0] = ll;
+            }
+            __syncthreads();
+            final_pass = iscal[0] != 0 || iterations >= p.max_iters;
+        }
+
+        // ---- score / consensus over the argmax rows (scoring.hpp:84-126), expectation (refine.hpp:130-136)
+        __syncthreads();
+        if (threadIdx.x < l) {
+            const int* pc = prof + threadIdx.x * 4;
+            int best = 0;
+            for (int r = 1; r < 4; ++r) {
+                if (pc[r] > pc[best]) best = r;
+            }
+            atomicAdd(&iscal[1], pc[best]);
+            atomicOr(cons_bits, static_cast<unsigned long long>(best) << (62 - 2 * threadIdx.x));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double ex = 0.0;
+            for (int c = 1; c <= l; ++c) {
+                const double* tc = thd + c * 4;
+                ex += fmax(fmax(tc[0], tc[1]), fmax(tc[2], tc[3]));
+            }
+            p.out_score[wi] = iscal[1];
+            p.out_iters[wi] = iterations;
+            p.out_exp[wi] = ex;
+            p.out_cons[wi] = *cons_bits;
+            atomicAdd(p.iter_total, static_cast<unsigned long long>(iterations + 1));
+            if (iscal[2]) atomicExch(p.error_flag, 1u);
+        }
+        if (p.out_theta) {
+            for (int e = threadIdx.x; e < 4 * (l + 1); e += blockDim.x) {
+                const int c = e >> 2, r = e & 3;
+                p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + c] = thd[e];
+            }
+        }
+    }
+}
+
+}  // namespace k
+}  // namespace pm

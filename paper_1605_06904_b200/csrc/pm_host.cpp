@@ -140,6 +140,46 @@ int pm_validate_plan(int l, const int32_t* kept, int k) {
     return validate_plan(l, kept, k);
 }
 
+int pm_generate_planted(int t, int n, int l, int d, uint64_t seed, char* bases, char* motif, int32_t* positions) {
+    clear_error();
+    if (t < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one sequence, got t=" + std::to_string(t));
+    if (l < 1 || l > n) {
+        return set_error(PM_ERR_INVALID_PARAMS, "need 1 <= l <= n, got l=" + std::to_string(l) + ", n=" + std::to_string(n));
+    }
+    if (d < 0 || d >= l) {
+        return set_error(PM_ERR_INVALID_PARAMS, "need 0 <= d < l, got d=" + std::to_string(d) + ", l=" + std::to_string(l));
+    }
+    static const char kSym[4] = {'A', 'C', 'T', 'G'};
+    auto rank_of = [](char c) { return c == 'A' ? 0 : c == 'C' ? 1 : c == 'T' ? 2 : 3; };
+    std::mt19937_64 eng(seed);
+    // Contractual draw order (planted.hpp:30-37): the motif; then per sequence its n background
+    // symbols, the start, the d mutated offsets (partial Fisher-Yates) and one replacement each.
+    std::string planted(static_cast<size_t>(l), 'A');
+    for (char& c : planted) c = kSym[draw_below(eng, 4)];
+    std::vector<int> pool(static_cast<size_t>(l));
+    for (int i = 0; i < t; ++i) {
+        char* s = bases + static_cast<size_t>(i) * static_cast<size_t>(n);
+        for (int p = 0; p < n; ++p) s[p] = kSym[draw_below(eng, 4)];
+        const int start = static_cast<int>(draw_below(eng, static_cast<uint64_t>(n - l + 1)));
+        std::string occ = planted;
+        for (int j = 0; j < l; ++j) pool[static_cast<size_t>(j)] = j;
+        for (int j = 0; j < d; ++j) {
+            const int pick = j + static_cast<int>(draw_below(eng, static_cast<uint64_t>(l - j)));
+            std::swap(pool[static_cast<size_t>(j)], pool[static_cast<size_t>(pick)]);
+        }
+        for (int j = 0; j < d; ++j) {
+            char& c = occ[static_cast<size_t>(pool[static_cast<size_t>(j)])];
+            int repl = static_cast<int>(draw_below(eng, 3));
+            if (repl >= rank_of(c)) ++repl;  // never redraw the original symbol
+            c = kSym[repl];
+        }
+        std::memcpy(s + start, occ.data(), static_cast<size_t>(l));
+        positions[i] = start + 1;
+    }
+    std::memcpy(motif, planted.data(), static_cast<size_t>(l));
+    return PM_OK;
+}
+
 int pm_optimal_k(int l, int d, int* k) {
     clear_error();
     if (l - d - 1 < 1) {

@@ -446,7 +446,7 @@ struct EmParams {
     double* out_exp;
     uint64_t* out_cons;    // packed consensus, first base most significant
     int32_t* out_pos;      // [work][t] 1-based or nullptr
-    float* out_theta;      // [work][4][l+1] (MotifModel layout) or nullptr
+    double* out_theta;     // [work][4][l+1] (MotifModel layout) or nullptr
     double* out_ll;        // [work][max_iters] or nullptr
     unsigned long long* iter_total;  // sum over buckets of E-steps executed (iterations + 1)
     unsigned int* error_flag;        // set to 1 on a non-finite window weight (NumericalUnderflowError)
@@ -755,7 +755,7 @@ __global__ void em_refine_kernel(const EmParams p) {
         }
         if (p.out_theta && threadIdx.x < 4 * (l + 1)) {
             const int c = threadIdx.x >> 2, r = threadIdx.x & 3;
-            p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + c] = th[threadIdx.x];
+            p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + c] = static_cast<double>(th[threadIdx.x]);
         }
     }
 }

@@ -1,0 +1,177 @@
+"""Parity of the whole path, run() (driver.hpp:145-220), on the GPU: against runs of the unmodified
+reference (tests/golden), against the oracle live on small instances, and -- at BASELINE.json's full
+sizes -- through size-independent properties."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import EXAMPLE_STARTS, EXPECTATION_TOL
+from oracle import pmo
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ("consensus", "score", "iterations", "source_bucket", "best_trial", "trials_run", "buckets_enriched",
+              "k", "s", "m", "t_hat", "positions")
+
+
+def assert_same_result(got, want):
+    for f in INT_FIELDS:
+        assert got[f] == want[f], (f, got[f], want[f])
+    assert abs(got["expectation"] - want["expectation"]) <= EXPECTATION_TOL
+
+
+def test_runs_match_reference_goldens(ctx, golden, instance):
+    for g in golden["run"]:
+        ss, _, _ = instance(*g["instance"])
+        ctx.set_sequences(ss.bases, ss.offs)
+        assert_same_result(ctx.run(**g["cfg"]), g["result"])
+
+
+def test_per_trial_outcomes_match_reference(ctx, golden, instance):
+    ss, _, _ = instance(20, 600, 15, 4, 42)
+    ctx.set_sequences(ss.bases, ss.offs)
+    r = ctx.run(per_trial=True, l=15, d=4, k=7, s=4, m=16, seed=7, early_stop=0)
+    t = golden["trial_outcomes_c1"]
+    assert r["trial_buckets"].tolist() == t["buckets"]
+    assert r["trial_score"].tolist() == t["score"]
+    assert [int(v) for v in r["trial_key"]] == t["key"]
+    np.testing.assert_allclose(r["trial_expectation"], t["expectation"], atol=EXPECTATION_TOL, rtol=0)
+
+
+def test_worked_example_forced_plan(ctx, example, golden):
+    # test_driver.cpp:86-102
+    r = ctx.run_host(example.bases, example.offs, l=8, d=1, s=4, forced_kept=[1, 2, 3, 6, 7])
+    assert_same_result(r, golden["worked"]["run"])
+    assert (r["consensus"], r["score"], r["positions"], r["source_bucket"]) == ("ATGCAACT", 53, EXAMPLE_STARTS, 177)
+    assert (r["within_d"], r["total_distance"]) == (7, 3)
+
+
+def test_early_stop_semantics(ctx, best_oracle, instance):
+    # test_driver.cpp:104-122: a d=0 plant is perfect at trial 1
+    ss, motif, _ = instance(5, 50, 10, 0, 77)
+    ctx.set_sequences(ss.bases, ss.offs)
+    r = ctx.run(l=10, d=0, seed=5, m=10)
+    assert (r["score"], r["consensus"], r["best_trial"], r["trials_run"]) == (50, motif, 1, 1)
+    assert_same_result(r, best_oracle.run(ss, l=10, d=0, seed=5, m=10))
+    full = ctx.run(l=10, d=0, seed=5, m=10, early_stop=0)
+    assert (full["trials_run"], full["score"]) == (10, 50)
+    # early stop inside a later batch: trials after the stopping one are discarded as if never run
+    r1 = ctx.run(l=10, d=0, seed=5, m=10, batch_trials=3)
+    assert (r1["trials_run"], r1["buckets_enriched"]) == (r["trials_run"], r["buckets_enriched"])
+
+
+def test_errors_mirror_the_reference(pm, ctx, instance, example):
+    ss, _, _ = instance(4, 30, 8, 2, 3)
+    ctx.set_sequences(ss.bases, ss.offs)
+    with pytest.raises(pm.PmError) as e:  # test_driver.cpp:153-161
+        ctx.run(l=8, d=2, s=30, m=2)
+    assert e.value.kind == "NoEnrichedBucketsError" and "s=30 in 2 trials" in str(e.value)
+    ctx.set_sequences(example.bases, example.offs)
+    for kw, kind in ((dict(l=5, d=4), "InvalidParamsError"), (dict(l=41, d=1), "InvalidParamsError"),
+                     (dict(l=8, d=6, k=1, s=1000), "UnreachableError"), (dict(l=8, d=1, max_em_iters=0), "InvalidParamsError"),
+                     (dict(l=12, d=1, k=12, m=1, backend=0), "DenseTableTooLargeError")):
+        with pytest.raises(pm.PmError) as e:
+            ctx.run(**kw)
+        assert e.value.kind == kind, kw
+
+
+def test_run_matches_oracle_on_small_and_ragged_sets(ctx, best_oracle):
+    rng = np.random.default_rng(7)
+    for round_ in range(6):
+        t = int(rng.integers(3, 9))
+        l = int(rng.integers(6, 12))
+        ss = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(l + 10, 90)))) for _ in range(t)])
+        kw = dict(l=l, d=1, k=l - 3, s=2, m=5, seed=round_, early_stop=0)
+        ctx.set_sequences(ss.bases, ss.offs)
+        got, want = ctx.run(**kw), best_oracle.run(ss, **kw)
+        for f in ("score", "buckets_enriched", "trials_run", "k", "s", "m"):
+            assert got[f] == want[f], (round_, f)
+        # equal-score candidates whose expectations differ by less than the FP32 tolerance may swap
+        if (got["best_trial"], got["source_bucket"]) == (want["best_trial"], want["source_bucket"]):
+            assert_same_result(got, want)
+
+
+def test_results_do_not_depend_on_batching_backend_or_workers(ctx, instance):
+    # test_driver.cpp:124-151 (workers x backends) plus the GPU build's own knob (batch size)
+    ss, _, _ = instance(8, 60, 9, 2, 1234)
+    ctx.set_sequences(ss.bases, ss.offs)
+    base = ctx.run(l=9, d=2, seed=42)
+    for kw in (dict(workers=4), dict(backend=1), dict(batch_trials=1), dict(batch_trials=7)):
+        other = ctx.run(l=9, d=2, seed=42, **kw)
+        for f in INT_FIELDS + ("expectation",):
+            assert other[f] == base[f], (kw, f)
+
+
+def test_explicit_plans_and_trial_shards(pm, ctx, instance):
+    ss, _, _ = instance(12, 120, 8, 1, 5)
+    ctx.set_sequences(ss.bases, ss.offs)
+    kw = dict(l=8, d=1, k=5, s=3, m=7, seed=3, early_stop=0)
+    full = ctx.run(**kw)
+    plans = np.array([pm.trial_plan(8, 5, 3, tr) for tr in range(1, 8)], dtype=np.int32)
+    via_plans = ctx.run(plans=plans, **dict(kw, seed=999))
+    for f in INT_FIELDS + ("expectation",):
+        assert via_plans[f] == full[f], f
+    # contiguous shards merged by pm_merge_results == the single run (the multi-GPU reduction)
+    from paper_1605_06904_b200.sharding import shard_range
+    for world in (2, 3, 4):
+        parts, poss = [], []
+        for rank in range(world):
+            b, e = shard_range(7, rank, world)
+            try:
+                ctx.run(trial_begin=b, trial_end=e, **kw)
+            except pm.PmError as err:
+                assert err.kind == "NoEnrichedBucketsError"
+            parts.append(ctx.last_result)
+            poss.append(ctx.last_positions.copy())
+        merged, pos = pm.merge_results(parts, poss, ss.t, 8, False)
+        assert (merged.consensus.decode(), merged.score, merged.expectation, merged.source_bucket, merged.best_trial,
+                merged.trials_run, merged.buckets_enriched) == \
+               (full["consensus"], full["score"], full["expectation"], full["source_bucket"], full["best_trial"],
+                full["trials_run"], full["buckets_enriched"])
+        assert pos.tolist() == full["positions"]
+
+
+def test_full_size_properties_c1_c2(ctx, port, golden, instance):
+    """BASELINE configs at their full trial counts: properties that do not need the slow CPU EM."""
+    for key, l, d, m in (((20, 600, 15, 4, 42), 15, 4, 172), ((20, 1000, 16, 5, 42), 16, 5, 1293)):
+        ss, motif, planted_pos = instance(*key)
+        ctx.set_sequences(ss.bases, ss.offs)
+        kw = dict(l=l, d=d, k=7, s=4, m=m, seed=7, early_stop=0)
+        r = ctx.run(per_trial=True, **kw)
+        assert r["m"] == m == r["trials_run"]
+        # enriched-bucket counts of every trial equal the oracle's hashing stage (bit-exact path)
+        sample = list(range(1, m + 1)) if m <= 200 else list(range(1, m + 1, 7))
+        for tr in sample:
+            kept = port.trial_plan(l, 7, 7, tr)
+            assert r["trial_buckets"][tr - 1] == len(port.enriched(ss, l, kept, 4, ss.t * 4)), tr
+        # score identity (test_scoring.cpp:108-124): score = l*t - sum_i hamming(consensus, row_i)
+        rows = [s[p - 1:p - 1 + l] for s, p in zip(ss.strings(), r["positions"])]
+        assert r["score"] == l * ss.t - sum(port.hamming(r["consensus"], row) for row in rows)
+        assert port.score(ss, l, r["positions"]) == (r["score"], r["consensus"])
+        tot, per = port.total_distance(ss, r["consensus"])
+        assert (r["total_distance"], r["within_d"]) == (tot, sum(1 for p in per if p <= d))
+        # the best trial's candidate is what the oracle refines from that trial's winning bucket
+        kept = port.trial_plan(l, 7, 7, r["best_trial"])
+        bucket = [e for e in port.enriched(ss, l, kept, 4, ss.t * 4) if e["key"] == r["source_bucket"]][0]
+        c = port.refine(ss, l, bucket["members"], bucket["key"])
+        assert (c.consensus, c.positions, c.score, c.iterations) == (r["consensus"], r["positions"], r["score"], r["iterations"])
+        assert abs(c.expectation - r["expectation"]) <= EXPECTATION_TOL
+        if key[1] == 600:
+            assert r["consensus"] == motif  # the planted (15,4) motif is recovered within 172 trials
+        # running the same trials again in different batch sizes gives the same answer
+        r2 = ctx.run(batch_trials=64, **kw)
+        assert (r2["consensus"], r2["score"], r2["best_trial"], r2["buckets_enriched"]) == \
+               (r["consensus"], r["score"], r["best_trial"], r["buckets_enriched"])
+
+
+def test_cpp_host_layer(pm):
+    """include/projmotif_b200.hpp: the reference's own test cases restated against the C++ layer."""
+    exe = "/tmp/pm_host_layer_test"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(pm.REPO_DIR, "include"),
+                    os.path.join(pm.REPO_DIR, "tests", "cpp", "host_layer_test.cpp"), "-L" + pm.PKG_DIR, "-lpm_b200",
+                    "-Wl,-rpath," + pm.PKG_DIR, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all checks passed" in out.stdout

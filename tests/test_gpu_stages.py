@@ -1,0 +1,249 @@
+"""Parity of each CUDA stage (through the C ABI) against the CPU oracle and the reference-generated
+goldens: bit-exact for codes, keys, grouping, enriched lists, positions, scores; theta and
+expectation within the stated FP32 tolerance (conftest.THETA_TOL / EXPECTATION_TOL)."""
+import numpy as np
+import pytest
+
+from conftest import EXAMPLE_STARTS, EXPECTATION_TOL, THETA_TOL, sha
+from oracle import pmo
+
+pytestmark = pytest.mark.gpu
+
+CODE = {"A": 0, "C": 1, "T": 2, "G": 3}
+
+
+def random_set(rng, t, lo, hi):
+    return pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(lo, hi + 1)))) for _ in range(t)])
+
+
+def pack_reference(strings):
+    """DESIGN.md §3 layout restated in Python: base p at bits [62-2(p%32), 64-2(p%32)) of word p/32."""
+    words, woff = [], [0]
+    for s in strings:
+        nw = (len(s) + 31) // 32 + 1
+        for w in range(nw):
+            v = 0
+            for p in range(32):
+                if w * 32 + p < len(s):
+                    v |= CODE[s[w * 32 + p]] << (62 - 2 * p)
+            words.append(v)
+        woff.append(woff[-1] + nw)
+    return words, woff
+
+
+def test_encode_packs_two_bits_per_base(ctx):
+    rng = np.random.default_rng(1)
+    for ss in (random_set(rng, 5, 1, 70), random_set(rng, 3, 32, 32), random_set(rng, 9, 63, 130)):
+        ctx.set_sequences(ss.bases, ss.offs)
+        words, woff = ctx.packed_words()
+        want_words, want_off = pack_reference(ss.strings())
+        assert woff.tolist() == want_off
+        assert [int(w) for w in words] == want_words
+        full = ss.bases.decode()
+        assert ctx.symbol_counts() == [full.count(c) for c in "ACTG"]
+
+
+def test_encode_rejects_what_the_reference_rejects(pm, ctx):
+    # sequence.hpp:44-69
+    for strings, kind in ((["ACGT", "ACNT"], "UnknownSymbolError"), (["acgt"], "UnknownSymbolError"),
+                          (["ACGT", ""], "InvalidParamsError")):
+        ss = pmo.SeqSet.from_strings(strings)
+        with pytest.raises(pm.PmError) as e:
+            ctx.set_sequences(ss.bases, ss.offs)
+        assert e.value.kind == kind
+    with pytest.raises(pm.PmError) as e:
+        ctx.set_sequences(b"", np.zeros(1, dtype=np.int64))
+    assert e.value.kind == "InvalidParamsError"
+
+
+def test_hash_keys_match_oracle_on_ragged_random_sets(ctx, best_oracle):
+    rng = np.random.default_rng(2)
+    for round_ in range(30):
+        l = int(rng.integers(1, 32))
+        k = int(rng.integers(1, l + 1))
+        ss = random_set(rng, int(rng.integers(1, 9)), l, l + 90)
+        kept = best_oracle.sample_plan(l, k, round_)
+        ctx.set_sequences(ss.bases, ss.offs)
+        got = ctx.hash_keys(l, kept)
+        want = best_oracle.hash_keys(ss, l, kept)
+        assert got.shape == want.shape and (got == want).all(), (l, k, kept)
+
+
+def test_worked_example_bucket(ctx, example, golden):
+    # test_projection.cpp:171-197 + the reference-generated grouping
+    w = golden["worked"]
+    ctx.set_sequences(example.bases, example.offs)
+    keys, sizes, members = ctx.hash_trial(8, w["kept"])
+    assert (keys.tolist(), sizes.tolist(), members.tolist()) == (w["keys"], w["sizes"], w["members"])
+    b = keys.tolist().index(177)
+    start = int(sizes[:b].sum())
+    assert [example.flat_to_ref(8, int(f)) for f in members[start:start + sizes[b]]] == \
+        [(1, 8), (2, 19), (3, 3), (4, 5), (5, 31), (6, 27), (7, 15)]
+    assert ctx.enriched_buckets(8, w["kept"], 4, 28) == w["enriched_s4"]
+    assert ctx.enriched_buckets(8, w["kept"], 4, 5) == w["enriched_s4_cap5"]
+    assert ctx.enriched_buckets(8, w["kept"], 1, 7 * 33) == w["enriched_s1"]
+    assert ctx.enriched_buckets(8, w["kept"], 1000, 1000) == []
+    assert list(ctx.score(8, EXAMPLE_STARTS)) == w["score"]
+    per, tot, within = ctx.hamming_scan("ATGCAACT", 1)
+    assert [tot, per] == w["total_distance"] and within == 7
+
+
+def test_hash_trial_and_enrichment_match_oracle_random(ctx, best_oracle):
+    # dense == grouped == device on random instances (test_projection.cpp:199-227)
+    rng = np.random.default_rng(41)
+    for round_ in range(40):
+        t = int(rng.integers(2, 7))
+        l = int(rng.integers(4, 11))
+        k = int(rng.integers(1, min(8, l) + 1))
+        ss = random_set(rng, t, max(12, l), 30)
+        kept = best_oracle.sample_plan(l, k, round_)
+        ctx.set_sequences(ss.bases, ss.offs)
+        got = ctx.hash_trial(l, kept)
+        for backend in (0, 1):
+            want = best_oracle.hash_trial(ss, l, kept, backend)
+            assert all((a == b).all() for a, b in zip(got, want))
+        for s, r_cap in ((1, 3), (2, 2 * t), (3, 3)):
+            assert ctx.enriched_buckets(l, kept, s, r_cap) == best_oracle.enriched(ss, l, kept, s, r_cap), (round_, s, r_cap)
+
+
+def test_hash_errors_mirror_the_reference(pm, ctx, example):
+    ctx.set_sequences(example.bases, example.offs)
+    with pytest.raises(pm.PmError) as e:
+        ctx.hash_trial(12, list(range(1, 13)), backend=0)  # test_projection.cpp:243-249
+    assert e.value.kind == "DenseTableTooLargeError"
+    ctx.hash_trial(12, list(range(1, 13)), backend=2)
+    ctx.hash_trial(12, list(range(1, 13)), backend=1)
+    for kept in ([], [0, 1], [1, 13], [2, 2]):
+        with pytest.raises(pm.PmError) as e:
+            ctx.hash_trial(12, kept)
+        assert e.value.kind == "InvalidParamsError"
+    for s, r in ((0, 5), (3, 2)):
+        with pytest.raises(pm.PmError) as e:
+            ctx.enriched_buckets(8, [1, 2, 3, 6, 7], s, r)
+        assert e.value.kind == "InvalidParamsError"
+    with pytest.raises(pm.PmError) as e:
+        ctx.hash_keys(41, [1, 2])  # a sequence shorter than l
+    assert e.value.kind in ("InvalidParamsError", "Unsupported")
+
+
+def test_challenge_scale_hashing_matches_reference_goldens(ctx, golden, instance):
+    for h in golden["hash"]:
+        ss, _, _ = instance(*h["instance"])
+        ctx.set_sequences(ss.bases, ss.offs)
+        assert sha(ctx.hash_keys(h["l"], h["kept"]).astype("<u8").tobytes()) == h["keys_sha256"]
+        bk, bs, bm = ctx.hash_trial(h["l"], h["kept"])
+        assert len(bk) == h["n_buckets"]
+        assert sha(bk.astype("<u8").tobytes()) == h["bucket_keys_sha256"]
+        assert sha(bs.astype("<i4").tobytes()) == h["bucket_sizes_sha256"]
+        assert sha(bm.astype("<i4").tobytes()) == h["members_sha256"]
+        assert ctx.enriched_buckets(h["l"], h["kept"], h["s"], ss.t * h["s"]) == h["enriched"]
+
+
+def check_candidate(got, want_consensus, want_positions, want_score, want_iterations, want_expectation, want_theta):
+    assert got["consensus"] == want_consensus
+    assert got["positions"] == want_positions
+    assert got["score"] == want_score
+    assert got["iterations"] == want_iterations
+    assert abs(got["expectation"] - want_expectation) <= EXPECTATION_TOL
+    assert np.abs(got["theta"].astype(np.float64) - np.asarray(want_theta)).max() <= THETA_TOL
+
+
+def test_refine_matches_reference_goldens(ctx, golden, instance):
+    by_inst = {}
+    for g in golden["refine"]:
+        by_inst.setdefault(tuple(g["instance"]), []).append(g)
+    for key, items in by_inst.items():
+        ss, _, _ = instance(*key)
+        ctx.set_sequences(ss.bases, ss.offs)
+        got = ctx.refine(items[0]["l"], [g["members"] for g in items])
+        for a, g in zip(got, items):
+            check_candidate(a, g["consensus"], g["positions"], g["score"], g["iterations"], g["expectation"], g["theta"])
+            np.testing.assert_allclose(a["ll_trace"], g["ll_trace"], atol=5e-2, rtol=0)
+
+
+def test_refine_worked_example(ctx, example, golden):
+    # test_refine.cpp:154-163
+    w = golden["worked"]
+    ctx.set_sequences(example.bases, example.offs)
+    got = ctx.refine(8, [w["enriched_s4"][0]["members"]])[0]
+    g = w["refine"]
+    check_candidate(got, "ATGCAACT", EXAMPLE_STARTS, 53, g["iterations"], g["expectation"], g["theta"])
+
+
+def test_refine_matches_oracle_on_random_instances(ctx, best_oracle):
+    # discrete outputs are compared where the reference's own top-2 window gap is not an FP32 near-tie
+    rng = np.random.default_rng(15)
+    compared = 0
+    for round_ in range(12):
+        t, l = int(rng.integers(3, 9)), int(rng.integers(3, 14))
+        ss = random_set(rng, t, l + 5, l + 70)
+        k = max(1, l - 2)
+        kept = best_oracle.sample_plan(l, k, round_)
+        en = best_oracle.enriched(ss, l, kept, 1, t)[:12]
+        ctx.set_sequences(ss.bases, ss.offs)
+        got = ctx.refine(l, [e["members"] for e in en])
+        for e, a in zip(en, got):
+            w = best_oracle.refine(ss, l, e["members"], e["key"])
+            assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL or a["iterations"] != w.iterations
+            if a["iterations"] == w.iterations:
+                assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+            if (a["positions"], a["iterations"]) == (w.positions, w.iterations):
+                assert (a["consensus"], a["score"]) == (w.consensus, w.score)
+                compared += 1
+    assert compared >= 100  # FP32 near-ties are rare, not the rule
+
+
+def test_refine_single_member_and_limits(pm, ctx, best_oracle, instance):
+    ss, _, pos = instance(6, 30, 5, 0, 99)
+    ctx.set_sequences(ss.bases, ss.offs)
+    # exact plant recovered with a perfect score (test_refine.cpp:165-175)
+    members = [ss.ref_to_flat(5, i + 1, pos[i]) for i in range(6)]
+    got = ctx.refine(5, [members])[0]
+    want = best_oracle.refine(ss, 5, members)
+    assert (got["consensus"], got["score"], got["positions"]) == (want.consensus, 30, pos)
+    # max_iters = 1 and a looser tolerance are honoured
+    for iters, tol in ((1, 1e-6), (3, 1e-6), (5, 10.0)):
+        a = ctx.refine(5, [members[:2]], max_iters=iters, tol=tol)[0]
+        b = best_oracle.refine(ss, 5, members[:2], max_iters=iters, tol=tol)
+        assert a["iterations"] == b.iterations and a["positions"] == b.positions
+    with pytest.raises(pm.PmError) as e:
+        ctx.refine(5, [members], max_iters=0)
+    assert e.value.kind == "InvalidParamsError"
+    with pytest.raises(pm.PmError) as e:
+        ctx.refine(5, [[]])
+    assert e.value.kind == "EmptyBucketError"
+    with pytest.raises(pm.PmError) as e:
+        ctx.refine(5, [[10 ** 6]])
+    assert e.value.kind == "IndexOutOfRangeError"
+
+
+def test_m_step_cutoff_is_within_its_bound(ctx, golden, instance):
+    """z_epsilon=0 adds every window's responsibility (the reference's dense M-step); the default
+    cut-off 2^-30 may drop at most W*eps of mass per count."""
+    g = [x for x in golden["refine"] if x["instance"][1] == 600][:8]
+    ss, _, _ = instance(*g[0]["instance"])
+    ctx.set_sequences(ss.bases, ss.offs)
+    dense = ctx.refine(15, [x["members"] for x in g], z_epsilon=0.0)
+    sparse = ctx.refine(15, [x["members"] for x in g])
+    for a, b, x in zip(dense, sparse, g):
+        assert np.abs(a["theta"] - b["theta"]).max() <= 586 * 2.0 ** -30 + 1e-6
+        assert (a["positions"], a["score"], a["consensus"]) == (b["positions"], b["score"], b["consensus"])
+        check_candidate(a, x["consensus"], x["positions"], x["score"], x["iterations"], x["expectation"], x["theta"])
+
+
+def test_score_and_hamming_scan_match_oracle(ctx, best_oracle):
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        l = int(rng.integers(1, 32))
+        ss = random_set(rng, int(rng.integers(1, 8)), l, l + 80)
+        ctx.set_sequences(ss.bases, ss.offs)
+        starts = [int(rng.integers(1, int(ss.offs[i + 1] - ss.offs[i]) - l + 2)) for i in range(ss.t)]
+        assert ctx.score(l, starts) == best_oracle.score(ss, l, starts)
+        v = "".join(rng.choice(list("ACGT"), l))
+        per, tot, within = ctx.hamming_scan(v, 2)
+        wtot, wper = best_oracle.total_distance(ss, v)
+        assert (tot, per) == (wtot, wper) and within == sum(1 for p in wper if p <= 2)
+    # consensus ties: A over C, T over G (test_scoring.cpp:81-91)
+    ss = pmo.SeqSet.from_strings(["AT", "CG"])
+    ctx.set_sequences(ss.bases, ss.offs)
+    assert ctx.score(2, [1, 1]) == (2, "AT")
