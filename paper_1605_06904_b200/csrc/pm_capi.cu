@@ -80,6 +80,7 @@ struct pm_ctx {
     int win_l = 0;
     std::vector<int64_t> win_off;
     int64_t* d_win_off = nullptr;
+    double* d_seq_logw = nullptr;
     int64_t x = 0, uniform_w = 0;
     DevBuf buf[S_COUNT_];
     // measurement: bytes moved by this context and stage timing events (read after a sync)
@@ -255,6 +256,9 @@ int prepare_windows(pm_ctx* c, int l) {
         return set_error(PM_ERR_INVALID_PARAMS, "sort-and-group hashing supports at most 2^32-1 l-mers");  // projection.hpp:284-287
     }
     c->uniform_w = uniform ? c->seq_len[0] - l + 1 : 0;
+    std::vector<double> logw(static_cast<size_t>(c->t));
+    for (int i = 0; i < c->t; ++i) logw[static_cast<size_t>(i)] = std::log(static_cast<double>(c->seq_len[static_cast<size_t>(i)] - l + 1));
+    PM_TRY(h2d(c, c->d_seq_logw, logw.data(), sizeof(double) * logw.size()));
     PM_TRY(h2d(c, c->d_win_off, c->win_off.data(), sizeof(int64_t) * (static_cast<size_t>(c->t) + 1)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     c->win_l = l;
@@ -441,16 +445,16 @@ EmSmemKernel em_smem_kernel_for(int l) {
 // must mirror the carve-up at the top of em_refine_smem_kernel
 size_t em_smem_bytes_v2(int nwarps, int G, int zlen) {
     size_t b = 0;
-    b += (128 + 128 + static_cast<size_t>(nwarps) + 2) * 8;                               // thd, D64, llpart, dscal
+    b += (128 + 128 + static_cast<size_t>(nwarps) + 6) * 8;                               // thd, D64, llpart, dscal
     b += (256 + static_cast<size_t>(nwarps) * 16 * G + 16 * static_cast<size_t>(G)) * 4;  // T, cpart, Cq
-    b += (static_cast<size_t>(nwarps) * k::kNearCap + 128 + 4) * 4;                       // near_j, prof, iscal
+    b += (static_cast<size_t>(nwarps) * k::kNearCap + 128 + 4 + 20) * 4;                  // near_j, prof, iscal, s_off
     b += 8;                                                                               // cons_bits
     b += static_cast<size_t>(zlen) * 4;                                                   // zbuf
     return b + 16;
 }
 
 int em_smem_warps_for(int t) {
-    for (int nw : {10, 8, 12, 16, 6, 5, 4}) {
+    for (int nw : {10, 8, 6, 5, 4}) {  // <= k::kEmSmemMaxWarps (the kernel's launch bound)
         if (t % nw == 0) return nw;
     }
     return t >= 16 ? 8 : 4;
@@ -499,6 +503,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.seq_len = c->d_seq_len;
     p.win_off = c->d_win_off;
     p.seq_sym = c->d_seq_sym;
+    p.seq_logw = c->d_seq_logw;
     for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
     p.tot_bases = static_cast<double>(c->total_bases);
     p.t = c->t;
@@ -530,6 +535,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen);
         EmSmemKernel kern = em_smem_kernel_for(l);
         PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
         PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         if (per_sm >= 1) {
@@ -645,6 +651,7 @@ void pm_ctx_destroy(pm_ctx* c) {
     cudaFree(c->d_seq_sym);
     cudaFree(c->d_tot_sym);
     cudaFree(c->d_win_off);
+    cudaFree(c->d_seq_logw);
     cudaFree(c->d_cls_entries);
     cudaFree(c->d_cls_group_off);
     cudaFree(c->d_seq_zoff);
@@ -667,6 +674,8 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     cudaFree(c->d_seq_sym);
     cudaFree(c->d_tot_sym);
     cudaFree(c->d_win_off);
+    cudaFree(c->d_seq_logw);
+    c->d_seq_logw = nullptr;
     cudaFree(c->d_cls_entries);
     cudaFree(c->d_cls_group_off);
     cudaFree(c->d_seq_zoff);
@@ -709,6 +718,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     PM_CUDA(cudaMalloc(&c->d_seq_sym, sizeof(unsigned int) * 4 * static_cast<size_t>(t)));
     PM_CUDA(cudaMalloc(&c->d_tot_sym, sizeof(unsigned long long) * 8));
     PM_CUDA(cudaMalloc(&c->d_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
+    PM_CUDA(cudaMalloc(&c->d_seq_logw, sizeof(double) * static_cast<size_t>(t)));
     PM_TRY(h2d(c, d_ascii, bases + base0, static_cast<size_t>(total_bases)));
     PM_TRY(h2d(c, d_offs, rel.data(), sizeof(int64_t) * rel.size()));
     PM_TRY(h2d(c, c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size()));

@@ -85,8 +85,11 @@ __device__ __forceinline__ void window_halves(uint64_t hi, uint64_t lo, int lane
     vl = __funnelshift_l(c, b, sh);
 }
 
+constexpr int kEmSmemMaxWarps = 10;
+
 template <int G>
-__global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
+__global__ void __launch_bounds__(kEmSmemMaxWarps * 32, 3)
+em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,14 +99,15 @@ __global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     double* thd = reinterpret_cast<double*>(smem_raw);  // [32][4] theta, column 0 = background
     double* D64 = thd + 128;                            // [32][4] log theta[r][c+1] - log theta[r][0]
     double* llpart = D64 + 128;                         // [nwarps]
-    double* dscal = llpart + nwarps;                    // [0] previous LL
-    float* T = reinterpret_cast<float*>(dscal + 2);     // [16][16] pair tables
+    double* dscal = llpart + nwarps;                    // [0] previous LL [2..5] log background
+    float* T = reinterpret_cast<float*>(dscal + 6);     // [16][16] pair tables
     float* cpart = T + 256;                             // [nwarps][16][G] per-warp class sums
     float* Cq = cpart + nwarps * 16 * G;                // [16][G]
     int* near_j = reinterpret_cast<int*>(Cq + 16 * G);  // [nwarps][kNearCap]
     int* prof = near_j + nwarps * kNearCap;             // [32][4]
     int* iscal = prof + 128;                            // [0] stop [1] score [2] bad
-    unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(iscal + 4);
+    int* s_off = iscal + 4;                             // [17] first group of each class (+3 pad)
+    unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(s_off + 20);
     float* zbuf = reinterpret_cast<float*>(cons_bits + 1);  // [zlen]
 
     int* my_near = near_j + warp * kNearCap;
@@ -112,9 +116,10 @@ __global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     // responsibilities of invalid windows (and the front pad) stay zero for the whole kernel: only
     // valid windows are ever written, and validity depends on the sequence set alone.
     for (int i = threadIdx.x; i < x.zlen; i += blockDim.x) zbuf[i] = 0.f;
+    if (threadIdx.x < 17) s_off[threadIdx.x] = x.cls_group_off[threadIdx.x];
 
     // M-step work split: contiguous ranges of (class, group) items per warp, fixed => deterministic
-    const int total_groups = x.cls_group_off[16];
+    const int total_groups = x.cls_group_off[16];  // (read before s_off is populated)
     const int item_lo = static_cast<int>(static_cast<long long>(total_groups) * warp / nwarps);
     const int item_hi = static_cast<int>(static_cast<long long>(total_groups) * (warp + 1) / nwarps);
 
@@ -152,6 +157,10 @@ __global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             for (int e = threadIdx.x; e < 4 * l; e += blockDim.x) {
                 const int c = e >> 2, r = e & 3;
                 D64[e] = log(fmax(thd[(c + 1) * 4 + r], 1e-9)) - log(fmax(thd[r], 1e-9));
+            }
+            if (threadIdx.x >= blockDim.x - 4) {
+                const int r = threadIdx.x - (blockDim.x - 4);
+                dscal[2 + r] = log(fmax(thd[r], 1e-9));
             }
             if (final_pass) {
                 for (int i = threadIdx.x; i < 128; i += blockDim.x) prof[i] = 0;
@@ -303,41 +312,31 @@ __global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 __syncwarp();
 
                 const unsigned int* sc = p.seq_sym + i * 4;
-                const double lbg0 = log(fmax(thd[0], 1e-9)), lbg1 = log(fmax(thd[1], 1e-9));
-                const double lbg2 = log(fmax(thd[2], 1e-9)), lbg3 = log(fmax(thd[3], 1e-9));
-                const double log_base = sc[0] * lbg0 + sc[1] * lbg1 + sc[2] * lbg2 + sc[3] * lbg3;
+                const double log_base = sc[0] * dscal[2] + sc[1] * dscal[3] + sc[2] * dscal[4] + sc[3] * dscal[5];
                 double lse;  // log sum_j exp(w_j)
-                if (!overflow) {
+                // The FP64 pass is skipped in the last iteration of the budget: its likelihood can no
+                // longer stop the loop (refine.hpp:296-304 breaks after max_iters regardless).
+                if (!overflow && iterations + 1 < p.max_iters) {
                     // FP64 re-evaluation of the dominant windows; the far tail (each < eps of the
                     // maximum) keeps its FP32 sum
                     const double far = static_cast<double>(warp_sum_f(s_far));
-                    double w64[(kNearCap + 31) / 32];
                     double m64 = -INFINITY;
-#pragma unroll
-                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
-                        const int e = u * 32 + lane;
-                        w64[u] = e < nnear ? window_weight_d(D64, load_window(wp, my_near[e]), l) : -INFINITY;
-                        m64 = fmax(m64, w64[u]);
-                    }
-                    m64 = warp_max_d(m64);
-                    double s64 = 0.0;
-#pragma unroll
-                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
-                        w64[u] = u * 32 + lane < nnear ? exp(w64[u] - m64) : 0.0;
-                        s64 += w64[u];
-                    }
-                    s64 = warp_sum_d(s64) + far * exp(static_cast<double>(M) - m64);
+                    double wa = -INFINITY, wb = -INFINITY;
+                    if (lane < nnear) wa = window_weight_d(D64, load_window(wp, my_near[lane]), l);
+                    if (nnear > 32 && lane + 32 < nnear) wb = window_weight_d(D64, load_window(wp, my_near[lane + 32]), l);
+                    m64 = warp_max_d(fmax(wa, wb));
+                    wa = lane < nnear ? exp(wa - m64) : 0.0;
+                    wb = (nnear > 32 && lane + 32 < nnear) ? exp(wb - m64) : 0.0;
+                    // far * exp(M - m64): |M - m64| ~ 1e-5 and far < W*eps, so first order is exact to ~1e-17
+                    const double s64 = warp_sum_d(wa + wb) + far * (1.0 + (static_cast<double>(M) - m64));
                     lse = m64 + log(s64);
-#pragma unroll
-                    for (int u = 0; u < (kNearCap + 31) / 32; ++u) {
-                        const int e = u * 32 + lane;
-                        if (e < nnear) zs[my_near[e]] = static_cast<float>(w64[u] / s64);
-                    }
+                    if (lane < nnear) zs[my_near[lane]] = static_cast<float>(wa / s64);
+                    if (nnear > 32 && lane + 32 < nnear) zs[my_near[lane + 32]] = static_cast<float>(wb / s64);
                 } else {
                     lse = static_cast<double>(M) + log(static_cast<double>(total));
                 }
                 // log P(S_i) = log prod theta_bg - log W + logsumexp_j w_ij   (refine.hpp:200)
-                ll_warp += log_base - log(static_cast<double>(W)) + lse;
+                ll_warp += log_base - p.seq_logw[i] + lse;
                 __syncwarp();
             }
             if (final_pass) break;
@@ -345,48 +344,40 @@ __global__ void em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             __syncthreads();
 
             // ================= M-step: conflict-free class gather =================
-            {
+            for (int q = 0; q < 16; ++q) {
+                const int a = max(item_lo, s_off[q]), b = min(item_hi, s_off[q + 1]);
+                if (a >= b) continue;  // this warp owns no group of class q
                 float acc[G];
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[g] = 0.f;
-                int cls = 0;
-                while (cls < 15 && x.cls_group_off[cls + 1] <= item_lo) ++cls;
-                for (int it = item_lo; it < item_hi; ++it) {
-                    while (it >= x.cls_group_off[cls + 1]) {
-                        // class finished for this warp: reduce lanes, publish, restart
-#pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            const float s = warp_sum_f(acc[g]);
-                            if (lane == 0) cpart[(warp * 16 + cls) * G + g] = s;
-                            acc[g] = 0.f;
-                        }
-                        ++cls;
-                    }
-                    const int pos = x.cls_entries[it * 32 + lane];
+                const uint16_t* __restrict__ ent = x.cls_entries + static_cast<size_t>(a) * 32 + lane;
+                int pos = ent[0];
+                for (int it = a; it < b; ++it) {
+                    ent += 32;
+                    const int nxt = it + 1 < b ? static_cast<int>(ent[0]) : 0;  // prefetch the next group
                     const float* zp = zbuf + pos;
 #pragma unroll
                     for (int g = 0; g < G; ++g) acc[g] += zp[-2 * g];
+                    pos = nxt;
                 }
-                if (item_hi > item_lo) {
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float s = warp_sum_f(acc[g]);
-                        if (lane == 0) cpart[(warp * 16 + cls) * G + g] = s;
-                    }
+                for (int g = 0; g < G; ++g) {
+                    const float sum = warp_sum_f(acc[g]);
+                    if (lane == 0) cpart[(warp * 16 + q) * G + g] = sum;
                 }
             }
             __syncthreads();
-            // C[q][g] = sum over the warps that touched class q, in warp order
+            // C[q][g] = sum over the warps that own groups of class q, in warp order
             for (int e = threadIdx.x; e < 16 * G; e += blockDim.x) {
                 const int q = e / G, g = e - q * G;
-                const int g_lo = x.cls_group_off[q], g_hi = x.cls_group_off[q + 1];
-                float s = 0.f;
+                const int g_lo = s_off[q], g_hi = s_off[q + 1];
+                float sum = 0.f;
                 for (int w = 0; w < nwarps; ++w) {
                     const int lo = static_cast<int>(static_cast<long long>(total_groups) * w / nwarps);
                     const int hi = static_cast<int>(static_cast<long long>(total_groups) * (w + 1) / nwarps);
-                    if (lo < g_hi && hi > g_lo && hi > lo) s += cpart[(w * 16 + q) * G + g];
+                    if (max(lo, g_lo) < min(hi, g_hi)) sum += cpart[(w * 16 + q) * G + g];
                 }
-                Cq[q * G + g] = s;
+                Cq[q * G + g] = sum;
             }
             __syncthreads();
             // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64

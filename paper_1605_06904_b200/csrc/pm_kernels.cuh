@@ -430,6 +430,7 @@ struct EmParams {
     const int32_t* seq_len;
     const int64_t* win_off;
     const unsigned int* seq_sym;  // t x 4
+    const double* seq_logw;       // t: log(n_i - l + 1)
     double tot_sym[4];
     double tot_bases;
     int t, l, max_iters;
@@ -627,7 +628,7 @@ __global__ void em_refine_kernel(const EmParams p) {
                 {
                     const unsigned int* sc = p.seq_sym + i * 4;
                     const double log_base = sc[0] * dscal[1] + sc[1] * dscal[2] + sc[2] * dscal[3] + sc[3] * dscal[4];
-                    ll_warp += log_base - log(static_cast<double>(W)) + static_cast<double>(M) +
+                    ll_warp += log_base - p.seq_logw[i] + static_cast<double>(M) +
                                log(static_cast<double>(total));
                 }
                 __syncwarp();
