@@ -76,6 +76,7 @@ struct pm_ctx {
     int* d_seq_zoff = nullptr;
     int zlen = 0;          // 0 => the set does not fit the shared-memory EM kernel
     int total_groups = 0;
+    double group_fill = 0.0;  // live entries / slots of the class-gather rows
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -185,16 +186,58 @@ int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
 // of the path; it depends on the sequence set only (not on l, the plan or the bucket).
 int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel, int t) {
     const int64_t total = rel[static_cast<size_t>(t)];
-    const int64_t zlen = k::kZPad + total;
-    if (zlen > 49000) return PM_OK;  // z would not fit in shared memory: the streaming kernel is used
+    if (k::kZPad + total + 32 * static_cast<int64_t>(t) > 49000 && k::kZPad + total > 47000) return PM_OK;
     auto code = [](char ch) { return (static_cast<unsigned char>(ch) >> 1) & 3; };
+    // Each sequence may start up to 31 slots later than the previous one ended; the slack is chosen
+    // greedily so that, per class, the positions spread evenly over the 32 address residues (the
+    // number of gather rows of a class is its fullest residue).
+    const bool may_shift = k::kZPad + total + 32 * static_cast<int64_t>(t) <= 49000;
+    std::vector<int> zoff(static_cast<size_t>(t));
+    std::vector<int> load(16 * 32, 0);
+    std::vector<int> mine(16 * 32);
+    int64_t cursor = k::kZPad;
+    for (int i = 0; i < t; ++i) {
+        const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
+        std::fill(mine.begin(), mine.end(), 0);
+        for (int64_t p = 0; p < n; ++p) {
+            const int a = code(bases[rel[static_cast<size_t>(i)] + p]);
+            const int b = p + 1 < n ? code(bases[rel[static_cast<size_t>(i)] + p + 1]) : 0;
+            ++mine[static_cast<size_t>((4 * a + b) * 32 + ((cursor + p) & 31))];
+        }
+        int best_shift = 0;
+        if (may_shift) {
+            int64_t best_cost = -1;
+            for (int sh = 0; sh < 32; ++sh) {
+                int64_t cost = 0;
+                for (int q = 0; q < 16; ++q) {
+                    int mx = 0;
+                    for (int r = 0; r < 32; ++r) {
+                        mx = std::max(mx, load[static_cast<size_t>(q * 32 + ((r + sh) & 31))] + mine[static_cast<size_t>(q * 32 + r)]);
+                    }
+                    cost += mx;
+                }
+                if (best_cost < 0 || cost < best_cost) {
+                    best_cost = cost;
+                    best_shift = sh;
+                }
+            }
+        }
+        for (int q = 0; q < 16; ++q) {
+            for (int r = 0; r < 32; ++r) load[static_cast<size_t>(q * 32 + ((r + best_shift) & 31))] += mine[static_cast<size_t>(q * 32 + r)];
+        }
+        cursor += best_shift;
+        zoff[static_cast<size_t>(i)] = static_cast<int>(cursor);
+        cursor += n;
+    }
+    const int64_t zlen = cursor;
+    if (zlen > 49000) return PM_OK;  // z would not fit in shared memory: the streaming kernel is used
     std::vector<std::vector<uint16_t>> bins(16 * 32);
     for (int i = 0; i < t; ++i) {
         const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
         for (int64_t p = 0; p < n; ++p) {
             const int a = code(bases[rel[static_cast<size_t>(i)] + p]);
             const int b = p + 1 < n ? code(bases[rel[static_cast<size_t>(i)] + p + 1]) : 0;
-            const int64_t pos = k::kZPad + rel[static_cast<size_t>(i)] + p;
+            const int64_t pos = zoff[static_cast<size_t>(i)] + p;
             bins[static_cast<size_t>((4 * a + b) * 32 + (pos & 31))].push_back(static_cast<uint16_t>(pos));
         }
     }
@@ -211,8 +254,6 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         }
         group_off[static_cast<size_t>(q) + 1] = group_off[static_cast<size_t>(q)] + static_cast<int>(groups);
     }
-    std::vector<int> zoff(static_cast<size_t>(t));
-    for (int i = 0; i < t; ++i) zoff[static_cast<size_t>(i)] = static_cast<int>(k::kZPad + rel[static_cast<size_t>(i)]);
     PM_CUDA(cudaMalloc(&c->d_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
     PM_CUDA(cudaMalloc(&c->d_cls_group_off, sizeof(int) * 17));
     PM_CUDA(cudaMalloc(&c->d_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
@@ -222,6 +263,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     PM_CUDA(cudaStreamSynchronize(c->stream));
     c->zlen = static_cast<int>(zlen);
     c->total_groups = group_off[16];
+    c->group_fill = entries.empty() ? 0.0 : static_cast<double>(total) / static_cast<double>(entries.size());
     return PM_OK;
 }
 
@@ -443,12 +485,13 @@ EmSmemKernel em_smem_kernel_for(int l) {
 }
 
 // must mirror the carve-up at the top of em_refine_smem_kernel
-size_t em_smem_bytes_v2(int nwarps, int G, int zlen) {
+size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t) {
     size_t b = 0;
     b += (128 + 128 + static_cast<size_t>(nwarps) + 6) * 8;                               // thd, D64, llpart, dscal
     b += (256 + static_cast<size_t>(nwarps) * 16 * G + 16 * static_cast<size_t>(G)) * 4;  // T, cpart, Cq
     b += (static_cast<size_t>(nwarps) * k::kNearCap + 128 + 4 + 20) * 4;                  // near_j, prof, iscal, s_off
     b += 8;                                                                               // cons_bits
+    b += (t <= k::kMaxFusedSeqs ? static_cast<size_t>((t + 1) & ~1) : 0) * 4;               // mprev
     b += static_cast<size_t>(zlen) * 4;                                                   // zbuf
     return b + 16;
 }
@@ -532,7 +575,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         const int G = (l + 1) / 2;
         const int nwarps = em_smem_warps_for(c->t);
         const int threads = nwarps * 32;
-        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen);
+        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen, c->t);
         EmSmemKernel kern = em_smem_kernel_for(l);
         PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));

@@ -85,7 +85,39 @@ __device__ __forceinline__ void window_halves(uint64_t hi, uint64_t lo, int lane
     vl = __funnelshift_l(c, b, sh);
 }
 
+// E-step pass A over one sequence: window weights w_j (lane = window).  kExp = false stores w_j;
+// kExp = true stores e_j = exp(w_j - ref) and accumulates their lane sum.  Tracks the lane maximum
+// (strict >, so the earliest offset is kept).
+template <int G, bool kExp>
+__device__ __forceinline__ void estep_pass_a(const float* __restrict__ T, const uint64_t* __restrict__ wp, int W,
+                                             int chunks, int lane, float* __restrict__ zs, float ref, float& best_w,
+                                             int& best_j, float& s_all) {
+    uint64_t hi = wp[0];
+    for (int c = 0; c < chunks; ++c) {
+        const uint64_t lo = wp[c + 1];
+        const int j = (c << 5) + lane;
+        uint32_t vh, vl;
+        window_halves(hi, lo, lane, vh, vl);
+        hi = lo;
+        if (j < W) {
+            const float w = window_weight_tree<G>(T, vh, vl);
+            if (kExp) {
+                const float e = __expf(w - ref);
+                zs[j] = e;
+                s_all += e;
+            } else {
+                zs[j] = w;
+            }
+            if (w > best_w) {
+                best_w = w;
+                best_j = j;
+            }
+        }
+    }
+}
+
 constexpr int kEmSmemMaxWarps = 10;
+constexpr int kMaxFusedSeqs = 1024;  // sequences whose previous per-sequence maximum is kept in smem
 
 template <int G>
 __global__ void __launch_bounds__(kEmSmemMaxWarps * 32, 3)
@@ -108,7 +140,9 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     int* iscal = prof + 128;                            // [0] stop [1] score [2] bad
     int* s_off = iscal + 4;                             // [17] first group of each class (+3 pad)
     unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(s_off + 20);
-    float* zbuf = reinterpret_cast<float*>(cons_bits + 1);  // [zlen]
+    float* mprev = reinterpret_cast<float*>(cons_bits + 1);  // [min(t, kMaxFusedSeqs) rounded to even]
+    const int n_mprev = t <= kMaxFusedSeqs ? ((t + 1) & ~1) : 0;
+    float* zbuf = mprev + n_mprev;                      // [zlen]
 
     int* my_near = near_j + warp * kNearCap;
     const int colshift = 62 - 2 * lane;
@@ -188,24 +222,16 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 const int chunks = (W + 31) >> 5;
                 float* zs = zbuf + x.seq_zoff[i];
 
-                // pass A: window weights, lane-local maximum (strict >: earliest offset kept)
-                float best_w = -INFINITY;
+                // pass A.  From the second iteration on the exp is fused in, taken relative to the
+                // previous iteration's maximum of this sequence (softmax is shift-invariant).
+                const bool fused = !final_pass && iterations > 0 && n_mprev > 0;
+                float ref = fused ? mprev[i] : 0.f;
+                float best_w = -INFINITY, s_all = 0.f;
                 int best_j = 0;
-                uint64_t hi = wp[0];
-                for (int c = 0; c < chunks; ++c) {
-                    const uint64_t lo = wp[c + 1];
-                    const int j = (c << 5) + lane;
-                    uint32_t vh, vl;
-                    window_halves(hi, lo, lane, vh, vl);
-                    hi = lo;
-                    if (j < W) {
-                        const float w = window_weight_tree<G>(T, vh, vl);
-                        zs[j] = w;
-                        if (w > best_w) {
-                            best_w = w;
-                            best_j = j;
-                        }
-                    }
+                if (fused) {
+                    estep_pass_a<G, true>(T, wp, W, chunks, lane, zs, ref, best_w, best_j, s_all);
+                } else {
+                    estep_pass_a<G, false>(T, wp, W, chunks, lane, zs, 0.f, best_w, best_j, s_all);
                 }
                 const float M = warp_max_f(best_w);
                 if (!(M > -INFINITY) || !(M < INFINITY)) iscal[2] = 1;
@@ -274,8 +300,40 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     continue;
                 }
 
-                // pass B: e_j = exp(w_j - M), their sum; windows with w_j >= M + log(eps) are listed
-                float s_all = 0.f, s_far = 0.f;
+                float total = 0.f;
+                bool have_e = false;
+                if (fused) {
+                    total = warp_sum_f(s_all);
+                    const float shift = M - ref;
+                    have_e = shift > -60.f && shift < 60.f && total > 0.f && total < INFINITY;
+                    if (!have_e) {  // the maximum moved too far for FP32 range: redo as two passes
+                        best_w = -INFINITY;
+                        estep_pass_a<G, false>(T, wp, W, chunks, lane, zs, 0.f, best_w, best_j, s_all);
+                        __syncwarp();
+                    }
+                }
+                if (!have_e) {
+                    // pass B (first iteration / fallback): e_j = exp(w_j - M) and their sum
+                    ref = M;
+                    s_all = 0.f;
+                    for (int c = 0; c < chunks; ++c) {
+                        const int j = (c << 5) + lane;
+                        if (j < W) {
+                            const float e = __expf(zs[j] - M);
+                            zs[j] = e;
+                            s_all += e;
+                        }
+                    }
+                    total = warp_sum_f(s_all);
+                }
+                if (!(total > 0.f)) iscal[2] = 1;
+                const float inv_total = 1.f / total;
+                if (n_mprev > 0 && lane == 0) mprev[i] = M;
+                __syncwarp();
+                // pass C: z_j = e_j / sum; windows with w_j >= M + log(eps), i.e. e_j >= exp(M - ref) * eps,
+                // are listed for the FP64 refinement
+                const float near_e = __expf(M - ref + p.log_z_eps);
+                float s_far = 0.f;
                 int nnear = 0;
                 bool overflow = false;
                 for (int c = 0; c < chunks; ++c) {
@@ -283,12 +341,10 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     float e = 0.f;
                     bool keep = false;
                     if (j < W) {
-                        const float w = zs[j];
-                        e = __expf(w - M);
-                        zs[j] = e;
-                        keep = w >= M + p.log_z_eps;
+                        e = zs[j];
+                        zs[j] = e * inv_total;
+                        keep = e >= near_e;
                     }
-                    s_all += e;
                     s_far += keep ? 0.f : e;
                     const unsigned ball = __ballot_sync(0xffffffffu, keep);
                     if (ball && !overflow) {
@@ -300,15 +356,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                         }
                     }
                 }
-                const float total = warp_sum_f(s_all);
-                if (!(total > 0.f)) iscal[2] = 1;
-                const float inv_total = 1.f / total;
-                __syncwarp();
-                // pass C: z_j = e_j / sum
-                for (int c = 0; c < chunks; ++c) {
-                    const int j = (c << 5) + lane;
-                    if (j < W) zs[j] *= inv_total;
-                }
+                s_far *= __expf(ref - M);  // far-tail sum relative to M
                 __syncwarp();
 
                 const unsigned int* sc = p.seq_sym + i * 4;
@@ -333,7 +381,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     if (lane < nnear) zs[my_near[lane]] = static_cast<float>(wa / s64);
                     if (nnear > 32 && lane + 32 < nnear) zs[my_near[lane + 32]] = static_cast<float>(wb / s64);
                 } else {
-                    lse = static_cast<double>(M) + log(static_cast<double>(total));
+                    lse = static_cast<double>(ref) + log(static_cast<double>(total));  // total is relative to ref
                 }
                 // log P(S_i) = log prod theta_bg - log W + logsumexp_j w_ij   (refine.hpp:200)
                 ll_warp += log_base - p.seq_logw[i] + lse;
@@ -380,39 +428,35 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 Cq[q * G + g] = sum;
             }
             __syncthreads();
-            // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64
-            if (threadIdx.x <= l) {
-                double raw[4];
-                if (threadIdx.x < l) {
-                    const int c = threadIdx.x, g = c >> 1;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        double s = 0.0;
-                        for (int o = 0; o < 4; ++o) s += static_cast<double>(Cq[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
-                        raw[r] = s;
-                    }
+            // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64.
+            // Thread e = 4c + r owns theta cell (column c, symbol r); c == l is the background column.
+            // The four lanes of a column exchange their values with shuffles.
+            if (warp < (4 * (l + 1) + 31) / 32) {
+                const int e = threadIdx.x;
+                const bool live = e < 4 * (l + 1);
+                const int c = live ? e >> 2 : 0, r = e & 3;
+                double raw;
+                if (c < l) {
+                    const int g = c >> 1;
+                    raw = 0.0;
+                    for (int o = 0; o < 4; ++o) raw += static_cast<double>(Cq[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
                 } else {
                     // background = symbol totals - expected motif counts, clamped at 0
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        double b = p.tot_sym[r];
-                        for (int c = 0; c < l; ++c) {
-                            const int g = c >> 1;
-                            for (int o = 0; o < 4; ++o) b -= static_cast<double>(Cq[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
-                        }
-                        raw[r] = fmax(b, 0.0);
+                    double b = p.tot_sym[r];
+                    for (int cc = 0; cc < l; ++cc) {
+                        const int g = cc >> 1;
+                        double cnt = 0.0;
+                        for (int o = 0; o < 4; ++o) cnt += static_cast<double>(Cq[((cc & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                        b -= cnt;
                     }
+                    raw = fmax(b, 0.0);
                 }
-                const double sum = raw[0] + raw[1] + raw[2] + raw[3];
-                double fs = 0.0;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    raw[r] = sum > 0.0 ? fmax(raw[r] / sum, 1e-9) : 0.25;
-                    fs += raw[r];
-                }
-                const int col = threadIdx.x < l ? threadIdx.x + 1 : 0;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) thd[col * 4 + r] = raw[r] / fs;
+                double sum = raw + __shfl_xor_sync(0xffffffffu, raw, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                const double v = sum > 0.0 ? fmax(raw / sum, 1e-9) : 0.25;
+                double fs = v + __shfl_xor_sync(0xffffffffu, v, 1);
+                fs += __shfl_xor_sync(0xffffffffu, fs, 2);
+                if (live) thd[(c < l ? c + 1 : 0) * 4 + r] = v / fs;
             }
             ++iterations;
             if (threadIdx.x == 0) {
