@@ -101,6 +101,7 @@ typedef struct pm_run_result {
     int64_t em_lookup_adds;   /* E-step lookup-adds executed: sum over buckets of (iterations+1) * x * l */
     int64_t h2d_bytes;        /* bytes this call copied host->device ... */
     int64_t d2h_bytes;        /* ... and device->host */
+    int64_t em_work;          /* SURVEY §8(d) W_EM: sum_b (2 I_b+1) x l + 4 (I_b+1) x  (E- and M-step work) */
 } pm_run_result;
 
 /* --------------------------------------------------------------------------------------------

@@ -91,7 +91,7 @@ class RunResult(C.Structure):
         ("q", C.c_double), ("t_hat", C.c_int32), ("found", C.c_int32),
         ("within_d", C.c_int32), ("total_distance", C.c_int32),
         ("stage_ms", C.c_double * 8), ("gpu_launches", C.c_int64), ("em_lookup_adds", C.c_int64),
-        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("em_work", C.c_int64),
     ]
 
     def as_dict(self):

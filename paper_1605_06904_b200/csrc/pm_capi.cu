@@ -1224,6 +1224,13 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
     out->em_lookup_adds += static_cast<int64_t>(scal[0]) * c->x * l;
+    {
+        // W_EM = sum_b (2 I_b + 1) x l lookup-adds + 4 (I_b + 1) x; scal[0] = sum_b (I_b + 1)
+        int64_t n_buckets = 0;
+        for (unsigned int nr : n_rec) n_buckets += nr;
+        const int64_t s_iters1 = static_cast<int64_t>(scal[0]);
+        out->em_work += (2 * s_iters1 - n_buckets) * c->x * l + 4 * s_iters1 * c->x;
+    }
 
     // Ascending-trial reduction, driver.hpp:195-208.
     const int perfect = l * c->t;

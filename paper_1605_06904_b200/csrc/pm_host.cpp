@@ -358,6 +358,9 @@ int pm_merge_results(const pm_run_result* parts, const int32_t* const* parts_pos
         acc.wall_ms = std::max(acc.wall_ms, p.wall_ms);
         acc.gpu_launches += p.gpu_launches;
         acc.em_lookup_adds += p.em_lookup_adds;
+        acc.em_work += p.em_work;
+        acc.h2d_bytes += p.h2d_bytes;
+        acc.d2h_bytes += p.d2h_bytes;
         for (int j = 0; j < 8; ++j) acc.stage_ms[j] = std::max(acc.stage_ms[j], p.stage_ms[j]);
         if (p.found && (winner < 0 || pm_candidate_improves(p.score, p.expectation, p.source_bucket, acc.score,
                                                             acc.expectation, acc.source_bucket))) {
