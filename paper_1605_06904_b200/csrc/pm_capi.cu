@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -49,7 +50,7 @@ struct DevBuf {
 enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
-    S_SCAL, S_MEMBERS, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
+    S_SCAL, S_MEMBERS, S_MPREV, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
 };
 
 }  // namespace
@@ -74,7 +75,9 @@ struct pm_ctx {
     uint16_t* d_cls_entries = nullptr;
     int* d_cls_group_off = nullptr;
     int* d_seq_zoff = nullptr;
-    int zlen = 0;          // 0 => the set does not fit the shared-memory EM kernel
+    k::TileDesc* d_tiles = nullptr;
+    int n_tiles = 0;
+    int zlen = 0;          // largest tile's z slots; 0 => some sequence does not fit the shared-memory EM kernel
     int total_groups = 0;
     double group_fill = 0.0;  // live entries / slots of the class-gather rows
     // window index space for the current l
@@ -180,32 +183,49 @@ int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
     return PM_OK;
 }
 
-// Index build for the shared-memory EM kernel (pm_em_smem.cuh): the pair class 4*s_p + s_{p+1} of every base
-// position, grouped per class into warps of 32 positions with pairwise distinct addresses mod 32 so
-// that the M-step gather is free of bank conflicts.  A layout table like word_off, not arithmetic
-// of the path; it depends on the sequence set only (not on l, the plan or the bucket).
+// Index build for the shared-memory EM kernel (pm_em_smem.cuh).  Sequences are split into tiles whose
+// responsibilities fit the kernel's z buffer; per tile, the pair class 4*s_p + s_{p+1} of every base
+// position is grouped per class into rows of 32 slots with pairwise distinct addresses mod 32, so
+// the M-step gather is free of bank conflicts.  A layout table like word_off, not arithmetic of
+// the path; it depends on the sequence set only (not on l, the plan or the bucket).
 int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel, int t) {
     const int64_t total = rel[static_cast<size_t>(t)];
-    if (k::kZPad + total + 32 * static_cast<int64_t>(t) > 49000 && k::kZPad + total > 47000) return PM_OK;
+    // small sets: one tile (every t=20 config); large sets: tiles of ~12.6k slots (3 CTAs per SM)
+    const int64_t single = k::kZPad + total + 32 * static_cast<int64_t>(t);
+    int64_t cap = single <= 21000 ? single : 12600;
+    if (const char* env = std::getenv("PM_B200_TILE_SLOTS")) {  // test knob: force small tiles
+        const long v = std::atol(env);
+        if (v >= 256 && v <= 48000) cap = v;
+    }
     auto code = [](char ch) { return (static_cast<unsigned char>(ch) >> 1) & 3; };
-    // Each sequence may start up to 31 slots later than the previous one ended; the slack is chosen
-    // greedily so that, per class, the positions spread evenly over the 32 address residues (the
-    // number of gather rows of a class is its fullest residue).
-    const bool may_shift = k::kZPad + total + 32 * static_cast<int64_t>(t) <= 49000;
+    std::vector<k::TileDesc> tiles;
     std::vector<int> zoff(static_cast<size_t>(t));
-    std::vector<int> load(16 * 32, 0);
-    std::vector<int> mine(16 * 32);
-    int64_t cursor = k::kZPad;
-    for (int i = 0; i < t; ++i) {
-        const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
-        std::fill(mine.begin(), mine.end(), 0);
-        for (int64_t p = 0; p < n; ++p) {
-            const int a = code(bases[rel[static_cast<size_t>(i)] + p]);
-            const int b = p + 1 < n ? code(bases[rel[static_cast<size_t>(i)] + p + 1]) : 0;
-            ++mine[static_cast<size_t>((4 * a + b) * 32 + ((cursor + p) & 31))];
-        }
-        int best_shift = 0;
-        if (may_shift) {
+    std::vector<int> group_off;  // 17 per tile
+    std::vector<uint16_t> entries;
+    std::vector<int> load(16 * 32), mine(16 * 32);
+    std::vector<std::vector<uint16_t>> bins(16 * 32);
+    int64_t live_slots = 0;
+    int zcap = 0;
+    int i = 0;
+    while (i < t) {
+        k::TileDesc tile;
+        tile.seq_begin = i;
+        tile.group_base = static_cast<int>(entries.size() / 32);
+        std::fill(load.begin(), load.end(), 0);
+        for (auto& b : bins) b.clear();
+        int64_t cursor = k::kZPad;
+        while (i < t) {
+            const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
+            if (cursor + 31 + n > cap) break;
+            const char* sq = bases + rel[static_cast<size_t>(i)];
+            // the slack before this sequence (0..31 slots) is chosen greedily so that, per class, the
+            // positions spread evenly over the 32 address residues (rows of a class = its fullest residue)
+            std::fill(mine.begin(), mine.end(), 0);
+            for (int64_t p = 0; p < n; ++p) {
+                const int q = 4 * code(sq[p]) + (p + 1 < n ? code(sq[p + 1]) : 0);
+                ++mine[static_cast<size_t>(q * 32 + ((cursor + p) & 31))];
+            }
+            int best_shift = 0;
             int64_t best_cost = -1;
             for (int sh = 0; sh < 32; ++sh) {
                 int64_t cost = 0;
@@ -221,49 +241,52 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
                     best_shift = sh;
                 }
             }
-        }
-        for (int q = 0; q < 16; ++q) {
-            for (int r = 0; r < 32; ++r) load[static_cast<size_t>(q * 32 + ((r + best_shift) & 31))] += mine[static_cast<size_t>(q * 32 + r)];
-        }
-        cursor += best_shift;
-        zoff[static_cast<size_t>(i)] = static_cast<int>(cursor);
-        cursor += n;
-    }
-    const int64_t zlen = cursor;
-    if (zlen > 49000) return PM_OK;  // z would not fit in shared memory: the streaming kernel is used
-    std::vector<std::vector<uint16_t>> bins(16 * 32);
-    for (int i = 0; i < t; ++i) {
-        const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
-        for (int64_t p = 0; p < n; ++p) {
-            const int a = code(bases[rel[static_cast<size_t>(i)] + p]);
-            const int b = p + 1 < n ? code(bases[rel[static_cast<size_t>(i)] + p + 1]) : 0;
-            const int64_t pos = zoff[static_cast<size_t>(i)] + p;
-            bins[static_cast<size_t>((4 * a + b) * 32 + (pos & 31))].push_back(static_cast<uint16_t>(pos));
-        }
-    }
-    std::vector<int> group_off(17, 0);
-    std::vector<uint16_t> entries;
-    for (int q = 0; q < 16; ++q) {
-        size_t groups = 0;
-        for (int r = 0; r < 32; ++r) groups = std::max(groups, bins[static_cast<size_t>(q * 32 + r)].size());
-        for (size_t g = 0; g < groups; ++g) {
-            for (int r = 0; r < 32; ++r) {
-                const std::vector<uint16_t>& b = bins[static_cast<size_t>(q * 32 + r)];
-                entries.push_back(g < b.size() ? b[g] : static_cast<uint16_t>(32 + r));  // dummy: a zero slot, same bank
+            for (int q = 0; q < 16; ++q) {
+                for (int r = 0; r < 32; ++r) load[static_cast<size_t>(q * 32 + ((r + best_shift) & 31))] += mine[static_cast<size_t>(q * 32 + r)];
             }
+            cursor += best_shift;
+            zoff[static_cast<size_t>(i)] = static_cast<int>(cursor);
+            for (int64_t p = 0; p < n; ++p) {
+                const int q = 4 * code(sq[p]) + (p + 1 < n ? code(sq[p + 1]) : 0);
+                bins[static_cast<size_t>(q * 32 + ((cursor + p) & 31))].push_back(static_cast<uint16_t>(cursor + p));
+            }
+            cursor += n;
+            live_slots += n;
+            ++i;
         }
-        group_off[static_cast<size_t>(q) + 1] = group_off[static_cast<size_t>(q)] + static_cast<int>(groups);
+        if (i == tile.seq_begin) return PM_OK;  // a single sequence exceeds the z buffer: streaming kernel
+        tile.seq_end = i;
+        tile.zlen = static_cast<int>(cursor);
+        zcap = std::max(zcap, tile.zlen);
+        int row = 0;
+        for (int q = 0; q < 16; ++q) {
+            group_off.push_back(row);
+            size_t rows = 0;
+            for (int r = 0; r < 32; ++r) rows = std::max(rows, bins[static_cast<size_t>(q * 32 + r)].size());
+            for (size_t g = 0; g < rows; ++g) {
+                for (int r = 0; r < 32; ++r) {
+                    const std::vector<uint16_t>& b = bins[static_cast<size_t>(q * 32 + r)];
+                    entries.push_back(g < b.size() ? b[g] : static_cast<uint16_t>(32 + r));  // dummy: zero slot, same bank
+                }
+            }
+            row += static_cast<int>(rows);
+        }
+        group_off.push_back(row);
+        tiles.push_back(tile);
     }
     PM_CUDA(cudaMalloc(&c->d_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
-    PM_CUDA(cudaMalloc(&c->d_cls_group_off, sizeof(int) * 17));
+    PM_CUDA(cudaMalloc(&c->d_cls_group_off, sizeof(int) * group_off.size()));
     PM_CUDA(cudaMalloc(&c->d_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
+    PM_CUDA(cudaMalloc(&c->d_tiles, sizeof(k::TileDesc) * tiles.size()));
     PM_TRY(h2d(c, c->d_cls_entries, entries.data(), sizeof(uint16_t) * entries.size()));
-    PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * 17));
+    PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * group_off.size()));
     PM_TRY(h2d(c, c->d_seq_zoff, zoff.data(), sizeof(int) * zoff.size()));
+    PM_TRY(h2d(c, c->d_tiles, tiles.data(), sizeof(k::TileDesc) * tiles.size()));
     PM_CUDA(cudaStreamSynchronize(c->stream));
-    c->zlen = static_cast<int>(zlen);
-    c->total_groups = group_off[16];
-    c->group_fill = entries.empty() ? 0.0 : static_cast<double>(total) / static_cast<double>(entries.size());
+    c->zlen = zcap;
+    c->n_tiles = static_cast<int>(tiles.size());
+    c->total_groups = static_cast<int>(entries.size() / 32);
+    c->group_fill = entries.empty() ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(entries.size());
     return PM_OK;
 }
 
@@ -582,13 +605,18 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         int per_sm = 0;
         PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         if (per_sm >= 1) {
-            k::EmSmemExtra x;
-            x.cls_entries = c->d_cls_entries;
-            x.cls_group_off = c->d_cls_group_off;
-            x.seq_zoff = c->d_seq_zoff;
-            x.zlen = c->zlen;
             const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
             const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
+            k::EmSmemExtra x;
+            x.tiles = c->d_tiles;
+            x.n_tiles = c->n_tiles;
+            x.cls_entries = c->d_cls_entries;
+            x.tile_group_off = c->d_cls_group_off;
+            x.seq_zoff = c->d_seq_zoff;
+            x.mprev_g = nullptr;
+            if (c->t > k::kMaxFusedSeqs) {
+                PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * static_cast<size_t>(c->t), &x.mprev_g));
+            }
             kern<<<grid, threads, smem, c->stream>>>(p, x);
             return check_launch(c, "em_refine_smem");
         }
@@ -698,6 +726,7 @@ void pm_ctx_destroy(pm_ctx* c) {
     cudaFree(c->d_cls_entries);
     cudaFree(c->d_cls_group_off);
     cudaFree(c->d_seq_zoff);
+    cudaFree(c->d_tiles);
     delete c;
 }
 
@@ -722,6 +751,9 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     cudaFree(c->d_cls_entries);
     cudaFree(c->d_cls_group_off);
     cudaFree(c->d_seq_zoff);
+    cudaFree(c->d_tiles);
+    c->d_tiles = nullptr;
+    c->n_tiles = 0;
     c->d_cls_entries = nullptr;
     c->d_cls_group_off = nullptr;
     c->d_seq_zoff = nullptr;

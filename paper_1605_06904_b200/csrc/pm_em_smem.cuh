@@ -28,11 +28,22 @@ namespace k {
 constexpr int kZPad = 64;    // zero entries in front of the first sequence (dummy lanes read 32..63)
 constexpr int kNearCap = 64; // near-maximum windows re-evaluated in FP64, per warp
 
+// A tile is a run of consecutive sequences whose responsibilities fit the z buffer together; it has
+// its own class-group table.  Small sets (every t=20 config) are a single tile; large sets are
+// swept tile by tile with the class sums accumulated across tiles.
+struct TileDesc {
+    int seq_begin, seq_end;  // sequences [seq_begin, seq_end)
+    int zlen;                // z slots used by the tile (front pad + sequences + balancing gaps)
+    int group_base;          // first row of the tile in cls_entries
+};
+
 struct EmSmemExtra {
-    const uint16_t* cls_entries;  // [total_groups][32] padded flat positions (kZPad + offs_i + p), dummies 32+lane
-    const int* cls_group_off;     // [17] first group of each class
-    const int* seq_zoff;          // [t] kZPad + offs_i
-    int zlen;                     // kZPad + total bases
+    const TileDesc* tiles;
+    int n_tiles;
+    const uint16_t* cls_entries;  // [rows][32] z slots relative to the tile (dummies 32+lane point at the zero pad)
+    const int* tile_group_off;    // [n_tiles][17] first row of each class, relative to group_base
+    const int* seq_zoff;          // [t] first z slot of each sequence within its tile
+    float* mprev_g;               // [gridDim.x][t] previous per-sequence maxima when t > kMaxFusedSeqs
 };
 
 __device__ __forceinline__ double warp_max_d(double v) {
@@ -140,22 +151,13 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     int* iscal = prof + 128;                            // [0] stop [1] score [2] bad
     int* s_off = iscal + 4;                             // [17] first group of each class (+3 pad)
     unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(s_off + 20);
-    float* mprev = reinterpret_cast<float*>(cons_bits + 1);  // [min(t, kMaxFusedSeqs) rounded to even]
+    float* mprev_s = reinterpret_cast<float*>(cons_bits + 1);  // [min(t, kMaxFusedSeqs) rounded to even]
     const int n_mprev = t <= kMaxFusedSeqs ? ((t + 1) & ~1) : 0;
-    float* zbuf = mprev + n_mprev;                      // [zlen]
+    float* zbuf = mprev_s + n_mprev;                    // [max tile zlen]
+    float* mprev = n_mprev > 0 ? mprev_s : x.mprev_g + static_cast<size_t>(blockIdx.x) * t;
 
     int* my_near = near_j + warp * kNearCap;
     const int colshift = 62 - 2 * lane;
-
-    // responsibilities of invalid windows (and the front pad) stay zero for the whole kernel: only
-    // valid windows are ever written, and validity depends on the sequence set alone.
-    for (int i = threadIdx.x; i < x.zlen; i += blockDim.x) zbuf[i] = 0.f;
-    if (threadIdx.x < 17) s_off[threadIdx.x] = x.cls_group_off[threadIdx.x];
-
-    // M-step work split: contiguous ranges of (class, group) items per warp, fixed => deterministic
-    const int total_groups = x.cls_group_off[16];  // (read before s_off is populated)
-    const int item_lo = static_cast<int>(static_cast<long long>(total_groups) * warp / nwarps);
-    const int item_hi = static_cast<int>(static_cast<long long>(total_groups) * (warp + 1) / nwarps);
 
     const unsigned int n_work = p.n_work_dev ? *p.n_work_dev : p.n_work;
     for (unsigned int wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
@@ -214,17 +216,28 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             }
             __syncthreads();
 
-            // ================= E-step: warp per sequence =================
             double ll_warp = 0.0;
-            for (int i = warp; i < t; i += nwarps) {
+            for (int e = lane; e < 16 * G; e += 32) cpart[warp * 16 * G + e] = 0.f;  // this warp's class sums
+            for (int tile_i = 0; tile_i < x.n_tiles; ++tile_i) {
+            const TileDesc tile = x.tiles[tile_i];
+            // ================= E-step: warp per sequence of the tile =================
+            if (threadIdx.x < 17) s_off[threadIdx.x] = x.tile_group_off[tile_i * 17 + threadIdx.x];
+            for (int k = threadIdx.x, k_end = x.seq_zoff[tile.seq_begin]; k < k_end; k += blockDim.x) zbuf[k] = 0.f;  // front pad
+            for (int i = tile.seq_begin + warp; i < tile.seq_end; i += nwarps) {
                 const uint64_t* __restrict__ wp = p.words + p.word_off[i];
                 const int W = p.seq_len[i] - l + 1;
                 const int chunks = (W + 31) >> 5;
                 float* zs = zbuf + x.seq_zoff[i];
+                {
+                    // slots that are not window starts (the last l-1 bases and the balancing gap up to the
+                    // next sequence) read as zero in the M-step gather
+                    const int z_end = (i + 1 < tile.seq_end ? x.seq_zoff[i + 1] : tile.zlen) - x.seq_zoff[i];
+                    for (int k = W + lane; k < z_end; k += 32) zs[k] = 0.f;
+                }
 
                 // pass A.  From the second iteration on the exp is fused in, taken relative to the
                 // previous iteration's maximum of this sequence (softmax is shift-invariant).
-                const bool fused = !final_pass && iterations > 0 && n_mprev > 0;
+                const bool fused = !final_pass && iterations > 0;
                 float ref = fused ? mprev[i] : 0.f;
                 float best_w = -INFINITY, s_all = 0.f;
                 int best_j = 0;
@@ -328,7 +341,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 }
                 if (!(total > 0.f)) iscal[2] = 1;
                 const float inv_total = 1.f / total;
-                if (n_mprev > 0 && lane == 0) mprev[i] = M;
+                if (lane == 0) mprev[i] = M;
                 __syncwarp();
                 // pass C: z_j = e_j / sum; windows with w_j >= M + log(eps), i.e. e_j >= exp(M - ref) * eps,
                 // are listed for the FP64 refinement
@@ -387,45 +400,51 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 ll_warp += log_base - p.seq_logw[i] + lse;
                 __syncwarp();
             }
+            if (final_pass) {  // the final sweep has no M-step
+                if (tile_i + 1 < x.n_tiles) __syncthreads();  // the next tile reuses the z buffer
+                continue;
+            }
+            __syncthreads();
+
+            // ================= M-step of the tile: conflict-free class gather =================
+            {
+                const int total_groups = s_off[16];
+                const int item_lo = static_cast<int>(static_cast<long long>(total_groups) * warp / nwarps);
+                const int item_hi = static_cast<int>(static_cast<long long>(total_groups) * (warp + 1) / nwarps);
+                const uint16_t* __restrict__ rows = x.cls_entries + static_cast<size_t>(tile.group_base) * 32;
+                for (int q = 0; q < 16; ++q) {
+                    const int a = max(item_lo, s_off[q]), b = min(item_hi, s_off[q + 1]);
+                    if (a >= b) continue;  // this warp owns no row of class q
+                    float acc[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) acc[g] = 0.f;
+                    const uint16_t* __restrict__ ent = rows + static_cast<size_t>(a) * 32 + lane;
+                    int pos = ent[0];
+                    for (int it = a; it < b; ++it) {
+                        ent += 32;
+                        const int nxt = it + 1 < b ? static_cast<int>(ent[0]) : 0;  // prefetch the next row
+                        const float* zp = zbuf + pos;
+#pragma unroll
+                        for (int g = 0; g < G; ++g) acc[g] += zp[-2 * g];
+                        pos = nxt;
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float sum = warp_sum_f(acc[g]);
+                        if (lane == 0) cpart[(warp * 16 + q) * G + g] += sum;
+                    }
+                }
+            }
+            if (tile_i + 1 < x.n_tiles) __syncthreads();  // z buffer and s_off are reused by the next tile
+            }  // tiles
             if (final_pass) break;
             if (lane == 0) llpart[warp] = ll_warp;
             __syncthreads();
-
-            // ================= M-step: conflict-free class gather =================
-            for (int q = 0; q < 16; ++q) {
-                const int a = max(item_lo, s_off[q]), b = min(item_hi, s_off[q + 1]);
-                if (a >= b) continue;  // this warp owns no group of class q
-                float acc[G];
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc[g] = 0.f;
-                const uint16_t* __restrict__ ent = x.cls_entries + static_cast<size_t>(a) * 32 + lane;
-                int pos = ent[0];
-                for (int it = a; it < b; ++it) {
-                    ent += 32;
-                    const int nxt = it + 1 < b ? static_cast<int>(ent[0]) : 0;  // prefetch the next group
-                    const float* zp = zbuf + pos;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[g] += zp[-2 * g];
-                    pos = nxt;
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float sum = warp_sum_f(acc[g]);
-                    if (lane == 0) cpart[(warp * 16 + q) * G + g] = sum;
-                }
-            }
-            __syncthreads();
-            // C[q][g] = sum over the warps that own groups of class q, in warp order
+            // C[q][g] = sum of the per-warp class sums, in warp order
             for (int e = threadIdx.x; e < 16 * G; e += blockDim.x) {
-                const int q = e / G, g = e - q * G;
-                const int g_lo = s_off[q], g_hi = s_off[q + 1];
                 float sum = 0.f;
-                for (int w = 0; w < nwarps; ++w) {
-                    const int lo = static_cast<int>(static_cast<long long>(total_groups) * w / nwarps);
-                    const int hi = static_cast<int>(static_cast<long long>(total_groups) * (w + 1) / nwarps);
-                    if (max(lo, g_lo) < min(hi, g_hi)) sum += cpart[(w * 16 + q) * G + g];
-                }
-                Cq[q * G + g] = sum;
+                for (int w = 0; w < nwarps; ++w) sum += cpart[w * 16 * G + e];
+                Cq[e] = sum;
             }
             __syncthreads();
             // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64.

@@ -175,3 +175,18 @@ def test_cpp_host_layer(pm):
     out = subprocess.run([exe], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "all checks passed" in out.stdout
+
+
+def test_run_with_more_than_1024_sequences(ctx, port):
+    """t = 1100 short sequences: multi-tile EM with the per-sequence maxima kept in global memory."""
+    rng = np.random.default_rng(3)
+    strings = ["".join(rng.choice(list("ACGT"), 40)) for _ in range(1100)]
+    ss = pmo.SeqSet.from_strings(strings)
+    kw = dict(l=10, d=2, k=8, s=6, m=2, seed=5, early_stop=0)
+    ctx.set_sequences(ss.bases, ss.offs)
+    got = ctx.run(per_trial=True, **kw)
+    b, sc, ex, key = port.trial_outcomes(ss, 1, 2, **kw)
+    assert got["trial_buckets"].tolist() == b.tolist()
+    assert got["trial_score"].tolist() == sc.tolist()
+    assert [int(v) for v in got["trial_key"]] == [int(v) for v in key]
+    np.testing.assert_allclose(got["trial_expectation"], ex, atol=EXPECTATION_TOL, rtol=0)

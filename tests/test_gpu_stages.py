@@ -247,3 +247,44 @@ def test_score_and_hamming_scan_match_oracle(ctx, best_oracle):
     ss = pmo.SeqSet.from_strings(["AT", "CG"])
     ctx.set_sequences(ss.bases, ss.offs)
     assert ctx.score(2, [1, 1]) == (2, "AT")
+
+
+def test_tiled_em_equals_single_tile_and_reference(pm, golden, instance):
+    """Large sets are swept in sequence tiles; forcing small tiles on a golden
+    instance must reproduce the reference candidates exactly like the single-tile layout."""
+    import os
+    g = [x for x in golden["refine"] if x["instance"][1] == 600][:10]
+    ss, _, _ = instance(*g[0]["instance"])
+    results = {}
+    for slots in (None, 4000, 1500):
+        if slots is None:
+            os.environ.pop("PM_B200_TILE_SLOTS", None)
+        else:
+            os.environ["PM_B200_TILE_SLOTS"] = str(slots)
+        try:
+            with pm.Context(0) as c:
+                c.set_sequences(ss.bases, ss.offs)
+                results[slots] = c.refine(15, [x["members"] for x in g])
+        finally:
+            os.environ.pop("PM_B200_TILE_SLOTS", None)
+    for slots, res in results.items():
+        for a, x in zip(res, g):
+            check_candidate(a, x["consensus"], x["positions"], x["score"], x["iterations"], x["expectation"], x["theta"])
+    for a, b in zip(results[None], results[1500]):
+        assert np.abs(a["theta"] - b["theta"]).max() < 1e-6
+
+
+def test_many_sequences_multi_tile_matches_oracle(ctx, best_oracle):
+    """t = 300 ragged sequences (about 60k bases => several tiles, previous maxima in global memory
+    is exercised separately by t > 1024 in test_gpu_run)."""
+    rng = np.random.default_rng(99)
+    ss = random_set(rng, 300, 150, 250)
+    l, kept = 11, [1, 2, 4, 5, 7, 8, 10, 11]
+    ctx.set_sequences(ss.bases, ss.offs)
+    en = best_oracle.enriched(ss, l, kept, 5, 300 * 5)
+    assert ctx.enriched_buckets(l, kept, 5, 300 * 5) == en
+    pick = en[:6]
+    got = ctx.refine(l, [e["members"] for e in pick])
+    for e, a in zip(pick, got):
+        w = best_oracle.refine(ss, l, e["members"], e["key"])
+        check_candidate(a, w.consensus, w.positions, w.score, w.iterations, w.expectation, w.theta)
