@@ -38,6 +38,9 @@ CONFIGS = {
     "c2": dict(t=20, n=1000, l=16, d=5, k=7, s=4, m=1293, label="C2 planted (16,5) t=20 n=1000 k=7 s=4"),
     "c3": dict(t=20, n=1000, l=18, d=6, k=7, s=4, m=2218, label="C3 planted (18,6) t=20 n=1000 k=7 s=4"),
     "c4": dict(t=20, n=1000, l=20, d=7, k=7, s=4, m=3421, label="C4 planted (20,7) t=20 n=1000 k=7 s=4"),
+    # large-scale sweep; k, s are what the reference derives for this size (k=l-d-1, s=ceil(2x/4^k)); m explicit
+    "c5": dict(t=10000, n=1000, l=15, d=4, k=10, s=19, m=2, label="C5 planted (15,4) t=10000 n=1000 k=10 s=19",
+               extrapolate_cpu=True),
 }
 INSTANCE_SEED = 42
 RUN_SEED = 7
@@ -133,6 +136,31 @@ def cpu_trials_per_second(oracle, kind, ss, cfg, trials, workers):
     return trials / dt, dt
 
 
+def cpu_extrapolated_trials_per_second(oracle, ss, cfg, workers, n_buckets_sample=16):
+    """C5: a full CPU trial is hours.  Time hash_trial+enriched_buckets of one trial in full and
+    refine() on a sample of its buckets (spread over `workers` threads), then extrapolate:
+    trial time = t_hash + n_buckets * mean(t_refine) / workers.  Labelled as extrapolated."""
+    from concurrent.futures import ThreadPoolExecutor
+    kept = oracle.trial_plan(cfg["l"], cfg["k"], RUN_SEED, 1)
+    t0 = time.perf_counter()
+    en = oracle.enriched(ss, cfg["l"], kept, cfg["s"], ss.t * cfg["s"])
+    t_hash = time.perf_counter() - t0
+    step = max(1, len(en) // n_buckets_sample)
+    pick = en[::step][:n_buckets_sample]
+
+    def one(e):
+        a = time.perf_counter()
+        oracle.refine(ss, cfg["l"], e["members"], e["key"], want_theta=False)
+        return time.perf_counter() - a
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        per = list(ex.map(one, pick))
+    wall = time.perf_counter() - t0
+    t_trial = t_hash + len(en) * (sum(per) / len(per)) / workers
+    return 1.0 / t_trial, dict(t_hash_s=t_hash, buckets=len(en), refine_s_mean=sum(per) / len(per), sampled=len(pick),
+                               sample_wall_s=wall + t_hash)
+
+
 def run_reference_arm(args, cfg, rank, world):
     if rank != 0:
         return  # rank 0 alone runs the CPU arm
@@ -140,6 +168,22 @@ def run_reference_arm(args, cfg, rank, world):
     ss, _, _ = oracle.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], INSTANCE_SEED)
     cores = os.cpu_count() or 1
     workers = cores if kind == "reference" else 1  # the C port is a scalar single-thread restatement
+    if cfg.get("extrapolate_cpu"):
+        vals, info = [], None
+        for _ in range(max(1, min(args.steps, 2))):
+            v, info = cpu_extrapolated_trials_per_second(oracle, ss, cfg, cores)
+            vals.append(v)
+        value = sum(vals) / len(vals)
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(vals),
+                "warmup": 0, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["label"], "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED,
+                           "note": "EXTRAPOLATED: hashing in full + refine() on sampled buckets, see cpu_baseline.sample"},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                                 "sample": f"extrapolated from {info}"},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+        return
     sample = max(workers, 2) * (1 if cfg["n"] > 600 else 2)  # trials per step: ~1-3 s of host time
     for _ in range(args.warmup):
         cpu_trials_per_second(oracle, kind, ss, cfg, sample, workers)
@@ -318,7 +362,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "clocks": clocks,
     }
 
-    if not args.no_extras:
+    if not args.no_extras and cfg["t"] <= 100:
         line["time_to_motif"] = time_to_motif(pm, ctx, cfg)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)
@@ -358,6 +402,9 @@ def cpu_baseline(cfg):
     ss, _, _ = oracle.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], INSTANCE_SEED)
     cores = os.cpu_count() or 1
     workers = cores if kind == "reference" else 1
+    if cfg.get("extrapolate_cpu"):
+        value, info = cpu_extrapolated_trials_per_second(oracle, ss, cfg, cores)
+        return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": f"EXTRAPOLATED from {info}"}
     # calibrate on `workers` trials, then size the sample for ~15 s of wall time
     rate, dt = cpu_trials_per_second(oracle, kind, ss, cfg, max(workers, 2), workers)
     sample = int(max(workers, rate * 15.0))  # ~15 s; trials are i.i.d. in cost, so the sample may exceed m

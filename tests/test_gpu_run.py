@@ -190,3 +190,40 @@ def test_run_with_more_than_1024_sequences(ctx, port):
     assert got["trial_score"].tolist() == sc.tolist()
     assert [int(v) for v in got["trial_key"]] == [int(v) for v in key]
     np.testing.assert_allclose(got["trial_expectation"], ex, atol=EXPECTATION_TOL, rtol=0)
+
+
+def test_large_scale_c5_hashing_and_one_bucket(pm, ctx, port):
+    """BASELINE config 5 at full size (t=10,000 x n=1000, (15,4), k=10, s=19): every key and every
+    enriched list bit-exact, one bucket's EM against the oracle (a full CPU trial would take hours)."""
+    bases, offs, motif, _ = pm.generate_planted(10000, 1000, 15, 4, 42)
+    ss = pmo.SeqSet(bases, offs)
+    ctx.set_sequences(bases, offs)
+    kept = pm.trial_plan(15, 10, 7, 1)
+    assert (ctx.hash_keys(15, kept) == port.hash_keys(ss, 15, kept)).all()
+    want = port.enriched(ss, 15, kept, 19, 10000 * 19)
+    got = ctx.enriched_buckets(15, kept, 19, 10000 * 19)
+    assert got == want and len(got) > 5000
+    e = want[len(want) // 3]
+    a = ctx.refine(15, [e["members"]])[0]
+    w = port.refine(ss, 15, e["members"], e["key"])
+    assert (a["consensus"], a["score"], a["iterations"], a["positions"]) == (w.consensus, w.score, w.iterations, w.positions)
+    assert np.abs(a["theta"] - w.theta).max() <= 1e-4 and abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+
+
+def test_degenerate_shapes_match_oracle(ctx, best_oracle):
+    """Edge shapes the reference accepts: one sequence, one window per sequence (n == l), l = 1,
+    identity projection (k == l), windows fewer than a warp, s = 1."""
+    cases = [
+        (["ACGTACGTACGTAAACCC"], dict(l=4, d=1, k=2, s=2, m=3, seed=1, early_stop=0)),
+        (["ACGTAC", "ACGTTC", "ACGAAC", "TTGTAC"], dict(l=6, d=1, k=4, s=2, m=4, seed=2, early_stop=0)),   # n == l
+        (["ACGT" * 5, "TTGA" * 6, "CCAG" * 4], dict(l=1, d=0, k=1, s=1, m=1, seed=3, early_stop=0)),        # l = 1
+        (["ACGTTGCAAGCT" * 3, "ACGTTGCATGCT" * 3, "GGGTTGCAAGCA" * 2], dict(l=8, d=1, k=8, s=2, m=1, seed=4, early_stop=0)),  # k == l
+        (["A" * 40, "A" * 35], dict(l=5, d=0, k=3, s=1, m=1, seed=5, early_stop=0)),                       # all windows identical
+    ]
+    for strings, kw in cases:
+        ss = pmo.SeqSet.from_strings(strings)
+        ctx.set_sequences(ss.bases, ss.offs)
+        got, want = ctx.run(**kw), best_oracle.run(ss, **kw)
+        for f in ("consensus", "score", "positions", "iterations", "source_bucket", "best_trial", "trials_run", "buckets_enriched"):
+            assert got[f] == want[f], (strings[0][:12], f, got[f], want[f])
+        assert abs(got["expectation"] - want["expectation"]) <= EXPECTATION_TOL
