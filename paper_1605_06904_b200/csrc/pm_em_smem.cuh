@@ -96,34 +96,58 @@ __device__ __forceinline__ void window_halves(uint64_t hi, uint64_t lo, int lane
     vl = __funnelshift_l(c, b, sh);
 }
 
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
 // E-step pass A over one sequence: window weights w_j (lane = window).  kExp = false stores w_j;
-// kExp = true stores e_j = exp(w_j - ref) and accumulates their lane sum.  Tracks the lane maximum
-// (strict >, so the earliest offset is kept).
-template <int G, bool kExp>
+// kExp = true stores e_j = exp(w_j - ref) = 2^(w_j log2e - ref2) and accumulates their lane sum.
+// kArg tracks the lane's first maximum and its offset (final sweep), otherwise only the maximum.
+template <int G, bool kExp, bool kArg>
+__device__ __forceinline__ void estep_window(const float* __restrict__ T, uint32_t vh, uint32_t vl, int j,
+                                             float* __restrict__ zs, float ref2, float& best_w, int& best_j,
+                                             float& s_all) {
+    const float w = window_weight_tree<G>(T, vh, vl);
+    if (kExp) {
+        const float e = fast_ex2(fmaf(w, kLog2e, -ref2));
+        zs[j] = e;
+        s_all += e;
+    } else {
+        zs[j] = w;
+    }
+    if (kArg) {
+        if (w > best_w) {  // strict: the earliest offset is kept
+            best_w = w;
+            best_j = j;
+        }
+    } else {
+        best_w = fmaxf(best_w, w);
+    }
+}
+
+template <int G, bool kExp, bool kArg>
 __device__ __forceinline__ void estep_pass_a(const float* __restrict__ T, const uint64_t* __restrict__ wp, int W,
-                                             int chunks, int lane, float* __restrict__ zs, float ref, float& best_w,
+                                             int lane, float* __restrict__ zs, float ref, float& best_w,
                                              int& best_j, float& s_all) {
+    const float ref2 = ref * kLog2e;
+    const int full = W >> 5;  // chunks in which every lane has a window
     uint64_t hi = wp[0];
-    for (int c = 0; c < chunks; ++c) {
+    int c = 0;
+    for (; c < full; ++c) {
         const uint64_t lo = wp[c + 1];
-        const int j = (c << 5) + lane;
         uint32_t vh, vl;
         window_halves(hi, lo, lane, vh, vl);
         hi = lo;
-        if (j < W) {
-            const float w = window_weight_tree<G>(T, vh, vl);
-            if (kExp) {
-                const float e = __expf(w - ref);
-                zs[j] = e;
-                s_all += e;
-            } else {
-                zs[j] = w;
-            }
-            if (w > best_w) {
-                best_w = w;
-                best_j = j;
-            }
-        }
+        estep_window<G, kExp, kArg>(T, vh, vl, (c << 5) + lane, zs, ref2, best_w, best_j, s_all);
+    }
+    const int j = (c << 5) + lane;
+    if (j < W) {  // ragged tail
+        uint32_t vh, vl;
+        window_halves(hi, wp[c + 1], lane, vh, vl);
+        estep_window<G, kExp, kArg>(T, vh, vl, j, zs, ref2, best_w, best_j, s_all);
     }
 }
 
@@ -242,9 +266,11 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 float best_w = -INFINITY, s_all = 0.f;
                 int best_j = 0;
                 if (fused) {
-                    estep_pass_a<G, true>(T, wp, W, chunks, lane, zs, ref, best_w, best_j, s_all);
+                    estep_pass_a<G, true, false>(T, wp, W, lane, zs, ref, best_w, best_j, s_all);
+                } else if (final_pass) {
+                    estep_pass_a<G, false, true>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
                 } else {
-                    estep_pass_a<G, false>(T, wp, W, chunks, lane, zs, 0.f, best_w, best_j, s_all);
+                    estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
                 }
                 const float M = warp_max_f(best_w);
                 if (!(M > -INFINITY) || !(M < INFINITY)) iscal[2] = 1;
@@ -321,7 +347,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     have_e = shift > -60.f && shift < 60.f && total > 0.f && total < INFINITY;
                     if (!have_e) {  // the maximum moved too far for FP32 range: redo as two passes
                         best_w = -INFINITY;
-                        estep_pass_a<G, false>(T, wp, W, chunks, lane, zs, 0.f, best_w, best_j, s_all);
+                        estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
                         __syncwarp();
                     }
                 }
@@ -332,7 +358,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     for (int c = 0; c < chunks; ++c) {
                         const int j = (c << 5) + lane;
                         if (j < W) {
-                            const float e = __expf(zs[j] - M);
+                            const float e = fast_ex2((zs[j] - M) * kLog2e);
                             zs[j] = e;
                             s_all += e;
                         }
