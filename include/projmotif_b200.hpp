@@ -17,7 +17,10 @@
 // All heavy work happens in libpm_b200.so on the GPU; nothing here computes the path on the CPU.
 // Link with -lpm_b200 (paper_1605_06904_b200/libpm_b200.so).
 #pragma once
+#include <cctype>
+#include <charconv>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -35,7 +38,11 @@ namespace projmotif_b200 {
 struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ParamError : Error { using Error::Error; };
 struct ParseError : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
 struct UnknownSymbolError : ParseError { using ParseError::ParseError; };
+struct EmptyInputError : ParseError { using ParseError::ParseError; };
+struct RecordWithoutSequenceError : ParseError { using ParseError::ParseError; };
+struct FastaFormatError : ParseError { using ParseError::ParseError; };
 struct KmerTooLongError : ParamError { using ParamError::ParamError; };
 struct IndexOutOfRangeError : ParamError { using ParamError::ParamError; };
 struct LengthMismatchError : ParamError { using ParamError::ParamError; };
@@ -81,14 +88,21 @@ struct LmerRef {
 
 class SequenceSet {
 public:
-    explicit SequenceSet(std::vector<std::string> sequences) : seqs_(std::move(sequences)) {
+    explicit SequenceSet(std::vector<std::string> sequences, std::vector<std::string> names = {})
+        : seqs_(std::move(sequences)), names_(std::move(names)) {
         if (seqs_.empty()) throw InvalidParamsError("a sequence set needs at least one sequence");
+        if (!names_.empty() && names_.size() != seqs_.size()) {
+            throw InvalidParamsError("sequence names must match the sequence count");
+        }
+        if (names_.empty()) {
+            for (std::size_t i = 0; i < seqs_.size(); ++i) names_.push_back("seq" + std::to_string(i + 1));
+        }
         offs_.assign(seqs_.size() + 1, 0);
         for (std::size_t i = 0; i < seqs_.size(); ++i) {
-            if (seqs_[i].empty()) throw InvalidParamsError("sequence 'seq" + std::to_string(i + 1) + "' is empty");
+            if (seqs_[i].empty()) throw InvalidParamsError("sequence '" + names_[i] + "' is empty");
             for (char c : seqs_[i]) {
                 if (c != 'A' && c != 'C' && c != 'G' && c != 'T') {
-                    throw UnknownSymbolError(std::string("symbol '") + c + "' in sequence 'seq" + std::to_string(i + 1) +
+                    throw UnknownSymbolError(std::string("symbol '") + c + "' in sequence '" + names_[i] +
                                              "' is not in alphabet \"ACTG\"");
                 }
             }
@@ -99,6 +113,7 @@ public:
     int count() const { return static_cast<int>(seqs_.size()); }
     int length(int i) const { return static_cast<int>(seqs_.at(static_cast<std::size_t>(i - 1)).size()); }
     const std::string& sequence(int i) const { return seqs_.at(static_cast<std::size_t>(i - 1)); }
+    const std::string& name(int i) const { return names_.at(static_cast<std::size_t>(i - 1)); }
     int window_count(int i, int l) const {
         const int w = length(i) - l + 1;
         if (l < 1 || w < 1) throw InvalidParamsError("sequence has no l-mer of length " + std::to_string(l));
@@ -135,6 +150,7 @@ public:
 
 private:
     std::vector<std::string> seqs_;
+    std::vector<std::string> names_;
     std::string bases_;
     std::vector<std::int64_t> offs_;
 };
@@ -460,6 +476,188 @@ inline RunResult run(const RunConfig& config, const SequenceSet& seqs) {
     out.within_d = r.within_d;
     out.total_distance = r.total_distance;
     return out;
+}
+
+// ---- fasta.hpp:18-97 (host text I/O)
+inline SequenceSet parse_fasta(std::string_view text) {
+    std::vector<std::string> names, seqs;
+    int line_no = 0;
+    std::size_t pos = 0;
+    bool in_record = false;
+    while (pos <= text.size()) {
+        const std::size_t eol = text.find('\n', pos);
+        std::string_view line = text.substr(pos, (eol == std::string_view::npos ? text.size() : eol) - pos);
+        pos = eol == std::string_view::npos ? text.size() + 1 : eol + 1;
+        ++line_no;
+        while (!line.empty() && (line.back() == '\r' || line.back() == ' ' || line.back() == '\t')) line.remove_suffix(1);
+        if (line.empty()) continue;
+        if (line.front() == '>') {
+            if (in_record && seqs.back().empty()) {
+                throw RecordWithoutSequenceError("record '" + names.back() + "' has no sequence data");
+            }
+            std::string_view header = line.substr(1);
+            while (!header.empty() && (header.front() == ' ' || header.front() == '\t')) header.remove_prefix(1);
+            names.emplace_back(header);
+            seqs.emplace_back();
+            in_record = true;
+            continue;
+        }
+        if (!in_record) {
+            throw FastaFormatError("sequence data before the first '>' header at line " + std::to_string(line_no));
+        }
+        for (char raw : line) {
+            if (raw == ' ' || raw == '\t') continue;
+            const char c = static_cast<char>(std::toupper(static_cast<unsigned char>(raw)));
+            if (c != 'A' && c != 'C' && c != 'G' && c != 'T') {
+                throw UnknownSymbolError(std::string("unknown symbol '") + raw + "' in record '" + names.back() +
+                                         "' at line " + std::to_string(line_no));
+            }
+            seqs.back().push_back(c);
+        }
+    }
+    if (seqs.empty()) throw EmptyInputError("FASTA input contains no records");
+    if (in_record && seqs.back().empty()) {
+        throw RecordWithoutSequenceError("record '" + names.back() + "' has no sequence data");
+    }
+    return SequenceSet(std::move(seqs), std::move(names));
+}
+
+inline std::string serialize_fasta(const SequenceSet& seqs, int line_width = 60) {
+    if (line_width < 1) throw InvalidParamsError("FASTA line width must be positive");
+    std::string out;
+    for (int i = 1; i <= seqs.count(); ++i) {
+        out += '>';
+        out += seqs.name(i);
+        out += '\n';
+        const std::string& s = seqs.sequence(i);
+        for (std::size_t start = 0; start < s.size(); start += static_cast<std::size_t>(line_width)) {
+            out += s.substr(start, static_cast<std::size_t>(line_width));
+            out += '\n';
+        }
+    }
+    return out;
+}
+
+// ---- planted.hpp:38-101
+struct PlantedInstance {
+    SequenceSet sequences;
+    std::string motif;
+    StartVector positions;
+    int l = 0;
+    int d = 0;
+    std::uint64_t seed = 0;
+};
+
+inline PlantedInstance generate_planted(int t, int n, int l, int d, std::uint64_t seed) {
+    std::string bases(static_cast<std::size_t>(t > 0 ? t : 0) * static_cast<std::size_t>(n > 0 ? n : 0), 'A');
+    std::string motif(static_cast<std::size_t>(l > 0 ? l : 0), 'A');
+    std::vector<std::int32_t> pos(static_cast<std::size_t>(t > 0 ? t : 1));
+    detail::check(pm_generate_planted(t, n, l, d, seed, bases.data(), motif.data(), pos.data()));
+    std::vector<std::string> seqs;
+    for (int i = 0; i < t; ++i) seqs.push_back(bases.substr(static_cast<std::size_t>(i) * static_cast<std::size_t>(n), static_cast<std::size_t>(n)));
+    return PlantedInstance{SequenceSet(std::move(seqs)), motif, StartVector(pos.begin(), pos.begin() + t), l, d, seed};
+}
+
+// ---- report.hpp:15-64 (schema v1).  The reference renders with nlohmann::ordered_json::dump(2);
+// the writer below reproduces that layout byte for byte (insertion order, two-space indent, one
+// array element per line, shortest round-trip doubles with a trailing ".0" for integral values).
+namespace detail {
+inline std::string json_double(double v) {
+    char buf[64];
+    const auto res = std::to_chars(buf, buf + sizeof(buf), v);
+    std::string s(buf, res.ptr);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";  // 'n' keeps inf/nan untouched
+    return s;
+}
+inline std::string json_string(const std::string& v) {
+    std::string out = "\"";
+    for (char c : v) {
+        switch (c) {
+            case '"': out += "\\\""; break;
+            case '\\': out += "\\\\"; break;
+            case '\n': out += "\\n"; break;
+            case '\t': out += "\\t"; break;
+            case '\r': out += "\\r"; break;
+            default:
+                if (static_cast<unsigned char>(c) < 0x20) {
+                    char esc[8];
+                    std::snprintf(esc, sizeof(esc), "\\u%04x", c);
+                    out += esc;
+                } else {
+                    out += c;
+                }
+        }
+    }
+    return out + "\"";
+}
+inline std::string json_int_array(const std::vector<int>& v, const std::string& indent) {
+    if (v.empty()) return "[]";
+    std::string out = "[\n";
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        out += indent + "  " + std::to_string(v[i]) + (i + 1 < v.size() ? ",\n" : "\n");
+    }
+    return out + indent + "]";
+}
+inline std::string format_ms(double ms) {  // driver.hpp:237-241
+    char buf[32];
+    std::snprintf(buf, sizeof(buf), "%.3f", ms);
+    return buf;
+}
+}  // namespace detail
+
+inline constexpr int kResultSchemaVersion = 1;
+
+inline std::string render_result_json(const RunResult& r) {
+    std::string o = "{\n";
+    o += "  \"version\": " + std::to_string(kResultSchemaVersion) + ",\n";
+    o += "  \"params\": {\n";
+    o += "    \"l\": " + std::to_string(r.params.l) + ",\n";
+    o += "    \"d\": " + std::to_string(r.params.d) + ",\n";
+    o += "    \"k\": " + std::to_string(r.params.k) + ",\n";
+    o += "    \"s\": " + std::to_string(r.params.s) + ",\n";
+    o += "    \"m\": " + std::to_string(r.params.m) + ",\n";
+    o += "    \"q\": " + detail::json_double(r.params.q) + ",\n";
+    o += "    \"seed\": " + std::to_string(r.seed) + "\n";
+    o += "  },\n";
+    o += "  \"best\": {\n";
+    o += "    \"motif\": " + detail::json_string(r.best.consensus) + ",\n";
+    o += "    \"score\": " + std::to_string(r.best.score) + ",\n";
+    o += "    \"expectation\": " + detail::json_double(r.best.expectation) + ",\n";
+    o += "    \"positions\": " + detail::json_int_array(r.best.positions, "    ") + ",\n";
+    o += "    \"source_bucket\": " + std::to_string(r.best.source_bucket) + ",\n";
+    o += "    \"trial\": " + std::to_string(r.best_trial) + "\n";
+    o += "  },\n";
+    o += "  \"stats\": {\n";
+    o += "    \"trials_run\": " + std::to_string(r.trials_run) + ",\n";
+    o += "    \"buckets_enriched\": " + std::to_string(r.buckets_enriched) + ",\n";
+    o += "    \"wall_ms\": " + detail::json_double(r.wall_ms) + "\n";
+    o += "  }\n";
+    o += "}\n";
+    return o;
+}
+
+inline std::string render_result_tsv(const RunResult& r) {
+    std::string positions;
+    for (std::size_t i = 0; i < r.best.positions.size(); ++i) {
+        if (i > 0) positions += ',';
+        positions += std::to_string(r.best.positions[i]);
+    }
+    std::string out = "motif\tscore\texpectation\tpositions\tsource_bucket\ttrial\ttrials_run\tbuckets_enriched\twall_ms\n";
+    out += r.best.consensus + "\t" + std::to_string(r.best.score) + "\t" + detail::json_double(r.best.expectation) + "\t" +
+           positions + "\t" + std::to_string(r.best.source_bucket) + "\t" + std::to_string(r.best_trial) + "\t" +
+           std::to_string(r.trials_run) + "\t" + std::to_string(r.buckets_enriched) + "\t" + detail::format_ms(r.wall_ms) + "\n";
+    return out;
+}
+
+inline std::string truth_json(const PlantedInstance& inst) {
+    std::string o = "{\n";
+    o += "  \"motif\": " + detail::json_string(inst.motif) + ",\n";
+    o += "  \"positions\": " + detail::json_int_array(inst.positions, "  ") + ",\n";
+    o += "  \"d\": " + std::to_string(inst.d) + ",\n";
+    o += "  \"l\": " + std::to_string(inst.l) + ",\n";
+    o += "  \"seed\": " + std::to_string(inst.seed) + "\n";
+    o += "}\n";
+    return o;
 }
 
 }  // namespace projmotif_b200

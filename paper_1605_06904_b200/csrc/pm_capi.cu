@@ -190,9 +190,14 @@ int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
 // the path; it depends on the sequence set only (not on l, the plan or the bucket).
 int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel, int t) {
     const int64_t total = rel[static_cast<size_t>(t)];
-    // small sets: one tile (every t=20 config); large sets: tiles of ~12.6k slots (3 CTAs per SM)
     const int64_t single = k::kZPad + total + 32 * static_cast<int64_t>(t);
-    int64_t cap = single <= 21000 ? single : 12600;
+    // one tile up to ~13.5k slots (3 CTAs/SM); above that, balanced tiles of at most ~12.6k slots
+    // (two tiles for the n=1000 configs: 4 CTAs/SM, measured +5 % over one 84 KB tile)
+    int64_t cap = single;
+    if (single > 13500) {
+        const int64_t nt = (single + 12599) / 12600;
+        cap = single / nt + 700;
+    }
     if (const char* env = std::getenv("PM_B200_TILE_SLOTS")) {  // test knob: force small tiles
         const long v = std::atol(env);
         if (v >= 256 && v <= 48000) cap = v;
