@@ -50,7 +50,7 @@ struct DevBuf {
 enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
-    S_SCAL, S_MEMBERS, S_MPREV, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
+    S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
 };
 
 }  // namespace
@@ -380,14 +380,25 @@ int sort_segments(pm_ctx* c, KeyT* ka, KeyT* kb, unsigned int* ia, unsigned int*
         const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nseg));
         k::radix_hist_kernel<KeyT><<<grid, k::kSortWarps * 32, 0, c->stream>>>(kin, stride, len, len_dev, tiles, shift, counts);
         PM_TRY(check_launch(c, "radix_hist"));
-        k::radix_scan_kernel<<<nseg, 256, 0, c->stream>>>(counts, tiles);
-        PM_TRY(check_launch(c, "radix_scan"));
+        const unsigned int* digit_base = nullptr;
+        if (tiles <= 64) {
+            k::radix_scan_kernel<<<nseg, 256, 0, c->stream>>>(counts, tiles);
+            PM_TRY(check_launch(c, "radix_scan"));
+        } else {  // large segments: scan the 256 digit rows of a segment in parallel
+            unsigned int* totals = nullptr;
+            PM_TRY(get_buf(c, S_DIGIT_TOT, static_cast<size_t>(nseg) * 256, &totals));
+            k::radix_scan_rows_kernel<<<dim3(256, static_cast<unsigned>(nseg)), 256, 0, c->stream>>>(counts, tiles, totals);
+            PM_TRY(check_launch(c, "radix_scan_rows"));
+            k::radix_digit_base_kernel<<<nseg, 256, 0, c->stream>>>(totals);
+            PM_TRY(check_launch(c, "radix_digit_base"));
+            digit_base = totals;
+        }
         if (first) {
             k::radix_scatter_kernel<KeyT, true><<<grid, k::kSortWarps * 32, 0, c->stream>>>(
-                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts);
+                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts, digit_base);
         } else {
             k::radix_scatter_kernel<KeyT, false><<<grid, k::kSortWarps * 32, 0, c->stream>>>(
-                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts);
+                kin, iin, kout, iout, stride, len, len_dev, tiles, shift, counts, digit_base);
         }
         PM_TRY(check_launch(c, "radix_scatter"));
         first = false;
@@ -453,8 +464,16 @@ int find_enriched(pm_ctx* c, const Sorted<KeyT>& s, int n_trials, int thr, Recor
     PM_TRY(get_buf(c, S_REC_START, n, &r->start));
     PM_TRY(get_buf(c, S_REC_SIZE, n, &r->size));
     PM_TRY(get_buf(c, S_NREC, static_cast<size_t>(n_trials) + 1, &r->n_rec));
-    k::enrich_kernel<KeyT><<<n_trials, 1024, 0, c->stream>>>(s.keys, c->x, thr, r->cap_e, r->key, r->start, r->size, r->n_rec);
-    return check_launch(c, "enrich");
+    const int etiles = static_cast<int>((c->x + k::kEnrichTile - 1) / k::kEnrichTile);
+    unsigned int* tile_cnt = nullptr;
+    PM_TRY(get_buf(c, S_ETILES, static_cast<size_t>(n_trials) * static_cast<size_t>(etiles), &tile_cnt));
+    const dim3 grid(static_cast<unsigned>(etiles), static_cast<unsigned>(n_trials));
+    k::enrich_kernel<KeyT, false><<<grid, 1024, 0, c->stream>>>(s.keys, c->x, thr, r->cap_e, etiles, tile_cnt, r->key, r->start, r->size);
+    PM_TRY(check_launch(c, "enrich_count"));
+    k::enrich_scan_kernel<<<n_trials, 1024, 0, c->stream>>>(tile_cnt, etiles, r->n_rec);
+    PM_TRY(check_launch(c, "enrich_scan"));
+    k::enrich_kernel<KeyT, true><<<grid, 1024, 0, c->stream>>>(s.keys, c->x, thr, r->cap_e, etiles, tile_cnt, r->key, r->start, r->size);
+    return check_launch(c, "enrich_write");
 }
 
 // ---------------------------------------------------------------------------------------------

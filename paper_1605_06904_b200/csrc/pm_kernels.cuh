@@ -234,13 +234,61 @@ __global__ void __launch_bounds__(256) radix_scan_kernel(unsigned int* __restric
     }
 }
 
+// Many-tile variant of the scan (large segments): one CTA per (digit, segment) row scans its tiles in
+// place and records the row total; a second kernel turns the 256 totals of a segment into digit
+// bases, which the scatter kernel adds (digit_base != nullptr).
+__global__ void __launch_bounds__(256) radix_scan_rows_kernel(unsigned int* __restrict__ counts, int tiles,
+                                                              unsigned int* __restrict__ totals /* [seg][256] */) {
+    __shared__ unsigned int part[256];
+    const int d = blockIdx.x, seg = blockIdx.y;
+    unsigned int* row = counts + (static_cast<int64_t>(seg) * 256 + d) * tiles;
+    const int per = (tiles + 255) / 256;
+    const int b = min(tiles, static_cast<int>(threadIdx.x) * per), e = min(tiles, b + per);
+    unsigned int sum = 0;
+    for (int i = b; i < e; ++i) sum += row[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    unsigned int v = sum;
+    for (int o = 1; o < 256; o <<= 1) {
+        const unsigned int add = static_cast<int>(threadIdx.x) >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        v += add;
+        part[threadIdx.x] = v;
+        __syncthreads();
+    }
+    unsigned int run = v - sum;
+    for (int i = b; i < e; ++i) {
+        const unsigned int c = row[i];
+        row[i] = run;
+        run += c;
+    }
+    if (threadIdx.x == 255) totals[seg * 256 + d] = v;
+}
+
+__global__ void __launch_bounds__(256) radix_digit_base_kernel(unsigned int* __restrict__ totals) {
+    __shared__ unsigned int part[256];
+    unsigned int* row = totals + static_cast<int64_t>(blockIdx.x) * 256;
+    const unsigned int mine = row[threadIdx.x];
+    part[threadIdx.x] = mine;
+    __syncthreads();
+    unsigned int v = mine;
+    for (int o = 1; o < 256; o <<= 1) {
+        const unsigned int add = static_cast<int>(threadIdx.x) >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        v += add;
+        part[threadIdx.x] = v;
+        __syncthreads();
+    }
+    row[threadIdx.x] = v - mine;  // exclusive
+}
+
 // kFirst: payload of the input is the element's own index within the segment (no idx_in read).
 template <typename KeyT, bool kFirst>
 __global__ void __launch_bounds__(kSortWarps * 32)
 radix_scatter_kernel(const KeyT* __restrict__ keys_in, const unsigned int* __restrict__ idx_in,
                      KeyT* __restrict__ keys_out, unsigned int* __restrict__ idx_out, int64_t seg_stride,
                      int64_t seg_len, const unsigned int* __restrict__ seg_len_dev, int tiles, int shift,
-                     const unsigned int* __restrict__ offsets) {
+                     const unsigned int* __restrict__ offsets, const unsigned int* __restrict__ digit_base) {
     __shared__ unsigned int warp_cnt[kSortWarps][256];  // per-warp digit counts, then exclusive prefix over warps
     const int seg = blockIdx.y, tile = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -276,6 +324,7 @@ radix_scatter_kernel(const KeyT* __restrict__ keys_in, const unsigned int* __res
     // exclusive prefix over warps per digit, plus the tile's global offset for that digit
     for (int d = threadIdx.x; d < 256; d += blockDim.x) {
         unsigned int run = offsets[(static_cast<int64_t>(seg) * 256 + d) * tiles + tile];
+        if (digit_base) run += digit_base[seg * 256 + d];
 #pragma unroll
         for (int w = 0; w < kSortWarps; ++w) {
             const unsigned int c = warp_cnt[w][d];
@@ -297,54 +346,55 @@ radix_scatter_kernel(const KeyT* __restrict__ keys_in, const unsigned int* __res
 }
 
 // ---------------------------------------------------------------------------------------------
-// enrich: one CTA per trial over its sorted key segment.  An element is the head of a bucket
-// when its predecessor has a different key; the bucket is enriched when the key s-1 places
-// further still matches; its size is an upper-bound search.  Heads are compacted in key order
-// with a block-wide ordered scan (ballot + warp prefix + warp totals).
-// Output per trial (stride cap_e): rec_key, rec_start (segment-relative), rec_size; n_rec[trial].
+// enrich: CTA (tile, trial) over a tile of the trial's sorted key segment.  An element is the head
+// of a bucket when its predecessor has a different key; the bucket is enriched when the key s-1
+// places further still matches; its size is an upper-bound search.  Two passes: kWrite = false counts
+// the enriched heads of the tile; after an exclusive scan of the tile counts, kWrite = true compacts
+// them in key order (block-wide ordered scan: ballot + warp prefix + warp totals) behind the
+// tile's offset.  Output per trial (stride cap_e): rec_key, rec_start (segment-relative), rec_size.
 // ---------------------------------------------------------------------------------------------
-template <typename KeyT>
+constexpr int kEnrichTile = 8192;
+
+template <typename KeyT, bool kWrite>
 __global__ void __launch_bounds__(1024)
-enrich_kernel(const KeyT* __restrict__ keys, int64_t x, int s, int64_t cap_e, uint64_t* __restrict__ rec_key,
-              unsigned int* __restrict__ rec_start, unsigned int* __restrict__ rec_size,
-              unsigned int* __restrict__ n_rec) {
+enrich_kernel(const KeyT* __restrict__ keys, int64_t x, int s, int64_t cap_e, int etiles,
+              unsigned int* __restrict__ tile_cnt /* [trial][etiles]: counts (pass 1) / exclusive offsets (pass 2) */,
+              uint64_t* __restrict__ rec_key, unsigned int* __restrict__ rec_start, unsigned int* __restrict__ rec_size) {
     __shared__ unsigned int warp_tot[32];
     __shared__ unsigned int chunk_base;
-    const int trial = blockIdx.x;
+    const int trial = blockIdx.y, tile = blockIdx.x;
     const KeyT* kk = keys + static_cast<int64_t>(trial) * x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    if (threadIdx.x == 0) chunk_base = 0;
+    if (threadIdx.x == 0) chunk_base = kWrite ? tile_cnt[static_cast<int64_t>(trial) * etiles + tile] : 0u;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < x; c0 += blockDim.x) {
+    const int64_t t_begin = static_cast<int64_t>(tile) * kEnrichTile;
+    const int64_t t_end = min(x, t_begin + kEnrichTile);
+    for (int64_t c0 = t_begin; c0 < t_end; c0 += blockDim.x) {
         const int64_t i = c0 + threadIdx.x;
         bool hit = false;
         KeyT key = 0;
-        unsigned int size = 0;
-        if (i < x) {
+        if (i < t_end) {
             key = kk[i];
             const bool head = (i == 0) || (kk[i - 1] != key);
-            if (head && i + s - 1 < x && kk[i + s - 1] == key) {
-                hit = true;
+            hit = head && i + s - 1 < x && kk[i + s - 1] == key;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) warp_tot[warp] = __popc(ball);
+        __syncthreads();
+        if (kWrite && hit) {
+            unsigned int before = chunk_base;
+            for (int w = 0; w < warp; ++w) before += warp_tot[w];
+            const int64_t e = before + __popc(ball & ((1u << lane) - 1u));
+            if (e < cap_e) {
                 int64_t lo = i + s - 1, hi = x;  // kk[lo] == key; first index > lo with a different key
                 while (hi - lo > 1) {
                     const int64_t mid = (lo + hi) >> 1;
                     if (kk[mid] == key) lo = mid; else hi = mid;
                 }
-                size = static_cast<unsigned int>(hi - i);
-            }
-        }
-        const unsigned ball = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) warp_tot[warp] = __popc(ball);
-        __syncthreads();
-        unsigned int before = chunk_base;
-        for (int w = 0; w < warp; ++w) before += warp_tot[w];
-        if (hit) {
-            const int64_t e = before + __popc(ball & ((1u << lane) - 1u));
-            if (e < cap_e) {
                 const int64_t o = static_cast<int64_t>(trial) * cap_e + e;
                 rec_key[o] = static_cast<uint64_t>(key);
                 rec_start[o] = static_cast<unsigned int>(i);
-                rec_size[o] = size;
+                rec_size[o] = static_cast<unsigned int>(hi - i);
             }
         }
         __syncthreads();
@@ -355,7 +405,36 @@ enrich_kernel(const KeyT* __restrict__ keys, int64_t x, int s, int64_t cap_e, ui
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) n_rec[trial] = chunk_base;
+    if (!kWrite && threadIdx.x == 0) tile_cnt[static_cast<int64_t>(trial) * etiles + tile] = chunk_base;
+}
+
+// per trial: tile counts -> exclusive offsets (in place), n_rec[trial] = total.  grid = trials.
+__global__ void __launch_bounds__(1024) enrich_scan_kernel(unsigned int* __restrict__ tile_cnt, int etiles,
+                                                           unsigned int* __restrict__ n_rec) {
+    __shared__ unsigned int part[1024];
+    unsigned int* row = tile_cnt + static_cast<int64_t>(blockIdx.x) * etiles;
+    const int per = (etiles + blockDim.x - 1) / blockDim.x;
+    const int b = min(etiles, static_cast<int>(threadIdx.x) * per), e = min(etiles, b + per);
+    unsigned int sum = 0;
+    for (int i = b; i < e; ++i) sum += row[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    // Hillis-Steele inclusive scan of the 1024 partials
+    unsigned int v = sum;
+    for (int o = 1; o < 1024; o <<= 1) {
+        const unsigned int add = static_cast<int>(threadIdx.x) >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        v += add;
+        part[threadIdx.x] = v;
+        __syncthreads();
+    }
+    unsigned int run = v - sum;
+    for (int i = b; i < e; ++i) {
+        const unsigned int c = row[i];
+        row[i] = run;
+        run += c;
+    }
+    if (threadIdx.x == blockDim.x - 1) n_rec[blockIdx.x] = v;
 }
 
 // exclusive scan of n_rec[0..n) -> work_off[0..n], single CTA
