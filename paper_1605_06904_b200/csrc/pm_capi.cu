@@ -14,6 +14,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -80,6 +81,8 @@ struct pm_ctx {
     int zlen = 0;          // largest tile's z slots; 0 => some sequence does not fit the shared-memory EM kernel
     int total_groups = 0;
     double group_fill = 0.0;  // live entries / slots of the class-gather rows
+    int em_cfg_l = -1, em_cfg_threads = 0, em_cfg_per_sm = 0;  // cached launch setup of the smem EM kernel
+    size_t em_cfg_smem = 0;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -624,10 +627,18 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         const int threads = nwarps * 32;
         const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen, c->t);
         EmSmemKernel kern = em_smem_kernel_for(l);
-        PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
-        PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        if (c->em_cfg_l == l && c->em_cfg_smem == smem && c->em_cfg_threads == threads) {
+            per_sm = c->em_cfg_per_sm;  // attributes and occupancy were set up by an earlier launch
+        } else {
+            PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+            PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+            c->em_cfg_l = l;
+            c->em_cfg_smem = smem;
+            c->em_cfg_threads = threads;
+            c->em_cfg_per_sm = per_sm;
+        }
         if (per_sm >= 1) {
             const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
             const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
@@ -1245,6 +1256,10 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     PM_TRY(get_buf(c, S_OUT_ITERS, nb, &o.iters));
     PM_TRY(get_buf(c, S_OUT_EXP, nb, &o.expct));
     PM_TRY(get_buf(c, S_OUT_CONS, nb, &o.cons));
+    // positions of every bucket are written by the main launch when that is affordable; otherwise the
+    // winning bucket is re-run alone afterwards (deterministic kernel => identical candidate)
+    const bool all_positions = nb * static_cast<size_t>(c->t) * sizeof(int32_t) <= (256u << 20);
+    if (all_positions) PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
     PM_TRY(get_buf(c, S_SCAL, 4, &d_scal));
     PM_TRY(get_buf(c, S_BEST, static_cast<size_t>(n_trials), &best_work));
     PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
@@ -1313,7 +1328,12 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
             break;
         }
     }
-    if (new_best_work >= 0) {
+    if (new_best_work >= 0 && all_positions) {
+        st->positions.resize(static_cast<size_t>(c->t));
+        PM_TRY(d2h(c, st->positions.data(), o.pos + static_cast<size_t>(new_best_work) * static_cast<size_t>(c->t),
+                   sizeof(int32_t) * static_cast<size_t>(c->t)));
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+    } else if (new_best_work >= 0) {
         // Positions of the new incumbent: re-run its bucket alone with the position output on.
         // Same kernel, same launch shape per CTA, deterministic => identical candidate.
         EmOut o1;
@@ -1379,23 +1399,45 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
 
     RunState st;
     bool stop = false;
-    std::vector<int32_t> kept(static_cast<size_t>(params.k));
     for (int64_t first = tb; first <= te && !stop; first += batch) {
         const int64_t last = std::min(te, first + batch - 1);
-        std::vector<k::PlanProg> progs;
-        progs.reserve(static_cast<size_t>(last - first + 1));
-        for (int64_t trial = first; trial <= last; ++trial) {
-            const int32_t* plan;
-            if (cfg->forced_kept != nullptr) {
-                plan = cfg->forced_kept;
-            } else if (cfg->plans != nullptr) {
-                plan = cfg->plans + (trial - 1) * params.k;
-                PM_TRY(validate_plan(cfg->l, plan, params.k));
-            } else {
-                PM_TRY(pm_trial_plan(cfg->l, params.k, cfg->seed, trial, kept.data()));
-                plan = kept.data();
+        // Plans come from the reference's PRNG stream (one mt19937_64 per trial, driver.hpp:164):
+        // independent per trial, so the host samples them on a few threads.
+        const int64_t n_plans = last - first + 1;
+        std::vector<k::PlanProg> progs(static_cast<size_t>(n_plans));
+        std::vector<int> plan_rc(static_cast<size_t>(n_plans), PM_OK);
+        auto make_range = [&](int64_t a, int64_t b) {
+            std::vector<int32_t> mine(static_cast<size_t>(params.k));
+            for (int64_t i = a; i < b; ++i) {
+                const int64_t trial = first + i;
+                const int32_t* plan;
+                if (cfg->forced_kept != nullptr) {
+                    plan = cfg->forced_kept;
+                } else if (cfg->plans != nullptr) {
+                    plan = cfg->plans + (trial - 1) * params.k;
+                    plan_rc[static_cast<size_t>(i)] = validate_plan(cfg->l, plan, params.k);
+                } else {
+                    plan_rc[static_cast<size_t>(i)] = pm_trial_plan(cfg->l, params.k, cfg->seed, trial, mine.data());
+                    plan = mine.data();
+                }
+                if (plan_rc[static_cast<size_t>(i)] == PM_OK) progs[static_cast<size_t>(i)] = make_prog(plan, params.k);
             }
-            progs.push_back(make_prog(plan, params.k));
+        };
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        const int n_threads = static_cast<int>(std::min<int64_t>(std::min(8, hw), (n_plans + 31) / 32));
+        if (n_threads <= 1 || cfg->forced_kept != nullptr) {
+            make_range(0, n_plans);
+        } else {
+            std::vector<std::thread> pool;
+            const int64_t chunk = (n_plans + n_threads - 1) / n_threads;
+            for (int w = 0; w < n_threads; ++w) {
+                const int64_t a = w * chunk, b = std::min(n_plans, a + chunk);
+                if (a < b) pool.emplace_back(make_range, a, b);
+            }
+            for (std::thread& th : pool) th.join();
+        }
+        for (int rc_plan : plan_rc) {
+            if (rc_plan != PM_OK) return set_error(rc_plan, "invalid projection plan for a trial");
         }
         const int rc = key_bytes == 4
                            ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
