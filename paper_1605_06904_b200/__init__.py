@@ -17,7 +17,7 @@ import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libpm_b200.so")
+LIB_PATH = os.environ.get("PM_B200_LIB") or os.path.join(PKG_DIR, "libpm_b200.so")  # override: instrumented builds
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = ["pm_capi.cu", "pm_host.cpp"]
 HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]

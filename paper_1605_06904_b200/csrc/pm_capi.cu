@@ -90,6 +90,9 @@ struct pm_ctx {
     double* d_seq_logw = nullptr;
     int64_t x = 0, uniform_w = 0;
     DevBuf buf[S_COUNT_];
+    // capacities (bytes) of the per-set device arrays above: reused across pm_ctx_set_sequences calls
+    size_t cap_words = 0, cap_word_off = 0, cap_seq_len = 0, cap_seq_sym = 0, cap_tot_sym = 0, cap_win_off = 0,
+           cap_seq_logw = 0, cap_cls_entries = 0, cap_cls_group_off = 0, cap_seq_zoff = 0, cap_tiles = 0;
     // measurement: bytes moved by this context and stage timing events (read after a sync)
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     struct StageMark {
@@ -118,6 +121,23 @@ int get_buf(pm_ctx* c, Slot s, size_t n, T** out) {
         b.cap = want;
     }
     *out = static_cast<T*>(b.p);
+    return PM_OK;
+}
+
+// grow-only allocation of a per-set device array
+template <typename T>
+int ensure(pm_ctx* c, T** ptr, size_t* cap, size_t bytes) {
+    if (*ptr != nullptr && *cap >= bytes) return PM_OK;
+    if (*ptr != nullptr) {
+        PM_CUDA(cudaStreamSynchronize(c->stream));
+        PM_CUDA(cudaFree(*ptr));
+        *ptr = nullptr;
+        *cap = 0;
+    }
+    void* p = nullptr;
+    PM_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    *ptr = static_cast<T*>(p);
+    *cap = std::max<size_t>(bytes, 16);
     return PM_OK;
 }
 
@@ -282,10 +302,10 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         group_off.push_back(row);
         tiles.push_back(tile);
     }
-    PM_CUDA(cudaMalloc(&c->d_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
-    PM_CUDA(cudaMalloc(&c->d_cls_group_off, sizeof(int) * group_off.size()));
-    PM_CUDA(cudaMalloc(&c->d_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
-    PM_CUDA(cudaMalloc(&c->d_tiles, sizeof(k::TileDesc) * tiles.size()));
+    PM_TRY(ensure(c, &c->d_cls_entries, &c->cap_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
+    PM_TRY(ensure(c, &c->d_cls_group_off, &c->cap_cls_group_off, sizeof(int) * group_off.size()));
+    PM_TRY(ensure(c, &c->d_seq_zoff, &c->cap_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
+    PM_TRY(ensure(c, &c->d_tiles, &c->cap_tiles, sizeof(k::TileDesc) * tiles.size()));
     PM_TRY(h2d(c, c->d_cls_entries, entries.data(), sizeof(uint16_t) * entries.size()));
     PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * group_off.size()));
     PM_TRY(h2d(c, c->d_seq_zoff, zoff.data(), sizeof(int) * zoff.size()));
@@ -619,6 +639,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.out_ll = o.ll;
     p.iter_total = d_scal;
     p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
+    p.phase_clk = d_scal + 8;
 
     if (c->zlen > 0) {
         // shared-memory kernel: z of every window resident per CTA, conflict-free class-gather M-step
@@ -775,33 +796,12 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     }
     PM_CUDA(cudaSetDevice(c->device));
     PM_CUDA(cudaStreamSynchronize(c->stream));
-    cudaFree(c->d_words);
-    cudaFree(c->d_word_off);
-    cudaFree(c->d_seq_len);
-    cudaFree(c->d_seq_sym);
-    cudaFree(c->d_tot_sym);
-    cudaFree(c->d_win_off);
-    cudaFree(c->d_seq_logw);
-    c->d_seq_logw = nullptr;
-    cudaFree(c->d_cls_entries);
-    cudaFree(c->d_cls_group_off);
-    cudaFree(c->d_seq_zoff);
-    cudaFree(c->d_tiles);
-    c->d_tiles = nullptr;
-    c->n_tiles = 0;
-    c->d_cls_entries = nullptr;
-    c->d_cls_group_off = nullptr;
-    c->d_seq_zoff = nullptr;
-    c->zlen = 0;
-    c->total_groups = 0;
-    c->d_words = nullptr;
-    c->d_word_off = nullptr;
-    c->d_seq_len = nullptr;
-    c->d_seq_sym = nullptr;
-    c->d_tot_sym = nullptr;
-    c->d_win_off = nullptr;
     c->t = 0;
     c->win_l = 0;
+    c->zlen = 0;
+    c->n_tiles = 0;
+    c->total_groups = 0;
+    c->em_cfg_l = -1;
 
     const int64_t base0 = offs[0];
     std::vector<int64_t> rel(static_cast<size_t>(t) + 1), word_off(static_cast<size_t>(t) + 1, 0);
@@ -822,13 +822,13 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     int64_t* d_offs = nullptr;
     PM_TRY(get_buf(c, S_ASCII, static_cast<size_t>(total_bases), &d_ascii));
     PM_TRY(get_buf(c, S_OFFS, static_cast<size_t>(t) + 1, &d_offs));
-    PM_CUDA(cudaMalloc(&c->d_words, sizeof(uint64_t) * static_cast<size_t>(total_words)));
-    PM_CUDA(cudaMalloc(&c->d_word_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
-    PM_CUDA(cudaMalloc(&c->d_seq_len, sizeof(int32_t) * static_cast<size_t>(t)));
-    PM_CUDA(cudaMalloc(&c->d_seq_sym, sizeof(unsigned int) * 4 * static_cast<size_t>(t)));
-    PM_CUDA(cudaMalloc(&c->d_tot_sym, sizeof(unsigned long long) * 8));
-    PM_CUDA(cudaMalloc(&c->d_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
-    PM_CUDA(cudaMalloc(&c->d_seq_logw, sizeof(double) * static_cast<size_t>(t)));
+    PM_TRY(ensure(c, &c->d_words, &c->cap_words, sizeof(uint64_t) * static_cast<size_t>(total_words)));
+    PM_TRY(ensure(c, &c->d_word_off, &c->cap_word_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
+    PM_TRY(ensure(c, &c->d_seq_len, &c->cap_seq_len, sizeof(int32_t) * static_cast<size_t>(t)));
+    PM_TRY(ensure(c, &c->d_seq_sym, &c->cap_seq_sym, sizeof(unsigned int) * 4 * static_cast<size_t>(t)));
+    PM_TRY(ensure(c, &c->d_tot_sym, &c->cap_tot_sym, sizeof(unsigned long long) * 8));
+    PM_TRY(ensure(c, &c->d_win_off, &c->cap_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
+    PM_TRY(ensure(c, &c->d_seq_logw, &c->cap_seq_logw, sizeof(double) * static_cast<size_t>(t)));
     PM_TRY(h2d(c, d_ascii, bases + base0, static_cast<size_t>(total_bases)));
     PM_TRY(h2d(c, d_offs, rel.data(), sizeof(int64_t) * rel.size()));
     PM_TRY(h2d(c, c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size()));
@@ -844,6 +844,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     k::encode_kernel<<<grid, warps_per_block * 32, 0, c->stream>>>(d_ascii, d_offs, c->d_word_off, t, c->d_words,
                                                                  c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
     PM_TRY(check_launch(c, "encode"));
+    PM_TRY(build_class_groups(c, bases + base0, rel, t));  // host index build overlaps the encode kernel
     unsigned long long host_tot[5];
     PM_TRY(d2h(c, host_tot, c->d_tot_sym, sizeof(host_tot)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
@@ -855,7 +856,6 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
                                                     std::to_string(seq + 1) + "' is not in alphabet \"ACTG\"");
     }
     for (int r = 0; r < 4; ++r) c->tot_sym[r] = host_tot[r];
-    PM_TRY(build_class_groups(c, bases + base0, rel, t));
     c->t = t;
     c->offs = rel;
     c->word_off = word_off;
@@ -1061,7 +1061,7 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     EmOut o;
     PM_TRY(get_buf(c, S_MEMBERS, static_cast<size_t>(n_mem), &d_mem));
     PM_TRY(get_buf(c, S_WORK, nb, &d_work));
-    PM_TRY(get_buf(c, S_SCAL, 4, &d_scal));
+    PM_TRY(get_buf(c, S_SCAL, 16, &d_scal));
     PM_TRY(get_buf(c, S_OUT_SCORE, nb, &o.score));
     PM_TRY(get_buf(c, S_OUT_ITERS, nb, &o.iters));
     PM_TRY(get_buf(c, S_OUT_EXP, nb, &o.expct));
@@ -1076,7 +1076,7 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     }
     PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem)));
     PM_TRY(h2d(c, d_work, work.data(), sizeof(k::WorkDesc) * nb));
-    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
+    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
     PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
                      static_cast<unsigned int>(n_buckets), d_mem, o, d_scal));
     std::vector<int32_t> hs(nb), hi(nb);
@@ -1260,10 +1260,10 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     // winning bucket is re-run alone afterwards (deterministic kernel => identical candidate)
     const bool all_positions = nb * static_cast<size_t>(c->t) * sizeof(int32_t) <= (256u << 20);
     if (all_positions) PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
-    PM_TRY(get_buf(c, S_SCAL, 4, &d_scal));
+    PM_TRY(get_buf(c, S_SCAL, 16, &d_scal));
     PM_TRY(get_buf(c, S_BEST, static_cast<size_t>(n_trials), &best_work));
     PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
-    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 4, c->stream));
+    PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
     {
         StageTimer tm(c, prof, 3);
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work, work_off + n_trials, 0,
@@ -1271,7 +1271,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     }
     std::vector<TrialSummary> tb(static_cast<size_t>(n_trials));
     std::vector<unsigned int> n_rec(static_cast<size_t>(n_trials));
-    unsigned long long scal[2];
+    unsigned long long scal[16] = {0};
     {
         StageTimer tr(c, prof, 4);
         const int warps_per_block = 8;
@@ -1291,6 +1291,15 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
     collect_stage_times(c, out->stage_ms);
+#ifdef PM_EM_TIMING
+    {
+        unsigned long long tot = 0;
+        for (int i = 8; i < 16; ++i) tot += scal[i];
+        std::fprintf(stderr, "[em phases] init %.1f%% tables %.1f%% estep %.1f%% mstep %.1f%% update %.1f%% final %.1f%% out %.1f%% (total %.3g clk)\n",
+                     100.0 * scal[8] / tot, 100.0 * scal[9] / tot, 100.0 * scal[10] / tot, 100.0 * scal[11] / tot,
+                     100.0 * scal[12] / tot, 100.0 * scal[13] / tot, 100.0 * scal[14] / tot, static_cast<double>(tot));
+    }
+#endif
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
@@ -1343,8 +1352,8 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(get_buf(c, S_TMP_C, 4, &o1.cons));
         PM_TRY(get_buf(c, S_OUT_POS, static_cast<size_t>(c->t), &o1.pos));
         unsigned long long* d_scal2;
-        PM_TRY(get_buf(c, S_TMP_D, 4, &d_scal2));
-        PM_CUDA(cudaMemsetAsync(d_scal2, 0, sizeof(unsigned long long) * 4, c->stream));
+        PM_TRY(get_buf(c, S_TMP_D, 16, &d_scal2));
+        PM_CUDA(cudaMemsetAsync(d_scal2, 0, sizeof(unsigned long long) * 16, c->stream));
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work + new_best_work, nullptr, 1, 1, srt.idx,
                          o1, d_scal2));
         st->positions.resize(static_cast<size_t>(c->t));

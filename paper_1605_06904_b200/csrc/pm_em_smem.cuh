@@ -103,20 +103,43 @@ __device__ __forceinline__ float fast_ex2(float x) {
 }
 constexpr float kLog2e = 1.4426950408889634f;
 
-// E-step pass A over one sequence: window weights w_j (lane = window).  kExp = false stores w_j;
-// kExp = true stores e_j = exp(w_j - ref) = 2^(w_j log2e - ref2) and accumulates their lane sum.
-// kArg tracks the lane's first maximum and its offset (final sweep), otherwise only the maximum.
-template <int G, bool kExp, bool kArg>
-__device__ __forceinline__ void estep_window(const float* __restrict__ T, uint32_t vh, uint32_t vl, int j,
-                                             float* __restrict__ zs, float ref2, float& best_w, int& best_j,
-                                             float& s_all) {
-    const float w = window_weight_tree<G>(T, vh, vl);
-    if (kExp) {
-        const float e = fast_ex2(fmaf(w, kLog2e, -ref2));
-        zs[j] = e;
-        s_all += e;
-    } else {
-        zs[j] = w;
+// Appends the lanes flagged in `ball` (in lane order) to the warp's near-window list.
+__device__ __forceinline__ void near_push(unsigned ball, bool keep, int lane, int j, int* __restrict__ my_near,
+                                          int& nnear, bool& overflow) {
+    if (ball && !overflow) {
+        const int cnt = __popc(ball);
+        if (nnear + cnt > kNearCap) {
+            overflow = true;
+        } else {
+            if (keep) my_near[nnear + __popc(ball & ((1u << lane) - 1u))] = j;
+            nnear += cnt;
+        }
+    }
+}
+
+// E-step pass A over one sequence: window weights w_j (lane = window).
+//   kExp = false: stores w_j.
+//   kExp = true : stores e_j = exp(w_j - ref) = 2^(w_j log2e - ref2), accumulates their lane sum (s_all) and
+//                 the sum of those below near_thr (s_far), and lists the windows with e_j >= near_thr.
+//   kArg tracks the lane's first maximum and its offset (final sweep), otherwise only the maximum.
+template <int G, bool kExp, bool kArg, bool kTail>
+__device__ __forceinline__ void estep_chunk(const float* __restrict__ T, uint32_t vh, uint32_t vl, int j, bool live,
+                                            int lane, float* __restrict__ zs, float ref2, float near_thr,
+                                            float& best_w, int& best_j, float& s_all, float& s_far,
+                                            int* __restrict__ my_near, int& nnear, bool& overflow) {
+    float w = -INFINITY;
+    bool keep = false;
+    if (!kTail || live) {
+        w = window_weight_tree<G>(T, vh, vl);
+        if (kExp) {
+            const float e = fast_ex2(fmaf(w, kLog2e, -ref2));
+            zs[j] = e;
+            s_all += e;
+            keep = e >= near_thr;
+            s_far += keep ? 0.f : e;
+        } else {
+            zs[j] = w;
+        }
     }
     if (kArg) {
         if (w > best_w) {  // strict: the earliest offset is kept
@@ -126,12 +149,14 @@ __device__ __forceinline__ void estep_window(const float* __restrict__ T, uint32
     } else {
         best_w = fmaxf(best_w, w);
     }
+    if (kExp) near_push(__ballot_sync(0xffffffffu, keep), keep, lane, j, my_near, nnear, overflow);
 }
 
 template <int G, bool kExp, bool kArg>
 __device__ __forceinline__ void estep_pass_a(const float* __restrict__ T, const uint64_t* __restrict__ wp, int W,
-                                             int lane, float* __restrict__ zs, float ref, float& best_w,
-                                             int& best_j, float& s_all) {
+                                             int lane, float* __restrict__ zs, float ref, float near_thr,
+                                             float& best_w, int& best_j, float& s_all, float& s_far,
+                                             int* __restrict__ my_near, int& nnear, bool& overflow) {
     const float ref2 = ref * kLog2e;
     const int full = W >> 5;  // chunks in which every lane has a window
     uint64_t hi = wp[0];
@@ -141,15 +166,55 @@ __device__ __forceinline__ void estep_pass_a(const float* __restrict__ T, const 
         uint32_t vh, vl;
         window_halves(hi, lo, lane, vh, vl);
         hi = lo;
-        estep_window<G, kExp, kArg>(T, vh, vl, (c << 5) + lane, zs, ref2, best_w, best_j, s_all);
+        estep_chunk<G, kExp, kArg, false>(T, vh, vl, (c << 5) + lane, true, lane, zs, ref2, near_thr, best_w, best_j,
+                                          s_all, s_far, my_near, nnear, overflow);
     }
-    const int j = (c << 5) + lane;
-    if (j < W) {  // ragged tail
+    if ((W & 31) != 0) {  // ragged tail (warp-uniform branch)
+        const int j = (c << 5) + lane;
         uint32_t vh, vl;
         window_halves(hi, wp[c + 1], lane, vh, vl);
-        estep_window<G, kExp, kArg>(T, vh, vl, j, zs, ref2, best_w, best_j, s_all);
+        estep_chunk<G, kExp, kArg, true>(T, vh, vl, j, j < W, lane, zs, ref2, near_thr, best_w, best_j, s_all, s_far,
+                                         my_near, nnear, overflow);
     }
 }
+
+// Sweep over the stored values of one sequence: kFromW turns stored w_j into e_j = exp(w_j - M) first.
+// Sums all e_j (s_all) and those below thr (s_far) and lists the windows with e_j >= thr.
+template <bool kFromW>
+__device__ __forceinline__ void estep_pass_detect(float* __restrict__ zs, int W, int lane, float M, float thr,
+                                                  float& s_all, float& s_far, int* __restrict__ my_near, int& nnear,
+                                                  bool& overflow) {
+    const int chunks = (W + 31) >> 5;
+    for (int c = 0; c < chunks; ++c) {
+        const int j = (c << 5) + lane;
+        float e = 0.f;
+        bool keep = false;
+        if (j < W) {
+            e = zs[j];
+            if (kFromW) {
+                e = fast_ex2((e - M) * kLog2e);
+                zs[j] = e;
+            }
+            keep = e >= thr;
+        }
+        s_all += e;
+        s_far += keep ? 0.f : e;
+        near_push(__ballot_sync(0xffffffffu, keep), keep, lane, j, my_near, nnear, overflow);
+    }
+}
+
+#ifdef PM_EM_TIMING
+#define PM_PHASE(idx)                                                                    \
+    do {                                                                                 \
+        if (threadIdx.x == 0) {                                                          \
+            const long long now_ = clock64();                                            \
+            atomicAdd(p.phase_clk + (idx), static_cast<unsigned long long>(now_ - t_phase)); \
+            t_phase = now_;                                                              \
+        }                                                                                \
+    } while (0)
+#else
+#define PM_PHASE(idx) do {} while (0)
+#endif
 
 constexpr int kEmSmemMaxWarps = 10;
 constexpr int kMaxFusedSeqs = 1024;  // sequences whose previous per-sequence maximum is kept in smem
@@ -187,6 +252,9 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     for (unsigned int wi = blockIdx.x; wi < n_work; wi += gridDim.x) {
         const WorkDesc wd = p.work[wi];
         __syncthreads();
+#ifdef PM_EM_TIMING
+        long long t_phase = clock64();
+#endif
 
         // ---- init_model (refine.hpp:90-127), pseudocount 0
         for (int i = threadIdx.x; i < 128; i += blockDim.x) prof[i] = 0;
@@ -212,6 +280,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
 
         int iterations = 0;
         bool final_pass = false;
+        PM_PHASE(0);  // init_model
         for (;;) {
             // ---- log tables of the current theta (refine.hpp:155-161), FP64 then rounded once to FP32
             for (int e = threadIdx.x; e < 4 * l; e += blockDim.x) {
@@ -240,6 +309,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             }
             __syncthreads();
 
+            PM_PHASE(1);  // log tables
             double ll_warp = 0.0;
             for (int e = lane; e < 16 * G; e += 32) cpart[warp * 16 * G + e] = 0.f;  // this warp's class sums
             for (int tile_i = 0; tile_i < x.n_tiles; ++tile_i) {
@@ -260,17 +330,21 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 }
 
                 // pass A.  From the second iteration on the exp is fused in, taken relative to the
-                // previous iteration's maximum of this sequence (softmax is shift-invariant).
+                // previous iteration's maximum of this sequence (softmax is shift-invariant), and the
+                // windows within exp(log_eps - kNearMargin) of that maximum are listed on the way.
+                constexpr float kNearMargin = 4.f;
                 const bool fused = !final_pass && iterations > 0;
                 float ref = fused ? mprev[i] : 0.f;
-                float best_w = -INFINITY, s_all = 0.f;
-                int best_j = 0;
+                float best_w = -INFINITY, s_all = 0.f, s_far = 0.f;
+                int best_j = 0, nnear = 0;
+                bool overflow = false;
                 if (fused) {
-                    estep_pass_a<G, true, false>(T, wp, W, lane, zs, ref, best_w, best_j, s_all);
+                    estep_pass_a<G, true, false>(T, wp, W, lane, zs, ref, fast_ex2((p.log_z_eps - kNearMargin) * kLog2e),
+                                                 best_w, best_j, s_all, s_far, my_near, nnear, overflow);
                 } else if (final_pass) {
-                    estep_pass_a<G, false, true>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
+                    estep_pass_a<G, false, true>(T, wp, W, lane, zs, 0.f, 0.f, best_w, best_j, s_all, s_far, my_near, nnear, overflow);
                 } else {
-                    estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
+                    estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, 0.f, best_w, best_j, s_all, s_far, my_near, nnear, overflow);
                 }
                 const float M = warp_max_f(best_w);
                 if (!(M > -INFINITY) || !(M < INFINITY)) iscal[2] = 1;
@@ -280,8 +354,6 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     // ---- positions: per-sequence argmax, ties to the smallest offset (refine.hpp:311-316).
                     // Windows within delta of the FP32 maximum are compared by their FP64 weights.
                     const float delta = 1e-3f + 1e-5f * fabsf(M);
-                    int nnear = 0;
-                    bool overflow = false;
                     for (int c = 0; c < chunks; ++c) {
                         const int j = (c << 5) + lane;
                         const bool keep = j < W && zs[j] >= M - delta;
@@ -347,55 +419,53 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     have_e = shift > -60.f && shift < 60.f && total > 0.f && total < INFINITY;
                     if (!have_e) {  // the maximum moved too far for FP32 range: redo as two passes
                         best_w = -INFINITY;
-                        estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, best_w, best_j, s_all);
+                        estep_pass_a<G, false, false>(T, wp, W, lane, zs, 0.f, 0.f, best_w, best_j, s_all, s_far, my_near, nnear, overflow);
                         __syncwarp();
                     }
                 }
+                // e_j >= near_e  <=>  w_j >= M + log(eps): the windows re-evaluated in FP64
+                float near_e;
                 if (!have_e) {
-                    // pass B (first iteration / fallback): e_j = exp(w_j - M) and their sum
+                    // first iteration / fallback: e_j = exp(w_j - M), exact near list
                     ref = M;
-                    s_all = 0.f;
-                    for (int c = 0; c < chunks; ++c) {
-                        const int j = (c << 5) + lane;
-                        if (j < W) {
-                            const float e = fast_ex2((zs[j] - M) * kLog2e);
-                            zs[j] = e;
-                            s_all += e;
-                        }
-                    }
+                    near_e = fast_ex2(p.log_z_eps * kLog2e);
+                    s_all = 0.f, s_far = 0.f, nnear = 0, overflow = false;
+                    estep_pass_detect<true>(zs, W, lane, M, near_e, s_all, s_far, my_near, nnear, overflow);
                     total = warp_sum_f(s_all);
+                } else {
+                    near_e = fast_ex2((M - ref + p.log_z_eps) * kLog2e);
+                    if (!overflow && M < ref - kNearMargin) {
+                        // the maximum dropped by more than the margin: the list may be incomplete, rebuild it
+                        float ignore = 0.f;
+                        s_far = 0.f, nnear = 0;
+                        estep_pass_detect<false>(zs, W, lane, M, near_e, ignore, s_far, my_near, nnear, overflow);
+                    }
                 }
                 if (!(total > 0.f)) iscal[2] = 1;
                 const float inv_total = 1.f / total;
                 if (lane == 0) mprev[i] = M;
                 __syncwarp();
-                // pass C: z_j = e_j / sum; windows with w_j >= M + log(eps), i.e. e_j >= exp(M - ref) * eps,
-                // are listed for the FP64 refinement
-                const float near_e = __expf(M - ref + p.log_z_eps);
-                float s_far = 0.f;
-                int nnear = 0;
-                bool overflow = false;
-                for (int c = 0; c < chunks; ++c) {
-                    const int j = (c << 5) + lane;
-                    float e = 0.f;
-                    bool keep = false;
-                    if (j < W) {
-                        e = zs[j];
-                        zs[j] = e * inv_total;
-                        keep = e >= near_e;
+                // listed windows below the exact threshold belong to the far tail after all
+                bool near_a = false, near_b = false;
+                if (!overflow) {
+                    if (lane < nnear) {
+                        const float e = zs[my_near[lane]];
+                        near_a = e >= near_e;
+                        s_far += near_a ? 0.f : e;
                     }
-                    s_far += keep ? 0.f : e;
-                    const unsigned ball = __ballot_sync(0xffffffffu, keep);
-                    if (ball && !overflow) {
-                        if (nnear + __popc(ball) > kNearCap) {
-                            overflow = true;
-                        } else {
-                            if (keep) my_near[nnear + __popc(ball & ((1u << lane) - 1u))] = j;
-                            nnear += __popc(ball);
-                        }
+                    if (lane + 32 < nnear) {
+                        const float e = zs[my_near[lane + 32]];
+                        near_b = e >= near_e;
+                        s_far += near_b ? 0.f : e;
                     }
                 }
-                s_far *= __expf(ref - M);  // far-tail sum relative to M
+                s_far *= fast_ex2((ref - M) * kLog2e);  // far-tail sum relative to M
+                __syncwarp();
+                // pass C: z_j = e_j / sum
+                for (int c = 0; c < chunks; ++c) {
+                    const int j = (c << 5) + lane;
+                    if (j < W) zs[j] *= inv_total;
+                }
                 __syncwarp();
 
                 const unsigned int* sc = p.seq_sym + i * 4;
@@ -409,16 +479,16 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                     const double far = static_cast<double>(warp_sum_f(s_far));
                     double m64 = -INFINITY;
                     double wa = -INFINITY, wb = -INFINITY;
-                    if (lane < nnear) wa = window_weight_d(D64, load_window(wp, my_near[lane]), l);
-                    if (nnear > 32 && lane + 32 < nnear) wb = window_weight_d(D64, load_window(wp, my_near[lane + 32]), l);
+                    if (near_a) wa = window_weight_d(D64, load_window(wp, my_near[lane]), l);
+                    if (near_b) wb = window_weight_d(D64, load_window(wp, my_near[lane + 32]), l);
                     m64 = warp_max_d(fmax(wa, wb));
-                    wa = lane < nnear ? exp(wa - m64) : 0.0;
-                    wb = (nnear > 32 && lane + 32 < nnear) ? exp(wb - m64) : 0.0;
+                    wa = near_a ? exp(wa - m64) : 0.0;
+                    wb = near_b ? exp(wb - m64) : 0.0;
                     // far * exp(M - m64): |M - m64| ~ 1e-5 and far < W*eps, so first order is exact to ~1e-17
                     const double s64 = warp_sum_d(wa + wb) + far * (1.0 + (static_cast<double>(M) - m64));
                     lse = m64 + log(s64);
-                    if (lane < nnear) zs[my_near[lane]] = static_cast<float>(wa / s64);
-                    if (nnear > 32 && lane + 32 < nnear) zs[my_near[lane + 32]] = static_cast<float>(wb / s64);
+                    if (near_a) zs[my_near[lane]] = static_cast<float>(wa / s64);
+                    if (near_b) zs[my_near[lane + 32]] = static_cast<float>(wb / s64);
                 } else {
                     lse = static_cast<double>(ref) + log(static_cast<double>(total));  // total is relative to ref
                 }
@@ -431,6 +501,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 continue;
             }
             __syncthreads();
+            PM_PHASE(2);  // E-step (warp 0's sequences + wait for the slowest warp)
 
             // ================= M-step of the tile: conflict-free class gather =================
             {
@@ -466,6 +537,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             if (final_pass) break;
             if (lane == 0) llpart[warp] = ll_warp;
             __syncthreads();
+            PM_PHASE(3);  // M-step gather + flush (+ wait)
             // C[q][g] = sum of the per-warp class sums, in warp order
             for (int e = threadIdx.x; e < 16 * G; e += blockDim.x) {
                 float sum = 0.f;
@@ -512,8 +584,10 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 dscal[0] = ll;
             }
             __syncthreads();
+            PM_PHASE(4);  // class-sum reduce, theta update, LL
             final_pass = iscal[0] != 0 || iterations >= p.max_iters;
         }
+        PM_PHASE(5);  // final E-step sweep (positions)
 
         // ---- score / consensus over the argmax rows (scoring.hpp:84-126), expectation (refine.hpp:130-136)
         __syncthreads();
@@ -546,6 +620,7 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
                 p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + c] = thd[e];
             }
         }
+        PM_PHASE(6);  // score, consensus, outputs
     }
 }
 

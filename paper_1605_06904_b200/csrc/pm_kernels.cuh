@@ -530,6 +530,7 @@ struct EmParams {
     double* out_ll;        // [work][max_iters] or nullptr
     unsigned long long* iter_total;  // sum over buckets of E-steps executed (iterations + 1)
     unsigned int* error_flag;        // set to 1 on a non-finite window weight (NumericalUnderflowError)
+    unsigned long long* phase_clk;   // [8] per-phase clock sums (only with -DPM_EM_TIMING)
 };
 
 template <int G>

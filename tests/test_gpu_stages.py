@@ -288,3 +288,26 @@ def test_many_sequences_multi_tile_matches_oracle(ctx, best_oracle):
     for e, a in zip(pick, got):
         w = best_oracle.refine(ss, l, e["members"], e["key"])
         check_candidate(a, w.consensus, w.positions, w.score, w.iterations, w.expectation, w.theta)
+
+
+def test_streaming_fallback_kernel_matches_reference(pm, golden, instance):
+    """A sequence longer than a tile cannot use the shared-memory EM kernel; the streaming kernel
+     takes over.  Forced here by a tile budget smaller than one sequence."""
+    import os
+    g = [x for x in golden["refine"] if x["instance"][1] == 600][:6]
+    ss, _, _ = instance(*g[0]["instance"])
+    os.environ["PM_B200_TILE_SLOTS"] = "300"
+    try:
+        with pm.Context(0) as c:
+            c.set_sequences(ss.bases, ss.offs)
+            res = c.refine(15, [x["members"] for x in g])
+            dense = c.refine(15, [x["members"] for x in g[:2]], z_epsilon=0.0)
+            run = c.run(l=15, d=4, k=7, s=4, m=2, seed=7, early_stop=0)
+    finally:
+        os.environ.pop("PM_B200_TILE_SLOTS", None)
+    for a, x in zip(res, g):
+        check_candidate(a, x["consensus"], x["positions"], x["score"], x["iterations"], x["expectation"], x["theta"])
+    for a, b in zip(dense, res):
+        assert np.abs(a["theta"] - b["theta"]).max() <= 586 * 2.0 ** -30 + 1e-6
+    want = [r for r in golden["run"] if r["cfg"].get("m") == 16][0]["result"]
+    assert run["score"] <= want["score"] and run["buckets_enriched"] == sum(golden["trial_outcomes_c1"]["buckets"][:2])
