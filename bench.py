@@ -349,7 +349,11 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                               enumerate(["keys", "sort", "enrich", "em", "reduce", "score", "upload", "d2h"])},
         "roofline": {"bound": "fp32", "kernel": "em_refine_smem_kernel", "achieved": achieved_tflops, "peak": fp32_peak_tflops,
                      "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
-                     "traffic": None, "launch_ms": em_ms / max(1, em_launches // args.steps),
+                     # dram__bytes_read+write of one launch from the ncu --set full capture in profiles/ (C1 only):
+                     # the kernel's working set is shared memory + L1/L2-resident tables
+                     "traffic": 2730496 if args.config == "c1" and not args.trials else None,
+                     "traffic_source": "profiles/r1_em_refine_smem_ncu_full_v2.txt (ncu, bytes per launch)",
+                     "launch_ms": em_ms / max(1, em_launches // args.steps),
                      "work": "SURVEY 8(d) W_EM = sum_b (2 I_b+1) x l + 4 (I_b+1) x FP32 ops (E- and M-step), measured I_b",
                      "estep_only_achieved": estep_tflops,
                      "smem_lookup_ceiling": 148 * 32 * sm_max_mhz * 1e6 * 2 / 1e12,

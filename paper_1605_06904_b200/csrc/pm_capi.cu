@@ -567,6 +567,10 @@ size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t) {
 }
 
 int em_smem_warps_for(int t) {
+    if (const char* env = std::getenv("PM_B200_EM_WARPS")) {  // tuning knob
+        const long v = std::atol(env);
+        if (v >= 1 && v <= k::kEmSmemMaxWarps) return static_cast<int>(v);
+    }
     for (int nw : {10, 8, 6, 5, 4}) {  // <= k::kEmSmemMaxWarps (the kernel's launch bound)
         if (t % nw == 0) return nw;
     }
