@@ -311,7 +311,7 @@ class Context:
         return int(lib().pm_ctx_total_lmers(self._h, l))
 
     def packed_words(self):
-        nwords = int(sum((int(self.offs[i + 1] - self.offs[i]) + 31) // 32 + 1 for i in range(self.t)))
+        nwords = int(sum((((int(self.offs[i + 1] - self.offs[i]) + 31) // 32 + 2) & ~1) for i in range(self.t)))
         words = np.zeros(nwords, dtype=np.uint64)
         woff = np.zeros(self.t + 1, dtype=np.int64)
         _check(lib().pm_ctx_packed_words(self._h, _p(words, C.c_uint64), _p(woff, C.c_int64), C.c_int64(nwords)))

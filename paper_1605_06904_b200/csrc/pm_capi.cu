@@ -78,6 +78,7 @@ struct pm_ctx {
     int* d_seq_zoff = nullptr;
     k::TileDesc* d_tiles = nullptr;
     int n_tiles = 0;
+    int tile_words = 0;    // most packed words any tile needs (TMA stage size)
     int zlen = 0;          // largest tile's z slots; 0 => some sequence does not fit the shared-memory EM kernel
     int total_groups = 0;
     double group_fill = 0.0;  // live entries / slots of the class-gather rows
@@ -211,7 +212,8 @@ int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
 // position is grouped per class into rows of 32 slots with pairwise distinct addresses mod 32, so
 // the M-step gather is free of bank conflicts.  A layout table like word_off, not arithmetic of
 // the path; it depends on the sequence set only (not on l, the plan or the bucket).
-int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel, int t) {
+int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel,
+                       const std::vector<int64_t>& word_off, int t) {
     const int64_t total = rel[static_cast<size_t>(t)];
     const int64_t single = k::kZPad + total + 32 * static_cast<int64_t>(t);
     // one tile up to ~13.5k slots (3 CTAs/SM); above that, balanced tiles of at most ~12.6k slots
@@ -233,7 +235,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     std::vector<int> load(16 * 32), mine(16 * 32);
     std::vector<std::vector<uint16_t>> bins(16 * 32);
     int64_t live_slots = 0;
-    int zcap = 0;
+    int zcap = 0, wcap = 0;
     int i = 0;
     while (i < t) {
         k::TileDesc tile;
@@ -285,6 +287,9 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         if (i == tile.seq_begin) return PM_OK;  // a single sequence exceeds the z buffer: streaming kernel
         tile.seq_end = i;
         tile.zlen = static_cast<int>(cursor);
+        tile.word_begin = word_off[static_cast<size_t>(tile.seq_begin)];
+        tile.n_words = static_cast<int>(word_off[static_cast<size_t>(tile.seq_end)] - tile.word_begin);
+        wcap = std::max(wcap, tile.n_words);
         zcap = std::max(zcap, tile.zlen);
         int row = 0;
         for (int q = 0; q < 16; ++q) {
@@ -312,6 +317,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     PM_TRY(h2d(c, c->d_tiles, tiles.data(), sizeof(k::TileDesc) * tiles.size()));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     c->zlen = zcap;
+    c->tile_words = wcap;
     c->n_tiles = static_cast<int>(tiles.size());
     c->total_groups = static_cast<int>(entries.size() / 32);
     c->group_fill = entries.empty() ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(entries.size());
@@ -555,7 +561,7 @@ EmSmemKernel em_smem_kernel_for(int l) {
 }
 
 // must mirror the carve-up at the top of em_refine_smem_kernel
-size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t) {
+size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t, int tile_words, int n_tiles) {
     size_t b = 0;
     b += (128 + 128 + static_cast<size_t>(nwarps) + 6) * 8;                               // thd, D64, llpart, dscal
     b += (256 + static_cast<size_t>(nwarps) * 16 * G + 16 * static_cast<size_t>(G)) * 4;  // T, cpart, Cq
@@ -563,6 +569,9 @@ size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t) {
     b += 8;                                                                               // cons_bits
     b += (t <= k::kMaxFusedSeqs ? static_cast<size_t>((t + 1) & ~1) : 0) * 4;               // mprev
     b += static_cast<size_t>(zlen) * 4;                                                   // zbuf
+    b = (b + 15) & ~static_cast<size_t>(15);
+    b += static_cast<size_t>(tile_words) * 8 * (n_tiles > 1 ? 2 : 1);                     // TMA word stage(s)
+    b += 16;                                                                              // two mbarriers
     return b + 16;
 }
 
@@ -650,7 +659,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         const int G = (l + 1) / 2;
         const int nwarps = em_smem_warps_for(c->t);
         const int threads = nwarps * 32;
-        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen, c->t);
+        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen, c->t, c->tile_words, c->n_tiles);
         EmSmemKernel kern = em_smem_kernel_for(l);
         int per_sm = 0;
         if (c->em_cfg_l == l && c->em_cfg_smem == smem && c->em_cfg_threads == threads) {
@@ -674,6 +683,8 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
             x.tile_group_off = c->d_cls_group_off;
             x.seq_zoff = c->d_seq_zoff;
             x.mprev_g = nullptr;
+            x.zcap = c->zlen;
+            x.wcap = c->tile_words;
             if (c->t > k::kMaxFusedSeqs) {
                 PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * static_cast<size_t>(c->t), &x.mprev_g));
             }
@@ -815,7 +826,9 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     for (int i = 0; i < t; ++i) {
         const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
         len[static_cast<size_t>(i)] = static_cast<int32_t>(n);
-        const int64_t nw = (n + 31) / 32 + 1;  // +1 zero pad word: word a+1 of any window exists
+        // +1 zero pad word (word a+1 of any window exists), rounded up to an even count so that every
+        // sequence starts 16-byte aligned: tiles are staged into shared memory with TMA bulk copies
+        const int64_t nw = ((n + 31) / 32 + 2) & ~static_cast<int64_t>(1);
         word_off[static_cast<size_t>(i) + 1] = word_off[static_cast<size_t>(i)] + nw;
         max_words = std::max(max_words, nw);
     }
@@ -848,7 +861,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     k::encode_kernel<<<grid, warps_per_block * 32, 0, c->stream>>>(d_ascii, d_offs, c->d_word_off, t, c->d_words,
                                                                  c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
     PM_TRY(check_launch(c, "encode"));
-    PM_TRY(build_class_groups(c, bases + base0, rel, t));  // host index build overlaps the encode kernel
+    PM_TRY(build_class_groups(c, bases + base0, rel, word_off, t));  // host index build overlaps the encode kernel
     unsigned long long host_tot[5];
     PM_TRY(d2h(c, host_tot, c->d_tot_sym, sizeof(host_tot)));
     PM_CUDA(cudaStreamSynchronize(c->stream));

@@ -35,6 +35,8 @@ struct TileDesc {
     int seq_begin, seq_end;  // sequences [seq_begin, seq_end)
     int zlen;                // z slots used by the tile (front pad + sequences + balancing gaps)
     int group_base;          // first row of the tile in cls_entries
+    int n_words;             // packed words of the tile's sequences (even per sequence => 16-byte multiples)
+    int64_t word_begin;      // first packed word of the tile
 };
 
 struct EmSmemExtra {
@@ -44,6 +46,8 @@ struct EmSmemExtra {
     const int* tile_group_off;    // [n_tiles][17] first row of each class, relative to group_base
     const int* seq_zoff;          // [t] first z slot of each sequence within its tile
     float* mprev_g;               // [gridDim.x][t] previous per-sequence maxima when t > kMaxFusedSeqs
+    int zcap;                     // largest tile zlen (z buffer size)
+    int wcap;                     // largest tile n_words (TMA stage size)
 };
 
 __device__ __forceinline__ double warp_max_d(double v) {
@@ -94,6 +98,34 @@ __device__ __forceinline__ void window_halves(uint64_t hi, uint64_t lo, int lane
     const uint32_t a = upper ? h0 : h1, b = upper ? l1 : h0, c = upper ? l0 : l1;
     vh = __funnelshift_l(b, a, sh);
     vl = __funnelshift_l(c, b, sh);
+}
+
+// ---- TMA 1-D bulk copy global -> shared with mbarrier completion (sm_90+; SASS: UBLKCP)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ float fast_ex2(float x) {
@@ -244,6 +276,23 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
     const int n_mprev = t <= kMaxFusedSeqs ? ((t + 1) & ~1) : 0;
     float* zbuf = mprev_s + n_mprev;                    // [max tile zlen]
     float* mprev = n_mprev > 0 ? mprev_s : x.mprev_g + static_cast<size_t>(blockIdx.x) * t;
+    // packed words of the current tile (and, with several tiles, of the next one), filled by TMA
+    uint64_t* wstage = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(zbuf + x.zcap) + 15) & ~static_cast<uintptr_t>(15));
+    const int n_stages = x.n_tiles > 1 ? 2 : 1;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wstage + static_cast<size_t>(x.wcap) * n_stages);
+    // visit v of the cyclic tile walk uses stage v % n_stages; its data is complete when mbar[stage] has
+    // flipped (v / n_stages) & 1 ... tracked as a running visit counter
+    unsigned int visit = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const TileDesc t0 = x.tiles[0];
+        mbar_expect_tx(&mbar[0], static_cast<unsigned>(t0.n_words) * 8u);
+        tma_load_1d(wstage, p.words + t0.word_begin, static_cast<unsigned>(t0.n_words) * 8u, &mbar[0]);
+    }
+    __syncthreads();
 
     int* my_near = near_j + warp * kNearCap;
     const int colshift = 62 - 2 * lane;
@@ -314,11 +363,26 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             for (int e = lane; e < 16 * G; e += 32) cpart[warp * 16 * G + e] = 0.f;  // this warp's class sums
             for (int tile_i = 0; tile_i < x.n_tiles; ++tile_i) {
             const TileDesc tile = x.tiles[tile_i];
+            // ---- packed words of this tile: staged by TMA (single tile: once for the whole kernel)
+            const uint64_t* __restrict__ wtile = wstage + static_cast<size_t>(x.wcap) * (visit % n_stages);
+            if (x.n_tiles > 1) {
+                if (threadIdx.x == 0) {  // prefetch the next tile of the cyclic walk into the other stage
+                    const TileDesc nt = x.tiles[tile_i + 1 < x.n_tiles ? tile_i + 1 : 0];
+                    unsigned long long* nb = &mbar[(visit + 1) & 1];
+                    mbar_expect_tx(nb, static_cast<unsigned>(nt.n_words) * 8u);
+                    tma_load_1d(wstage + static_cast<size_t>(x.wcap) * ((visit + 1) & 1), p.words + nt.word_begin,
+                                static_cast<unsigned>(nt.n_words) * 8u, nb);
+                }
+                mbar_wait(&mbar[visit & 1], (visit >> 1) & 1);
+            } else if (visit == 0) {
+                mbar_wait(&mbar[0], 0);
+            }
+            ++visit;
             // ================= E-step: warp per sequence of the tile =================
             if (threadIdx.x < 17) s_off[threadIdx.x] = x.tile_group_off[tile_i * 17 + threadIdx.x];
             for (int k = threadIdx.x, k_end = x.seq_zoff[tile.seq_begin]; k < k_end; k += blockDim.x) zbuf[k] = 0.f;  // front pad
             for (int i = tile.seq_begin + warp; i < tile.seq_end; i += nwarps) {
-                const uint64_t* __restrict__ wp = p.words + p.word_off[i];
+                const uint64_t* __restrict__ wp = wtile + (p.word_off[i] - tile.word_begin);
                 const int W = p.seq_len[i] - l + 1;
                 const int chunks = (W + 31) >> 5;
                 float* zs = zbuf + x.seq_zoff[i];
@@ -621,6 +685,12 @@ em_refine_smem_kernel(const EmParams p, const EmSmemExtra x) {
             }
         }
         PM_PHASE(6);  // score, consensus, outputs
+    }
+    // no bulk copy may still be in flight into this CTA's shared memory when it exits
+    if (x.n_tiles > 1) {
+        mbar_wait(&mbar[visit & 1], (visit >> 1) & 1);
+    } else if (visit == 0) {
+        mbar_wait(&mbar[0], 0);
     }
 }
 

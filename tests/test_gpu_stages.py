@@ -20,7 +20,7 @@ def pack_reference(strings):
     """DESIGN.md §3 layout restated in Python: base p at bits [62-2(p%32), 64-2(p%32)) of word p/32."""
     words, woff = [], [0]
     for s in strings:
-        nw = (len(s) + 31) // 32 + 1
+        nw = ((len(s) + 31) // 32 + 2) & ~1  # zero pad word, even count (16-byte aligned sequences for TMA)
         for w in range(nw):
             v = 0
             for p in range(32):
