@@ -22,6 +22,7 @@
 #include "pm_internal.hpp"
 #include "pm_kernels.cuh"
 #include "pm_em_smem.cuh"
+#include "pm_em_pair.cuh"
 
 using namespace pm;
 
@@ -84,6 +85,9 @@ struct pm_ctx {
     double group_fill = 0.0;  // live entries / slots of the class-gather rows
     int em_cfg_l = -1, em_cfg_threads = 0, em_cfg_per_sm = 0;  // cached launch setup of the smem EM kernel
     size_t em_cfg_smem = 0;
+    int pair_cfg_l = -1, pair_cfg_threads = 0, pair_cfg_per_sm = 0;  // same for the two-bucket kernel
+    size_t pair_cfg_smem = 0;
+    int32_t max_seq_len = 0;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -307,6 +311,8 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         group_off.push_back(row);
         tiles.push_back(tile);
     }
+    const size_t live_rows = entries.size() / 32;
+    for (int r = 0; r < 2 * 32; ++r) entries.push_back(static_cast<uint16_t>(32 + (r & 31)));  // rows the gather's prefetch may touch
     PM_TRY(ensure(c, &c->d_cls_entries, &c->cap_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
     PM_TRY(ensure(c, &c->d_cls_group_off, &c->cap_cls_group_off, sizeof(int) * group_off.size()));
     PM_TRY(ensure(c, &c->d_seq_zoff, &c->cap_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
@@ -319,8 +325,8 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     c->zlen = zcap;
     c->tile_words = wcap;
     c->n_tiles = static_cast<int>(tiles.size());
-    c->total_groups = static_cast<int>(entries.size() / 32);
-    c->group_fill = entries.empty() ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(entries.size());
+    c->total_groups = static_cast<int>(live_rows);
+    c->group_fill = live_rows == 0 ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(live_rows * 32);
     return PM_OK;
 }
 
@@ -560,6 +566,53 @@ EmSmemKernel em_smem_kernel_for(int l) {
     }
 }
 
+template <int G>
+EmSmemKernel em_pair_for() { return k::em_refine_pair_kernel<G>; }
+
+EmSmemKernel em_pair_kernel_for(int l) {
+    switch ((l + 1) / 2) {
+        case 1: return em_pair_for<1>();
+        case 2: return em_pair_for<2>();
+        case 3: return em_pair_for<3>();
+        case 4: return em_pair_for<4>();
+        case 5: return em_pair_for<5>();
+        case 6: return em_pair_for<6>();
+        case 7: return em_pair_for<7>();
+        case 8: return em_pair_for<8>();
+        case 9: return em_pair_for<9>();
+        case 10: return em_pair_for<10>();
+        case 11: return em_pair_for<11>();
+        case 12: return em_pair_for<12>();
+        case 13: return em_pair_for<13>();
+        case 14: return em_pair_for<14>();
+        case 15: return em_pair_for<15>();
+        default: return em_pair_for<16>();
+    }
+}
+
+// must mirror the carve-up at the top of em_refine_pair_kernel
+size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_words) {
+    const size_t TH = 4 * (static_cast<size_t>(l) + 1), tpad = (static_cast<size_t>(t) + 1) & ~static_cast<size_t>(1);
+    const size_t NV = 2 * G <= 16 ? 16 : 32;
+    size_t b = 0;
+    b += (2 * TH + 2 * TH + 2 * TH + 2 * static_cast<size_t>(nwarps) + 12) * 8;              // thd, D64, L64, llpart, dscal
+    b += 16 * static_cast<size_t>(G) * 8;                                                    // T2
+    b += (32 * static_cast<size_t>(G) + (16 + static_cast<size_t>(nwarps)) * NV + 2 * tpad + 4) * 4;  // Cq, cpart, mprev, ubs
+    b += (256 + 8 + 20 + 12 + 4 * tpad) * 4;                                                 // prof, iscal, s_off, wrow, smeta
+    b += 16;                                                                                 // cons_bits
+    b += static_cast<size_t>(nwarps) * 2 * k::kPairNearCap * 2;                              // near_j
+    b = (b + 15) & ~static_cast<size_t>(15);
+    b += ((static_cast<size_t>(zcap) + 1) & ~static_cast<size_t>(1)) * 8;                    // zbuf (float2), 16-byte multiple
+    b += static_cast<size_t>(total_words) * 8;                                               // TMA word stage
+    b += 16;                                                                                 // mbarrier
+    return b + 16;
+}
+
+bool em_pair_enabled() {
+    const char* env = std::getenv("PM_B200_EM_PAIR");  // test/tuning knob: 0 selects the one-bucket kernel
+    return env == nullptr || std::atoi(env) != 0;
+}
+
 // must mirror the carve-up at the top of em_refine_smem_kernel
 size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t, int tile_words, int n_tiles) {
     size_t b = 0;
@@ -654,6 +707,44 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
     p.phase_clk = d_scal + 8;
 
+    if (c->zlen > 0 && c->t <= k::kPairMaxSeqs && c->total_words <= k::kPairMaxWords &&
+        c->max_seq_len < 65536 && em_pair_enabled()) {
+        // two buckets per CTA in lockstep (pm_em_pair.cuh): every t=20 configuration
+        const int G = (l + 1) / 2;
+        const int nwarps = em_smem_warps_for(c->t);
+        const int threads = nwarps * 32;
+        const size_t smem = em_pair_smem_bytes(nwarps, G, l, c->zlen, c->t, static_cast<int>(c->total_words));
+        if (smem <= 227 * 1024) {
+            EmSmemKernel kern = em_pair_kernel_for(l);
+            int per_sm = 0;
+            if (c->pair_cfg_l == l && c->pair_cfg_smem == smem && c->pair_cfg_threads == threads) {
+                per_sm = c->pair_cfg_per_sm;
+            } else {
+                PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+                PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+                c->pair_cfg_l = l;
+                c->pair_cfg_smem = smem;
+                c->pair_cfg_threads = threads;
+                c->pair_cfg_per_sm = per_sm;
+            }
+            if (per_sm >= 1) {
+                const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
+                const unsigned int grid = std::max(1u, std::min(full, (n_work_bound + 1) / 2));
+                k::EmSmemExtra x;
+                x.tiles = c->d_tiles;
+                x.n_tiles = c->n_tiles;
+                x.cls_entries = c->d_cls_entries;
+                x.tile_group_off = c->d_cls_group_off;
+                x.seq_zoff = c->d_seq_zoff;
+                x.mprev_g = nullptr;
+                x.zcap = c->zlen;
+                x.wcap = static_cast<int>(c->total_words);
+                kern<<<grid, threads, smem, c->stream>>>(p, x);
+                return check_launch(c, "em_refine_pair");
+            }
+        }
+    }
     if (c->zlen > 0) {
         // shared-memory kernel: z of every window resident per CTA, conflict-free class-gather M-step
         const int G = (l + 1) / 2;
@@ -817,6 +908,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     c->n_tiles = 0;
     c->total_groups = 0;
     c->em_cfg_l = -1;
+    c->pair_cfg_l = -1;
 
     const int64_t base0 = offs[0];
     std::vector<int64_t> rel(static_cast<size_t>(t) + 1), word_off(static_cast<size_t>(t) + 1, 0);
@@ -879,6 +971,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     c->seq_len = len;
     c->total_bases = total_bases;
     c->total_words = total_words;
+    c->max_seq_len = *std::max_element(len.begin(), len.end());
     return PM_OK;
 }
 

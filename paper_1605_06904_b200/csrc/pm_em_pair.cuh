@@ -1,0 +1,863 @@
+// pm_em_pair.cuh — EM refinement, TWO enriched buckets per CTA in lockstep (every t <= 64 config whose packed
+// words fit one 16 KB TMA stage: all t=20 configs of BASELINE.json).
+//
+// Same algorithm, precision scheme and tile/class-group index as pm_em_smem.cuh (refine.hpp:90-326); what
+// changes is that everything that depends on the SEQUENCE SET only is done once for two buckets:
+//   * the window word assembly and the nibble offsets of the E-step: one LDS.64 fetches the pair-table
+//     entries {T_A[g][q], T_B[g][q]} of both buckets (16 entries x 8 B = all 32 banks, conflict-free);
+//   * the responsibilities are stored interleaved {z_A[j], z_B[j]} so the M-step's class-row entry (slot of
+//     the base position) is loaded once and each LDS.64 of the gather feeds both buckets' accumulators
+//     (rows built for distinct slots mod 32 are also conflict-free for 8-byte slots: each half-warp covers
+//     the 32 banks exactly once);
+//   * loop control, prefetch of the class rows, sequence metadata.
+// Instruction count per bucket drops ~2x against the one-bucket kernel; shared-memory wavefronts per bucket
+// stay the same (8 per 32 windows in the E-step, 8 per class row in the M-step), which is the bound.
+//
+// Buckets of a pair iterate in lockstep.  A bucket whose likelihood gain fell below tol (refine.hpp:300) is
+// frozen: its theta is no longer updated, the lockstep sweeps it still takes part in do not change any of
+// its outputs, and its `iterations` is the count at the freeze.  The final E-step runs once for both.
+#pragma once
+#include "pm_em_smem.cuh"
+
+namespace pm {
+namespace k {
+
+constexpr int kPairMaxWarps = 10;
+constexpr int kPairMaxSeqs = 64;     // per-sequence state (previous maxima, metadata) lives in shared memory
+constexpr int kPairMaxWords = 2048;  // packed words of the whole set, staged once per CTA by one TMA bulk copy
+constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
+
+// The per-sequence bookkeeping around the two hot loops is large straight-line code that every warp walks
+// once per sequence; it is kept to ONE copy (rolled bucket loops, out-of-line FP64 exp/log) so the kernel
+// stays inside the instruction cache.
+__device__ __noinline__ double exp_f64(double x) { return exp(x); }
+__device__ __noinline__ double log_f64(double x) { return log(x); }
+
+__device__ __forceinline__ double window_weight_rolled(const double* __restrict__ D64, uint64_t v, int l) {
+    double w = 0.0;
+#pragma unroll 2
+    for (int c = 0; c < l; ++c) w += D64[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)];
+    return w;
+}
+
+struct SeqAcc {
+    float best_w, s_all, s_far;
+    int best_j, nnear, ncand;
+    bool overflow;
+};
+
+__device__ __forceinline__ void near_push16(unsigned ball, bool keep, int lane, int j, uint16_t* __restrict__ my_near,
+                                            int& nnear, bool& overflow) {
+    if (ball && !overflow) {
+        const int cnt = __popc(ball);
+        if (nnear + cnt > kPairNearCap) {
+            overflow = true;
+        } else {
+            if (keep) my_near[nnear + __popc(ball & ((1u << lane) - 1u))] = static_cast<uint16_t>(j);
+            nnear += cnt;
+        }
+    }
+}
+
+// byte offset of pair-table entry (nibble g of the window) for 8-byte entries
+template <int g>
+__device__ __forceinline__ uint32_t nibble_off8(uint32_t vh, uint32_t vl) {
+    return g < 7    ? (vh >> (25 - 4 * g)) & 0x78u
+           : g == 7 ? (vh << 3) & 0x78u
+           : g < 15 ? (vl >> (57 - 4 * g)) & 0x78u
+                    : (vl << 3) & 0x78u;
+}
+
+template <int G, int g = 0>
+struct PairLookup {
+    static __device__ __forceinline__ void run(const float2* __restrict__ T2, uint32_t vh, uint32_t vl, float2* t) {
+        t[g] = *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(T2) + g * 128 + nibble_off8<g>(vh, vl));
+        PairLookup<G, g + 1>::run(T2, vh, vl, t);
+    }
+    static __device__ __forceinline__ void run1(const float* __restrict__ Tb, uint32_t vh, uint32_t vl, float* t) {
+        t[g] = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(Tb) + g * 128 + nibble_off8<g>(vh, vl));
+        PairLookup<G, g + 1>::run1(Tb, vh, vl, t);
+    }
+};
+template <int G>
+struct PairLookup<G, G> {
+    static __device__ __forceinline__ void run(const float2*, uint32_t, uint32_t, float2*) {}
+    static __device__ __forceinline__ void run1(const float*, uint32_t, uint32_t, float*) {}
+};
+
+// log-odds of one window under both buckets' pair tables (FP32, pairwise-tree sums)
+template <int G>
+__device__ __forceinline__ void pair_weights(const float2* __restrict__ T2, uint32_t vh, uint32_t vl, float& w0, float& w1) {
+    float2 t[G];
+    PairLookup<G>::run(T2, vh, vl, t);
+#pragma unroll
+    for (int s = 1; s < G; s <<= 1) {
+#pragma unroll
+        for (int g = 0; g + s < G; g += 2 * s) {
+            t[g].x += t[g + s].x;
+            t[g].y += t[g + s].y;
+        }
+    }
+    w0 = t[0].x;
+    w1 = t[0].y;
+}
+
+// one bucket only (Tb = the float view of T2 offset by the bucket): same association as pair_weights
+template <int G>
+__device__ __forceinline__ float single_weight(const float* __restrict__ Tb, uint32_t vh, uint32_t vl) {
+    float t[G];
+    PairLookup<G>::run1(Tb, vh, vl, t);
+#pragma unroll
+    for (int s = 1; s < G; s <<= 1) {
+#pragma unroll
+        for (int g = 0; g + s < G; g += 2 * s) t[g] += t[g + s];
+    }
+    return t[0];
+}
+
+template <bool kExp, bool kTail>
+__device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live, float2* __restrict__ zq, float ref2a,
+                                            float ref2b, float near_thr, SeqAcc& a, SeqAcc& b);
+
+// kExp: stores e = exp(w - ref) of both buckets, sums them, counts each lane's windows with e >= near_thr.
+// !kExp (final sweep): stores w, tracks each lane's first maximum.
+template <int G, bool kExp, bool kTail>
+__device__ __forceinline__ void pair_chunk(const float2* __restrict__ T2, uint32_t vh, uint32_t vl, int j, bool live,
+                                           float2* __restrict__ zq, float ref2a, float ref2b, float near_thr, SeqAcc& a,
+                                           SeqAcc& b) {
+    float w0 = -INFINITY, w1 = -INFINITY;
+    if (!kTail || live) pair_weights<G>(T2, vh, vl, w0, w1);
+    pair_finish<kExp, kTail>(w0, w1, j, live, zq, ref2a, ref2b, near_thr, a, b);
+}
+
+// second half of pair_chunk: from the two weights to the stored value and the running sums
+template <bool kExp, bool kTail>
+__device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live, float2* __restrict__ zq, float ref2a,
+                                            float ref2b, float near_thr, SeqAcc& a, SeqAcc& b) {
+    if (!kTail || live) {
+        if (kExp) {
+            const float e0 = fast_ex2(fmaf(w0, kLog2e, -ref2a));
+            const float e1 = fast_ex2(fmaf(w1, kLog2e, -ref2b));
+            *zq = make_float2(e0, e1);
+            a.s_all += e0;
+            b.s_all += e1;
+            a.ncand += e0 >= near_thr ? 1 : 0;
+            b.ncand += e1 >= near_thr ? 1 : 0;
+        } else {
+            *zq = make_float2(w0, w1);
+        }
+    }
+    if (kExp) {
+        a.best_w = fmaxf(a.best_w, w0);
+        b.best_w = fmaxf(b.best_w, w1);
+    } else {
+        if (w0 > a.best_w) {  // strict: the earliest offset is kept
+            a.best_w = w0;
+            a.best_j = j;
+        }
+        if (w1 > b.best_w) {
+            b.best_w = w1;
+            b.best_j = j;
+        }
+    }
+}
+
+template <int G, bool kExp>
+__device__ __forceinline__ void pair_pass_a(const float2* __restrict__ T2, const uint64_t* __restrict__ wp, int W, int lane,
+                                            float2* __restrict__ zs, float refa, float refb, float near_thr, SeqAcc& a,
+                                            SeqAcc& b) {
+    const float ref2a = refa * kLog2e, ref2b = refb * kLog2e;
+    uint64_t hi = wp[0];
+    const uint64_t* __restrict__ wq = wp + 1;
+    float2* __restrict__ zq = zs + lane;
+    int j = lane;
+    // two chunks per trip: all sixteen table lookups are issued before the first dependent add (the compiler
+    // does not move shared-memory loads across the z stores on its own)
+    for (const int j_two = (W & ~63); j < j_two; j += 64) {
+        const uint64_t lo1 = wq[0], lo2 = wq[1];
+        wq += 2;
+        uint32_t vh1, vl1, vh2, vl2;
+        window_halves(hi, lo1, lane, vh1, vl1);
+        window_halves(lo1, lo2, lane, vh2, vl2);
+        hi = lo2;
+        float w0, w1, w2, w3;
+        pair_weights<G>(T2, vh1, vl1, w0, w1);
+        pair_weights<G>(T2, vh2, vl2, w2, w3);
+        pair_finish<kExp, false>(w0, w1, j, true, zq, ref2a, ref2b, near_thr, a, b);
+        pair_finish<kExp, false>(w2, w3, j + 32, true, zq + 32, ref2a, ref2b, near_thr, a, b);
+        zq += 64;
+    }
+    for (const int j_full = W & ~31; j < j_full; j += 32) {
+        const uint64_t lo = *wq++;
+        uint32_t vh, vl;
+        window_halves(hi, lo, lane, vh, vl);
+        hi = lo;
+        pair_chunk<G, kExp, false>(T2, vh, vl, j, true, zq, ref2a, ref2b, near_thr, a, b);
+        zq += 32;
+    }
+    if ((W & 31) != 0) {
+        uint32_t vh, vl;
+        window_halves(hi, *wq, lane, vh, vl);
+        pair_chunk<G, kExp, true>(T2, vh, vl, j, j < W, zq, ref2a, ref2b, near_thr, a, b);
+    }
+}
+
+// one bucket, plain weights into its half of the interleaved buffer (fallback when the maximum moved too far)
+template <int G>
+__device__ __forceinline__ void single_pass_w(const float* __restrict__ Tb, const uint64_t* __restrict__ wp, int W, int lane,
+                                              float* __restrict__ zb, float& best_w) {
+    const int chunks = (W + 31) >> 5;
+    uint64_t hi = wp[0];
+    for (int c = 0; c < chunks; ++c) {
+        const uint64_t lo = wp[c + 1];
+        uint32_t vh, vl;
+        window_halves(hi, lo, lane, vh, vl);
+        hi = lo;
+        const int j = (c << 5) + lane;
+        if (j < W) {
+            const float w = single_weight<G>(Tb, vh, vl);
+            zb[2 * j] = w;
+            best_w = fmaxf(best_w, w);
+        }
+    }
+}
+
+// sweep over one bucket's stored values (stride 2): kFromW turns stored w into e = exp(w - M) first
+template <bool kFromW>
+__device__ __forceinline__ void pair_detect(float* __restrict__ zb, int W, int lane, float M, float thr, float& s_all,
+                                            float& s_far, uint16_t* __restrict__ my_near, int& nnear, bool& overflow) {
+    const int chunks = (W + 31) >> 5;
+    for (int c = 0; c < chunks; ++c) {
+        const int j = (c << 5) + lane;
+        float e = 0.f;
+        bool keep = false;
+        if (j < W) {
+            e = zb[2 * j];
+            if (kFromW) {
+                e = fast_ex2((e - M) * kLog2e);
+                zb[2 * j] = e;
+            }
+            keep = e >= thr;
+        }
+        s_all += e;
+        s_far += keep ? 0.f : e;
+        near_push16(__ballot_sync(0xffffffffu, keep), keep, lane, j, my_near, nnear, overflow);
+    }
+}
+
+// After pass A of one sequence, one bucket: settle the reference maximum, the near list and the normaliser.
+// Returns 1/total; ref is updated when the fallback re-based the stored values on M.  The near list (windows
+// with e >= near_e, i.e. within log_z_eps of the maximum) is built by a second light sweep over the stored
+// values, and only when it can be short enough to be used: pass A merely counted the candidates against a
+// threshold kNearMargin below the previous maximum.
+template <int G>
+__device__ __forceinline__ float pair_settle(const float* __restrict__ Tb, const uint64_t* __restrict__ wp, int W, int lane,
+                                             float* __restrict__ zb, uint16_t* __restrict__ my_near, SeqAcc& a, float& ref,
+                                             float& M, float& near_e, float log_z_eps, bool force_rebuild, bool want_near,
+                                             int* bad) {
+    constexpr float kNearMargin = 4.f;
+    M = warp_max_f(a.best_w);
+    if (!(M > -INFINITY) || !(M < INFINITY)) *bad = 1;
+    float total = warp_sum_f(a.s_all);
+    const float shift = M - ref;
+    const bool have_e = shift > -60.f && shift < 60.f && total > 0.f && total < INFINITY;
+    if (!have_e) {
+        // the maximum is too far from the reference for FP32 range: redo this bucket as two passes
+        __syncwarp();
+        float bw = -INFINITY;
+        single_pass_w<G>(Tb, wp, W, lane, zb, bw);
+        M = warp_max_f(bw);
+        if (!(M > -INFINITY) || !(M < INFINITY)) *bad = 1;
+        __syncwarp();
+        ref = M;
+        near_e = fast_ex2(log_z_eps * kLog2e);
+        a.s_all = 0.f, a.s_far = 0.f, a.nnear = 0, a.overflow = false;
+        pair_detect<true>(zb, W, lane, M, near_e, a.s_all, a.s_far, my_near, a.nnear, a.overflow);
+        total = warp_sum_f(a.s_all);
+    } else {
+        near_e = fast_ex2((shift + log_z_eps) * kLog2e);
+        a.overflow = true;
+        if (want_near) {
+            // the count is an upper bound of the list length unless the maximum dropped below the margin
+            const int n = __reduce_add_sync(0xffffffffu, a.ncand);
+            if (force_rebuild || M < ref - kNearMargin || n <= kPairNearCap) {
+                __syncwarp();
+                float ignore = 0.f;
+                a.s_far = 0.f, a.nnear = 0, a.overflow = false;
+                pair_detect<false>(zb, W, lane, M, near_e, ignore, a.s_far, my_near, a.nnear, a.overflow);
+            }
+        }
+    }
+    if (!(total > 0.f)) *bad = 1;
+    return 1.f / total;
+}
+
+// transposed warp reduction of N values (N = 16 or 32): afterwards lane L holds the warp-wide sum of
+// v[(L * N) >> 5] in v[0] (both lanes of a pair for N = 16)
+template <int N>
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[N], int lane) {
+#pragma unroll
+    for (int n = N / 2, o = 16; n >= 1; n >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            const float keep = up ? v[i + n] : v[i];
+            const float send = up ? v[i] : v[i + n];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    if (N == 16) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    return v[0];
+}
+
+template <int G>
+__global__ void __launch_bounds__(kPairMaxWarps * 32, 2)
+em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int l = p.l, t = p.t;
+    const int TH = 4 * (l + 1);
+    const int tpad = (t + 1) & ~1;
+    constexpr int NV = 2 * G <= 16 ? 16 : 32;  // values per class flush (2 buckets x G column pairs, padded)
+
+    // ---- shared memory carve-up (mirrored by em_pair_smem_bytes on the host)
+    double* thd = reinterpret_cast<double*>(smem_raw);        // [2][TH] theta, cell 4c+r, column 0 = background
+    double* D64 = thd + 2 * TH;                               // [2][TH] log theta[r][c+1] - log theta[r][0]
+    double* L64 = D64 + 2 * TH;                               // [2][TH] log max(theta, 1e-9), written with theta
+    double* llpart = L64 + 2 * TH;                            // [nwarps][2]
+    double* dscal = llpart + 2 * nwarps;                      // [2][6]: [0] previous LL, [2..5] log background
+    float2* T2 = reinterpret_cast<float2*>(dscal + 12);       // [G][16] {bucket 0, bucket 1}
+    float* Cq = reinterpret_cast<float*>(T2 + 16 * G);        // [2][16][G] class sums
+    float* cpart = Cq + 32 * G;                               // [16 + nwarps][NV] slot = warp + class
+    float* mprev = cpart + (16 + nwarps) * NV;                // [2][tpad] previous per-sequence maxima
+    float* ubs = mprev + 2 * tpad;                            // [2] upper bound of any window weight (+2 pad)
+    int* prof = reinterpret_cast<int*>(ubs + 4);              // [2][128]
+    int* iscal = prof + 256;                                  // [2][4]: [0] stop [1] score [2] bad [3] iterations
+    int* s_off = iscal + 8;                                   // [17] first row of each class (+3 pad)
+    int* wrow = s_off + 20;                                   // [nwarps + 1] class-row range of each warp (12 slots)
+    int* smeta = wrow + 12;                                  // [tpad][4]: word offset, windows, z offset, z slots
+    unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(smeta + 4 * tpad);  // [2]
+    uint16_t* near_j = reinterpret_cast<uint16_t*>(cons_bits + 2);                            // [nwarps][2][kPairNearCap]
+    // offsets are aligned as integers (smem_raw is 16-byte aligned) so that every pointer below stays a
+    // provable shared-memory address: LDS/STS, not generic loads
+    const unsigned int z_off = (static_cast<unsigned int>(reinterpret_cast<unsigned char*>(near_j + nwarps * 2 * kPairNearCap) - smem_raw) + 15u) & ~15u;
+    float2* zbuf = reinterpret_cast<float2*>(smem_raw + z_off);
+    uint64_t* wstage = reinterpret_cast<uint64_t*>(smem_raw + z_off + static_cast<unsigned int>((x.zcap + 1) & ~1) * 8u);
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wstage + x.wcap);
+
+    // ---- packed words of the whole set: one TMA bulk copy per CTA, resident for every bucket
+    const int64_t word0 = x.tiles[0].word_begin;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar[0], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&mbar[0], static_cast<unsigned>(x.wcap) * 8u);
+        tma_load_1d(wstage, p.words + word0, static_cast<unsigned>(x.wcap) * 8u, &mbar[0]);
+    }
+    for (int i = threadIdx.x; i < t; i += blockDim.x) {
+        smeta[4 * i + 0] = static_cast<int>(p.word_off[i] - word0);
+        smeta[4 * i + 1] = p.seq_len[i] - l + 1;
+        smeta[4 * i + 2] = x.seq_zoff[i];
+    }
+    __syncthreads();
+    mbar_wait(&mbar[0], 0);
+
+    double sum_logw = 0.0;  // sum_i log W_i, used by the two threads that close an iteration
+    if (threadIdx.x >= blockDim.x - 2) {
+        for (int i = 0; i < t; ++i) sum_logw += p.seq_logw[i];
+    }
+    uint16_t* near_a = near_j + (warp * 2 + 0) * kPairNearCap;
+    uint16_t* near_b = near_j + (warp * 2 + 1) * kPairNearCap;
+    const int colshift = 62 - 2 * lane;
+    const float* T2f = reinterpret_cast<const float*>(T2);
+    float* zf = reinterpret_cast<float*>(zbuf);
+
+    const unsigned int n_work = p.n_work_dev ? *p.n_work_dev : p.n_work;
+    const unsigned int n_pairs = (n_work + 1) >> 1;
+    for (unsigned int pi = blockIdx.x; pi < n_pairs; pi += gridDim.x) {
+        const bool live1 = 2 * pi + 1 < n_work;
+        const unsigned int wis[2] = {2 * pi, live1 ? 2 * pi + 1 : 2 * pi};  // an odd tail refines its bucket twice
+        const WorkDesc wd0 = p.work[wis[0]], wd1 = p.work[wis[1]];
+        __syncthreads();
+#ifdef PM_EM_TIMING
+        long long t_phase = clock64();
+#endif
+
+        // ---- init_model (refine.hpp:90-127), pseudocount 0
+        #pragma unroll 1
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) prof[i] = 0;
+        if (threadIdx.x < 2) {
+            iscal[threadIdx.x * 4 + 0] = 0;
+            iscal[threadIdx.x * 4 + 2] = 0;
+            iscal[threadIdx.x * 4 + 3] = 0;
+            dscal[threadIdx.x * 6] = 0.0;
+        }
+        __syncthreads();
+        #pragma unroll 1
+        for (unsigned int m = threadIdx.x; m < wd0.count + wd1.count; m += blockDim.x) {
+            const int b = m >= wd0.count;
+            const int64_t f = b ? p.members[wd1.mem_begin + (m - wd0.count)] : p.members[wd0.mem_begin + m];
+            const int i = seq_of_flat(p.win_off, t, f);
+            const uint64_t v = load_window(wstage + smeta[4 * i], f - p.win_off[i]);
+            #pragma unroll 1
+            for (int c = 0; c < l; ++c) atomicAdd(&prof[b * 128 + c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)], 1);
+        }
+        __syncthreads();
+        #pragma unroll 1
+        for (int e2 = threadIdx.x; e2 < 2 * TH; e2 += blockDim.x) {
+            const int b = e2 >= TH, e = e2 - b * TH;
+            const int c = e >> 2, r = e & 3;
+            const double tv = c == 0 ? p.tot_sym[r] / p.tot_bases
+                                     : static_cast<double>(prof[b * 128 + (c - 1) * 4 + r]) / static_cast<double>(b ? wd1.count : wd0.count);
+            thd[e2] = tv;
+            L64[e2] = log_f64(fmax(tv, 1e-9));
+        }
+        __syncthreads();
+
+        PM_PHASE(0);  // init_model
+        int iterations = 0;  // lockstep sweeps done
+        bool stop0 = false, stop1 = false;
+        bool final_pass = false;
+        for (;;) {
+            // ---- log tables of the current thetas (refine.hpp:155-161) from L64 = log max(theta, 1e-9), which the
+            // thread that wrote a theta cell stored next to it: FP64 differences, rounded once to FP32
+            #pragma unroll 1
+            for (int e2 = threadIdx.x; e2 < 2 * 4 * l; e2 += blockDim.x) {
+                const int b = e2 >= 4 * l, e = e2 - b * 4 * l;
+                D64[b * TH + e] = L64[b * TH + e + 4] - L64[b * TH + (e & 3)];
+            }
+            if (threadIdx.x >= blockDim.x - 8) {
+                const int k8 = threadIdx.x - (blockDim.x - 8);
+                dscal[(k8 >> 2) * 6 + 2 + (k8 & 3)] = L64[(k8 >> 2) * TH + (k8 & 3)];
+            }
+            if (final_pass) {
+                #pragma unroll 1
+                for (int i = threadIdx.x; i < 256; i += blockDim.x) prof[i] = 0;
+                if (threadIdx.x < 2) {
+                    iscal[threadIdx.x * 4 + 1] = 0;
+                    cons_bits[threadIdx.x] = 0ULL;
+                }
+            }
+            #pragma unroll 1
+            for (int e2 = threadIdx.x; e2 < 32 * G; e2 += blockDim.x) {
+                const int b = e2 & 1, e = e2 >> 1;
+                const int g = e >> 4, q = e & 15;
+                const int c0 = 2 * g, c1 = 2 * g + 1;
+                const double* L = L64 + b * TH;
+                double v = 0.0;
+                if (c0 < l) v = L[(c0 + 1) * 4 + (q >> 2)] - L[q >> 2];
+                if (c1 < l) v += L[(c1 + 1) * 4 + (q & 3)] - L[q & 3];
+                reinterpret_cast<float*>(T2)[e2] = static_cast<float>(v);
+            }
+            if (iterations == 0 && !final_pass && warp >= nwarps - 2) {
+                // no window weight exceeds the sum of the column maxima: the reference point of iteration 0
+                const int b = warp - (nwarps - 2);
+                const double* L = L64 + b * TH;
+                const int c = lane + 1;
+                double m = 0.0;
+                if (lane < l) m = fmax(fmax(L[c * 4] - L[0], L[c * 4 + 1] - L[1]), fmax(L[c * 4 + 2] - L[2], L[c * 4 + 3] - L[3]));
+                m = warp_sum_d(m);
+                if (lane == 0) ubs[b] = static_cast<float>(m);
+            }
+            #pragma unroll 1
+            for (int e = threadIdx.x; e < 32 * G; e += blockDim.x) Cq[e] = 0.f;
+            __syncthreads();
+            PM_PHASE(1);  // log tables
+
+            double ll0 = 0.0, ll1 = 0.0;
+            for (int tile_i = 0; tile_i < x.n_tiles; ++tile_i) {
+                const TileDesc tile = x.tiles[tile_i];
+                if (threadIdx.x < 17) s_off[threadIdx.x] = x.tile_group_off[tile_i * 17 + threadIdx.x];
+                if (threadIdx.x >= 32 && threadIdx.x <= 32 + nwarps) {  // class rows [wrow[w], wrow[w+1]) belong to warp w
+                    const int w = threadIdx.x - 32;
+                    wrow[w] = static_cast<int>(static_cast<long long>(x.tile_group_off[tile_i * 17 + 16]) * w / nwarps);
+                }
+                for (int k = threadIdx.x, k_end = smeta[4 * tile.seq_begin + 2]; k < k_end; k += blockDim.x)
+                    zbuf[k] = make_float2(0.f, 0.f);  // front pad (dummy lanes of the class rows read it)
+                // ================= E-step: warp per sequence of the tile =================
+                for (int i = tile.seq_begin + warp; i < tile.seq_end; i += nwarps) {
+                    const uint64_t* __restrict__ wp = wstage + smeta[4 * i];
+                    const int W = smeta[4 * i + 1];
+                    const int zo = smeta[4 * i + 2];
+                    const int chunks = (W + 31) >> 5;
+                    float2* zs = zbuf + zo;
+                    float* zb0 = zf + 2 * zo;
+                    float* zb1 = zb0 + 1;
+                    {
+                        // slots that are not window starts read as zero in the M-step gather
+                        const int z_end = (i + 1 < tile.seq_end ? smeta[4 * (i + 1) + 2] : tile.zlen) - zo;
+                        #pragma unroll 1
+                        for (int k = W + lane; k < z_end; k += 32) zs[k] = make_float2(0.f, 0.f);
+                    }
+                    SeqAcc a = {-INFINITY, 0.f, 0.f, 0, 0, 0, false}, b = {-INFINITY, 0.f, 0.f, 0, 0, 0, false};
+
+                    if (final_pass) {
+                        pair_pass_a<G, false>(T2, wp, W, lane, zs, 0.f, 0.f, 0.f, a, b);
+                        __syncwarp();
+                        // ---- positions: per-sequence argmax, ties to the smallest offset (refine.hpp:311-316).
+                        // Windows within delta of the FP32 maximum are compared by their FP64 weights.
+                        const float Mf0 = warp_max_f(a.best_w), Mf1 = warp_max_f(b.best_w);
+                        if (!(Mf0 > -INFINITY) || !(Mf0 < INFINITY)) iscal[2] = 1;
+                        if (!(Mf1 > -INFINITY) || !(Mf1 < INFINITY)) iscal[6] = 1;
+                        {
+                            const float lim0 = Mf0 - (1e-3f + 1e-5f * fabsf(Mf0)), lim1 = Mf1 - (1e-3f + 1e-5f * fabsf(Mf1));
+                            for (int c = 0; c < chunks; ++c) {
+                                const int j = (c << 5) + lane;
+                                bool k0 = false, k1 = false;
+                                if (j < W) {
+                                    const float2 w2 = zs[j];
+                                    k0 = w2.x >= lim0;
+                                    k1 = w2.y >= lim1;
+                                }
+                                near_push16(__ballot_sync(0xffffffffu, k0), k0, lane, j, near_a, a.nnear, a.overflow);
+                                near_push16(__ballot_sync(0xffffffffu, k1), k1, lane, j, near_b, b.nnear, b.overflow);
+                            }
+                        }
+                        __syncwarp();
+#pragma unroll 1
+                        for (int bb = 0; bb < 2; ++bb) {
+                            const SeqAcc s = bb ? b : a;
+                            const uint16_t* my_near = near_a + bb * kPairNearCap;
+                            int arg;
+                            if (!s.overflow) {
+                                const double* D = D64 + bb * TH;
+                                double bw = -INFINITY;
+                                int bj = 0x7fffffff;
+                                for (int e = lane; e < s.nnear; e += 32) {
+                                    const int j = my_near[e];
+                                    const double w = window_weight_rolled(D, load_window(wp, j), l);
+                                    if (w > bw || (w == bw && j < bj)) {
+                                        bw = w;
+                                        bj = j;
+                                    }
+                                }
+#pragma unroll
+                                for (int o = 16; o > 0; o >>= 1) {
+                                    const double ow = __shfl_xor_sync(0xffffffffu, bw, o);
+                                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                                    if (ow > bw || (ow == bw && oj < bj)) {
+                                        bw = ow;
+                                        bj = oj;
+                                    }
+                                }
+                                arg = bj;
+                            } else {
+                                float bw = s.best_w;
+                                int bj = s.best_j;
+#pragma unroll
+                                for (int o = 16; o > 0; o >>= 1) {
+                                    const float ow = __shfl_xor_sync(0xffffffffu, bw, o);
+                                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                                    if (ow > bw || (ow == bw && oj < bj)) {
+                                        bw = ow;
+                                        bj = oj;
+                                    }
+                                }
+                                arg = bj;
+                            }
+                            if (p.out_pos && lane == 0 && (bb == 0 || live1)) p.out_pos[static_cast<int64_t>(wis[bb]) * t + i] = arg + 1;
+                            if (lane < l) {
+                                const uint64_t v = load_window(wp, arg);
+                                atomicAdd(&prof[bb * 128 + lane * 4 + (static_cast<unsigned>(v >> colshift) & 3u)], 1);
+                            }
+                            __syncwarp();
+                        }
+                        continue;
+                    }
+
+                    // pass A with the exp fused in, taken relative to the previous iteration's maximum of this
+                    // sequence (iteration 0: the upper bound); softmax is shift-invariant
+                    constexpr float kNearMargin = 4.f;
+                    const bool first = iterations == 0;
+                    float ref0 = first ? ubs[0] : mprev[i];
+                    float ref1 = first ? ubs[1] : mprev[tpad + i];
+                    // iteration 0 lists nothing on the way (its reference is far above the maximum): rebuilt below
+                    const float near_thr = first ? INFINITY : fast_ex2((p.log_z_eps - kNearMargin) * kLog2e);
+                    pair_pass_a<G, true>(T2, wp, W, lane, zs, ref0, ref1, near_thr, a, b);
+                    float M0 = 0.f, M1 = 0.f, inv0 = 0.f, inv1 = 0.f;
+                    // the FP64 pass is skipped in the last iteration of the budget: its likelihood can no longer
+                    // stop the loop (refine.hpp:296-304), so no near list is needed there
+                    const bool want_near = iterations + 1 < p.max_iters;
+#pragma unroll 1
+                    for (int bb = 0; bb < 2; ++bb) {  // rolled: one copy of the code for both buckets
+                        SeqAcc s = bb ? b : a;
+                        float ref = bb ? ref1 : ref0, M, ne;
+                        const float inv = pair_settle<G>(T2f + bb, wp, W, lane, zb0 + bb, near_a + bb * kPairNearCap, s, ref, M,
+                                                         ne, p.log_z_eps, first, want_near, &iscal[bb * 4 + 2]);
+                        if (lane == 0) mprev[bb * tpad + i] = M;
+                        if (bb) {
+                            b = s, ref1 = ref, M1 = M, inv1 = inv;
+                        } else {
+                            a = s, ref0 = ref, M0 = M, inv0 = inv;
+                        }
+                    }
+                    __syncwarp();
+                    // pass C: z_j = e_j / sum, both buckets
+                    {
+                        int j = lane;
+                        for (const int j4 = W - 96; j < j4; j += 128) {  // four chunks per trip: loads first, then stores
+                            float2 e0 = zs[j], e1 = zs[j + 32], e2 = zs[j + 64], e3 = zs[j + 96];
+                            e0.x *= inv0, e0.y *= inv1, e1.x *= inv0, e1.y *= inv1;
+                            e2.x *= inv0, e2.y *= inv1, e3.x *= inv0, e3.y *= inv1;
+                            zs[j] = e0, zs[j + 32] = e1, zs[j + 64] = e2, zs[j + 96] = e3;
+                        }
+                        for (; j < W; j += 32) {
+                            float2 e = zs[j];
+                            e.x *= inv0;
+                            e.y *= inv1;
+                            zs[j] = e;
+                        }
+                    }
+                    __syncwarp();
+                    // ---- log sum_j exp(w_j) per bucket
+#pragma unroll 1
+                    for (int bb = 0; bb < 2; ++bb) {
+                        const SeqAcc s = bb ? b : a;
+                        float* zb = zb0 + bb;
+                        const uint16_t* my_near = near_a + bb * kPairNearCap;
+                        // the list holds exactly the windows with e >= near_e (lane L owns entries L and L + 32)
+                        const bool n_a = !s.overflow && lane < s.nnear, n_b = !s.overflow && lane + 32 < s.nnear;
+                        const float ref = bb ? ref1 : ref0, M = bb ? M1 : M0, inv = bb ? inv1 : inv0;
+                        double lse;
+                        if (!s.overflow) {
+                            // FP64 re-evaluation of the dominant windows; the far tail (each < eps of the maximum)
+                            // keeps its FP32 sum, rescaled from ref to M
+                            const double* D = D64 + bb * TH;
+                            const double far = static_cast<double>(warp_sum_f(s.s_far) * fast_ex2((ref - M) * kLog2e));
+                            double wa = -INFINITY, wb = -INFINITY;
+                            if (n_a) wa = window_weight_rolled(D, load_window(wp, my_near[lane]), l);
+                            if (__any_sync(0xffffffffu, n_b)) {
+                                if (n_b) wb = window_weight_rolled(D, load_window(wp, my_near[lane + 32]), l);
+                            }
+                            const double m64 = warp_max_d(fmax(wa, wb));
+                            wa = n_a ? exp_f64(wa - m64) : 0.0;
+                            if (__any_sync(0xffffffffu, n_b)) wb = n_b ? exp_f64(wb - m64) : 0.0; else wb = 0.0;
+                            // far * exp(M - m64): |M - m64| ~ 1e-5 and far < W*eps, so first order is exact to ~1e-17
+                            const double s64 = warp_sum_d(wa + wb) + far * (1.0 + (static_cast<double>(M) - m64));
+                            lse = m64 + log_f64(s64);
+                            if (n_a) zb[2 * my_near[lane]] = static_cast<float>(wa / s64);
+                            if (n_b) zb[2 * my_near[lane + 32]] = static_cast<float>(wb / s64);
+                        } else {
+                            lse = static_cast<double>(ref) - static_cast<double>(logf(inv));  // total is relative to ref
+                        }
+                        // log P(S_i) = log prod theta_bg - log W + logsumexp_j w_ij (refine.hpp:200); the first two
+                        // terms are summed over the set by the thread that closes the iteration
+                        if (bb) ll1 += lse; else ll0 += lse;
+                    }
+                    __syncwarp();
+                }
+                if (final_pass) {
+                    if (tile_i + 1 < x.n_tiles) __syncthreads();  // the next tile reuses the z buffer
+                    continue;
+                }
+                __syncthreads();
+                PM_PHASE(2);  // E-step (warp 0's sequences + wait for the slowest warp)
+
+                // ================= M-step of the tile: conflict-free class gather, both buckets =================
+                {
+                    const int item_lo = wrow[warp], item_hi = wrow[warp + 1];
+                    const uint16_t* __restrict__ rows = x.cls_entries + static_cast<size_t>(tile.group_base) * 32 + lane;
+                    for (int q = 0; q < 16; ++q) {
+                        const int ra = max(item_lo, s_off[q]), rb = min(item_hi, s_off[q + 1]);
+                        if (ra >= rb) continue;  // this warp owns no row of class q
+                        float acc[NV];
+#pragma unroll
+                        for (int g = 0; g < NV; ++g) acc[g] = 0.f;
+                        // rows are padded at the end of the table: the two-ahead prefetch may run past rb
+                        const uint16_t* __restrict__ ent = rows + static_cast<size_t>(ra) * 32;
+                        int pos = ent[0], pos1 = ent[32];
+                        for (int it = ra; it < rb; ++it) {
+                            ent += 32;
+                            const int pos2 = ent[32];
+                            const float2* zp = zbuf + pos;
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                const float2 v = zp[-2 * g];
+                                acc[g] += v.x;
+                                acc[G + g] += v.y;
+                            }
+                            pos = pos1;
+                            pos1 = pos2;
+                        }
+                        const float sum = warp_transpose_sum<NV>(acc, lane);
+                        // lane L holds value (L*NV)>>5: value index v -> bucket v / G, pair v % G
+                        if (NV == 32 || (lane & 1) == 0) cpart[(warp + q) * NV + ((lane * NV) >> 5)] = sum;
+                    }
+                }
+                __syncthreads();
+                PM_PHASE(3);  // M-step gather (+ wait)
+                // class sums of the tile, per-warp partials added in warp order (deterministic)
+                {
+                    #pragma unroll 1
+                    for (int e = threadIdx.x; e < 32 * G; e += blockDim.x) {
+                        const int b = e / (16 * G), rem = e - b * 16 * G;
+                        const int q = rem / G, g = rem - q * G;
+                        float sum = 0.f;
+                        #pragma unroll 1
+                        for (int w = 0; w < nwarps; ++w) {
+                            if (max(wrow[w], s_off[q]) < min(wrow[w + 1], s_off[q + 1])) sum += cpart[(w + q) * NV + b * G + g];
+                        }
+                        Cq[e] += sum;
+                    }
+                }
+                if (tile_i + 1 < x.n_tiles) __syncthreads();  // z buffer, s_off and cpart are reused by the next tile
+            }  // tiles
+            if (final_pass) break;
+            if (lane == 0) {
+                llpart[warp * 2 + 0] = ll0;
+                llpart[warp * 2 + 1] = ll1;
+            }
+            __syncthreads();
+            // marginalise to motif counts, then write_column (refine.hpp:241-269) in FP64.
+            // Thread e = 4c + r owns theta cell (column c, symbol r); c == l is the background column.
+            // The four lanes of a column exchange their values with shuffles.  A frozen bucket keeps its theta.
+            ++iterations;
+            const int nw_m = (4 * l + 31) >> 5;  // warps covering the 4l motif cells of one bucket
+            if (nwarps >= 2 * nw_m + 2) {
+                // both buckets at once: warps [bb*nw_m, (bb+1)*nw_m) own bucket bb's motif cells, warp 2*nw_m + bb
+                // its background column (all 32 lanes share the l column sums, then lanes 0..3 normalise)
+                const bool bg_warp = warp >= 2 * nw_m && warp < 2 * nw_m + 2;
+                const int bb = bg_warp ? warp - 2 * nw_m : (warp < nw_m ? 0 : 1);
+                if (warp < 2 * nw_m + 2 && !(bb ? stop1 : stop0)) {
+                    const float* C = Cq + bb * 16 * G;
+                    const int e = bg_warp ? lane : static_cast<int>(threadIdx.x) - bb * nw_m * 32;
+                    const int r = e & 3;
+                    bool live;
+                    int cell;
+                    double raw;
+                    if (!bg_warp) {
+                        live = e < 4 * l;
+                        const int c = live ? e >> 2 : 0, g = c >> 1;
+                        cell = (c + 1) * 4 + r;
+                        raw = 0.0;
+                        for (int o = 0; o < 4; ++o) raw += static_cast<double>(C[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                    } else {
+                        // background = symbol totals - expected motif counts, clamped at 0
+                        live = lane < 4;
+                        cell = r;
+                        double cnt = 0.0;
+                        #pragma unroll 1
+                        for (int cc = lane >> 2; cc < l; cc += 8) {
+                            const int g = cc >> 1;
+                            for (int o = 0; o < 4; ++o) cnt += static_cast<double>(C[((cc & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                        }
+                        cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
+                        cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
+                        cnt += __shfl_xor_sync(0xffffffffu, cnt, 16);
+                        raw = fmax(p.tot_sym[r] - cnt, 0.0);
+                    }
+                    double sum = raw + __shfl_xor_sync(0xffffffffu, raw, 1);
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                    const double v = sum > 0.0 ? fmax(raw / sum, 1e-9) : 0.25;
+                    double fs = v + __shfl_xor_sync(0xffffffffu, v, 1);
+                    fs += __shfl_xor_sync(0xffffffffu, fs, 2);
+                    if (live) {
+                        const double tv = v / fs;
+                        thd[bb * TH + cell] = tv;
+                        L64[bb * TH + cell] = log_f64(fmax(tv, 1e-9));
+                    }
+                }
+            } else {
+            for (int bb = 0; bb < 2; ++bb) {
+                if (bb ? stop1 : stop0) continue;
+                if (warp < (TH + 31) / 32) {
+                    const float* C = Cq + bb * 16 * G;
+                    const int e = threadIdx.x;
+                    const bool live = e < TH;
+                    const int c = live ? e >> 2 : 0, r = e & 3;
+                    double raw;
+                    if (c < l) {
+                        const int g = c >> 1;
+                        raw = 0.0;
+                        for (int o = 0; o < 4; ++o) raw += static_cast<double>(C[((c & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                    } else {
+                        // background = symbol totals - expected motif counts, clamped at 0
+                        double bg = p.tot_sym[r];
+                        #pragma unroll 1
+                        for (int cc = 0; cc < l; ++cc) {
+                            const int g = cc >> 1;
+                            double cnt = 0.0;
+                            for (int o = 0; o < 4; ++o) cnt += static_cast<double>(C[((cc & 1) ? (4 * o + r) : (4 * r + o)) * G + g]);
+                            bg -= cnt;
+                        }
+                        raw = fmax(bg, 0.0);
+                    }
+                    double sum = raw + __shfl_xor_sync(0xffffffffu, raw, 1);
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                    const double v = sum > 0.0 ? fmax(raw / sum, 1e-9) : 0.25;
+                    double fs = v + __shfl_xor_sync(0xffffffffu, v, 1);
+                    fs += __shfl_xor_sync(0xffffffffu, fs, 2);
+                    if (live) {
+                        const double tv = v / fs;
+                        thd[bb * TH + (c < l ? c + 1 : 0) * 4 + r] = tv;
+                        L64[bb * TH + (c < l ? c + 1 : 0) * 4 + r] = log_f64(fmax(tv, 1e-9));
+                    }
+                }
+            }
+            }
+            if (threadIdx.x >= blockDim.x - 2) {
+                const int bb = threadIdx.x - (blockDim.x - 2);
+                if (!(bb ? stop1 : stop0)) {
+                    // sum_i (log prod theta_bg - log W_i) + sum_i logsumexp_i
+                    double ll = 0.0;
+                    for (int r = 0; r < 4; ++r) ll += p.tot_sym[r] * dscal[bb * 6 + 2 + r];
+                    ll -= sum_logw;
+                    for (int w = 0; w < nwarps; ++w) ll += llpart[w * 2 + bb];
+                    if (p.out_ll && (bb == 0 || live1)) p.out_ll[static_cast<int64_t>(wis[bb]) * p.max_iters + (iterations - 1)] = ll;
+                    iscal[bb * 4 + 0] = (iterations >= 2 && ll - dscal[bb * 6] < p.tol) ? 1 : 0;  // refine.hpp:296-304
+                    iscal[bb * 4 + 3] = iterations;
+                    dscal[bb * 6] = ll;
+                }
+            }
+            __syncthreads();
+            PM_PHASE(4);  // class-sum reduce, theta update, LL
+            stop0 = iscal[0] != 0;
+            stop1 = iscal[4] != 0;
+            final_pass = iterations >= p.max_iters || (stop0 && stop1);
+        }
+
+        // ---- score / consensus over the argmax rows (scoring.hpp:84-126), expectation (refine.hpp:130-136)
+        __syncthreads();
+        PM_PHASE(5);  // final E-step sweep (positions)
+        if (threadIdx.x < 64 && (threadIdx.x & 31) < l) {
+            const int bb = threadIdx.x >> 5, c = threadIdx.x & 31;
+            const int* pc = prof + bb * 128 + c * 4;
+            int best = 0;
+            for (int r = 1; r < 4; ++r) {
+                if (pc[r] > pc[best]) best = r;
+            }
+            atomicAdd(&iscal[bb * 4 + 1], pc[best]);
+            atomicOr(&cons_bits[bb], static_cast<unsigned long long>(best) << (62 - 2 * c));
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 && (threadIdx.x == 0 || live1)) {
+            const int bb = threadIdx.x;
+            const unsigned int wi = wis[bb];
+            double ex = 0.0;
+            #pragma unroll 1
+            for (int c = 1; c <= l; ++c) {
+                const double* tc = thd + bb * TH + c * 4;
+                ex += fmax(fmax(tc[0], tc[1]), fmax(tc[2], tc[3]));
+            }
+            p.out_score[wi] = iscal[bb * 4 + 1];
+            p.out_iters[wi] = iscal[bb * 4 + 3];
+            p.out_exp[wi] = ex;
+            p.out_cons[wi] = cons_bits[bb];
+            atomicAdd(p.iter_total, static_cast<unsigned long long>(iscal[bb * 4 + 3] + 1));
+            if (iscal[bb * 4 + 2]) atomicExch(p.error_flag, 1u);
+        }
+        if (p.out_theta) {
+            #pragma unroll 1
+            for (int e2 = threadIdx.x; e2 < 2 * TH; e2 += blockDim.x) {
+                const int bb = e2 >= TH, e = e2 - bb * TH;
+                if (bb && !live1) continue;
+                const int c = e >> 2, r = e & 3;
+                p.out_theta[static_cast<int64_t>(wis[bb]) * 4 * (l + 1) + r * (l + 1) + c] = thd[e2];
+            }
+        }
+        PM_PHASE(6);  // score, consensus, outputs
+    }
+}
+
+}  // namespace k
+}  // namespace pm
