@@ -347,16 +347,18 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "stage_ms_per_step": {name: stage[i] / args.steps for i, name in
                               enumerate(["keys", "sort", "enrich", "em", "reduce", "score", "upload", "d2h"])},
-        "roofline": {"bound": "fp32", "kernel": "em_refine_smem_kernel", "achieved": achieved_tflops, "peak": fp32_peak_tflops,
+        "roofline": {"bound": "fp32", "kernel": "em_refine_pair_kernel" if t <= 64 else "em_refine_smem_kernel",
+                     "achieved": achieved_tflops, "peak": fp32_peak_tflops,
                      "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
                      # dram__bytes_read+write of one launch from the ncu --set full capture in profiles/ (C1 only):
                      # the kernel's working set is shared memory + L1/L2-resident tables
-                     "traffic": 2730496 if args.config == "c1" and not args.trials else None,
-                     "traffic_source": "profiles/r1_em_refine_smem_ncu_full_v2.txt (ncu, bytes per launch)",
+                     "traffic": 2788864 if args.config == "c1" and not args.trials else None,
+                     "traffic_source": "profiles/r1_em_refine_pair_ncu_full.txt (ncu, dram bytes per launch)",
                      "launch_ms": em_ms / max(1, em_launches // args.steps),
                      "work": "SURVEY 8(d) W_EM = sum_b (2 I_b+1) x l + 4 (I_b+1) x FP32 ops (E- and M-step), measured I_b",
                      "estep_only_achieved": estep_tflops,
                      "smem_lookup_ceiling": 148 * 32 * sm_max_mhz * 1e6 * 2 / 1e12,
+                     "frac_of_smem_ceiling": (achieved_tflops / (148 * 32 * sm_max_mhz * 1e6 * 2 / 1e12)) if achieved_tflops else None,
                      "peak_source": f"148 SM x 128 FP32 lanes x {sm_max_mhz:.0f} MHz ({peak_kind} clocks), adds not FMAs"},
         "roofline_hash_bucket": {"bound": "hbm", "kernels": "project_keys+radix_sort+enrich",
                                  "achieved": (hb_bytes / (hb_ms * 1e-3) / 1e9) if hb_ms > 0 else None, "peak": hbm_peak,

@@ -1,0 +1,78 @@
+"""The two-buckets-per-CTA EM kernel (csrc/pm_em_pair.cuh): buckets of a pair run in lockstep, so the
+cases that matter are the ones where the two differ -- one converges early and is frozen while the other
+keeps iterating, an odd tail, a different partner -- and agreement with the one-bucket kernel."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import EXPECTATION_TOL, THETA_TOL
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(a, w):
+    assert a["iterations"] == w.iterations
+    assert a["positions"] == w.positions
+    assert (a["consensus"], a["score"]) == (w.consensus, w.score)
+    assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+    assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL
+
+
+def test_pairs_with_different_iteration_counts(ctx, best_oracle, instance):
+    """refine.hpp:296-304 stops each bucket on its own likelihood gain; with max_iters = 12 the enriched
+    buckets of this easy instance stop after 3..12 iterations, so most pairs hold a frozen bucket."""
+    t, n, l, d, seed = 10, 80, 7, 0, 11
+    ss, _, _ = instance(t, n, l, d, seed)
+    kept = best_oracle.sample_plan(l, 5, 1)
+    en = best_oracle.enriched(ss, l, kept, 2, t * 2)[:41]  # odd count: the last CTA refines a lone bucket
+    want = [best_oracle.refine(ss, l, e["members"], e["key"], max_iters=12) for e in en]
+    its = [w.iterations for w in want]
+    assert len(set(its)) >= 4 and any(its[i] != its[i + 1] for i in range(0, 40, 2)), its
+    ctx.set_sequences(ss.bases, ss.offs)
+    got = ctx.refine(l, [e["members"] for e in en], max_iters=12)
+    for a, w in zip(got, want):
+        _check(a, w)
+        np.testing.assert_allclose(a["ll_trace"][: w.iterations], w.ll_trace, atol=5e-2, rtol=0)
+
+
+def test_result_does_not_depend_on_the_partner(ctx, best_oracle, instance):
+    """A bucket's outputs are a function of the bucket alone: any pairing gives bit-identical results."""
+    ss, _, _ = instance(12, 120, 8, 0, 5)
+    kept = best_oracle.sample_plan(8, 5, 1)
+    en = best_oracle.enriched(ss, 8, kept, 2, 24)[:9]
+    ctx.set_sequences(ss.bases, ss.offs)
+    members = [e["members"] for e in en]
+    base = ctx.refine(8, members)
+    order = [4, 0, 8, 2, 6, 1, 7, 3, 5]
+    shuffled = ctx.refine(8, [members[i] for i in order])
+    alone = [ctx.refine(8, [m])[0] for m in members[:3]]
+    for pos, i in enumerate(order):
+        a, b = base[i], shuffled[pos]
+        assert (a["consensus"], a["score"], a["positions"], a["iterations"]) == \
+               (b["consensus"], b["score"], b["positions"], b["iterations"])
+        assert a["expectation"] == b["expectation"] and (a["theta"] == b["theta"]).all()
+    for a, b in zip(base, alone):
+        assert a["expectation"] == b["expectation"] and (a["theta"] == b["theta"]).all()
+
+
+def test_pair_kernel_agrees_with_one_bucket_kernel(pm, golden, instance):
+    """PM_B200_EM_PAIR=0 selects the one-bucket kernel (pm_em_smem.cuh): same discrete outputs on the
+    challenge-scale goldens, thetas within FP32 noise of each other."""
+    g = [x for x in golden["refine"] if x["instance"][1] == 600][:7]
+    ss, _, _ = instance(*g[0]["instance"])
+    res = {}
+    for flag in ("1", "0"):
+        os.environ["PM_B200_EM_PAIR"] = flag
+        try:
+            with pm.Context(0) as c:
+                c.set_sequences(ss.bases, ss.offs)
+                res[flag] = c.refine(15, [x["members"] for x in g])
+        finally:
+            os.environ.pop("PM_B200_EM_PAIR", None)
+    for a, b, x in zip(res["1"], res["0"], g):
+        assert (a["consensus"], a["score"], a["positions"], a["iterations"]) == \
+               (b["consensus"], b["score"], b["positions"], b["iterations"]) == \
+               (x["consensus"], x["score"], x["positions"], x["iterations"])
+        assert np.abs(a["theta"] - b["theta"]).max() < 1e-5
+        assert abs(a["expectation"] - x["expectation"]) <= EXPECTATION_TOL
