@@ -23,6 +23,7 @@
 #include "pm_kernels.cuh"
 #include "pm_em_smem.cuh"
 #include "pm_em_pair.cuh"
+#include "pm_hash_fused.cuh"
 
 using namespace pm;
 
@@ -328,6 +329,28 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     c->total_groups = static_cast<int>(live_rows);
     c->group_fill = live_rows == 0 ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(live_rows * 32);
     return PM_OK;
+}
+
+// PM_B200_HOST_TIMING=1: wall-clock marks of the host side of pm_run on stderr (where the GPU may sit idle)
+struct HostMarks {
+    bool on = std::getenv("PM_B200_HOST_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    std::string line;
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        std::snprintf(buf, sizeof(buf), " %s %.0fus", what, std::chrono::duration<double, std::micro>(now - t0).count());
+        line += buf;
+        t0 = now;
+    }
+    ~HostMarks() {
+        if (on && !line.empty()) std::fprintf(stderr, "[pm host]%s\n", line.c_str());
+    }
+};
+thread_local HostMarks* g_marks = nullptr;
+void host_mark(const char* what) {
+    if (g_marks) g_marks->mark(what);
 }
 
 int need_sequences(const pm_ctx* c) {
@@ -1319,6 +1342,63 @@ struct RunState {
     std::vector<int32_t> positions;
 };
 
+// must mirror the carve-up at the top of hash_bucket_fused_kernel
+size_t fused_hash_smem_bytes(int n_words, int keybits, int64_t cap_e, int t, int64_t x) {
+    const size_t n_keys = static_cast<size_t>(1) << keybits;
+    size_t b = static_cast<size_t>(n_words) * 8 + n_keys * 2 + std::max<size_t>(n_keys / 32, 1) * 4;
+    b += static_cast<size_t>(cap_e) * 4 + (2 * static_cast<size_t>(t) + 1) * 4 + (2 * (k::kFusedThreads / 32) + 2) * 4;
+    b += static_cast<size_t>(x) * 2 + 8 + 8;
+    return b + 16;
+}
+
+bool fused_hash_applies(const pm_ctx* c, int keybits, int64_t cap_e) {
+    const char* env = std::getenv("PM_B200_FUSED_HASH");  // test/tuning knob: 0 selects the radix-sort path
+    if (env != nullptr && std::atoi(env) == 0) return false;
+    return keybits <= 16 && c->x < 65536 && c->total_words <= k::kPairMaxWords &&
+           fused_hash_smem_bytes(static_cast<int>(c->total_words), keybits, cap_e, c->t, c->x) <= 200 * 1024;
+}
+
+// hash_trial + enriched_buckets of every trial of the batch, one CTA per trial (pm_hash_fused.cuh)
+int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keybits, int thr, unsigned int* members,
+                      Records* r) {
+    r->cap_e = std::max<int64_t>(1, c->x / thr);
+    const int n = static_cast<int>(progs.size());
+    const size_t nrec = static_cast<size_t>(n) * static_cast<size_t>(r->cap_e);
+    PM_TRY(get_buf(c, S_REC_KEY, nrec, &r->key));
+    PM_TRY(get_buf(c, S_REC_START, nrec, &r->start));
+    PM_TRY(get_buf(c, S_REC_SIZE, nrec, &r->size));
+    PM_TRY(get_buf(c, S_NREC, static_cast<size_t>(n) + 1, &r->n_rec));
+    const size_t smem = fused_hash_smem_bytes(static_cast<int>(c->total_words), keybits, r->cap_e, c->t, c->x);
+    PM_CUDA(cudaFuncSetAttribute(k::hash_bucket_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k::FusedHashParams p;
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.win_off = c->d_win_off;
+    p.t = c->t;
+    p.keybits = keybits;
+    p.x = static_cast<int>(c->x);
+    p.n_words = static_cast<int>(c->total_words);
+    p.thr = thr;
+    p.cap_e = static_cast<int>(r->cap_e);
+    p.members = members;
+    p.rec_key = r->key;
+    p.rec_start = r->start;
+    p.rec_size = r->size;
+    p.n_rec = r->n_rec;
+    for (int base = 0; base < n; base += k::kMaxConstPlans) {
+        const int cnt = std::min(k::kMaxConstPlans, n - base);
+        c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
+        PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
+                                        0, cudaMemcpyHostToDevice, c->stream));
+        p.plan_base = base;
+        p.n_trials = cnt;
+        const unsigned grid = static_cast<unsigned>(std::min(cnt, 2 * c->sm_count));
+        k::hash_bucket_fused_kernel<<<grid, k::kFusedThreads, smem, c->stream>>>(p);
+        PM_TRY(check_launch(c, "hash_bucket_fused"));
+    }
+    return PM_OK;
+}
+
 template <typename KeyT>
 int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
               int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
@@ -1329,7 +1409,12 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     const int r_cap = c->t * params.s;
     Sorted<KeyT> srt;
     Records rec;
-    {
+    const bool fused = fused_hash_applies(c, 2 * params.k, std::max<int64_t>(1, c->x / params.s));
+    if (fused) {
+        StageTimer tk(c, prof, 0);
+        PM_TRY(get_buf(c, S_IDX_A, progs.size() * static_cast<size_t>(c->x), &srt.idx));
+        PM_TRY(fused_hash_bucket(c, progs, 2 * params.k, params.s, srt.idx, &rec));
+    } else {
         StageTimer tk(c, prof, 0);
         const size_t n = progs.size() * static_cast<size_t>(c->x);
         KeyT *ka, *kb;
@@ -1347,7 +1432,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     k::WorkDesc* work;
     {
         StageTimer te(c, prof, 2);
-        PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
+        if (!fused) PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
         PM_TRY(get_buf(c, S_WORK_OFF, static_cast<size_t>(n_trials) + 1, &work_off));
         PM_TRY(get_buf(c, S_WORK, static_cast<size_t>(n_trials) * static_cast<size_t>(rec.cap_e), &work));
         k::work_scan_kernel<<<1, 1024, 0, c->stream>>>(rec.n_rec, n_trials, work_off);
@@ -1379,6 +1464,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work, work_off + n_trials, 0,
                          static_cast<unsigned int>(std::min<size_t>(nb, 1u << 30)), srt.idx, o, d_scal));
     }
+    host_mark("launched");
     std::vector<TrialSummary> tb(static_cast<size_t>(n_trials));
     std::vector<unsigned int> n_rec(static_cast<size_t>(n_trials));
     unsigned long long scal[16] = {0};
@@ -1400,6 +1486,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         td.stop();
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
+    host_mark("gpu-wait");
     collect_stage_times(c, out->stage_ms);
 #ifdef PM_EM_TIMING
     {
@@ -1518,6 +1605,10 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
 
     RunState st;
     bool stop = false;
+    HostMarks marks;
+    g_marks = &marks;
+    struct MarksGuard { ~MarksGuard() { g_marks = nullptr; } } marks_guard;
+    host_mark("setup");
     for (int64_t first = tb; first <= te && !stop; first += batch) {
         const int64_t last = std::min(te, first + batch - 1);
         // Plans come from the reference's PRNG stream (one mt19937_64 per trial, driver.hpp:164):
@@ -1543,7 +1634,8 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
             }
         };
         const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-        const int n_threads = static_cast<int>(std::min<int64_t>(std::min(8, hw), (n_plans + 31) / 32));
+        // ~0.3 us per plan (LazyMt64): threads only pay off for thousands of plans
+        const int n_threads = static_cast<int>(std::min<int64_t>(std::min(8, hw), (n_plans + 1023) / 1024));
         if (n_threads <= 1 || cfg->forced_kept != nullptr) {
             make_range(0, n_plans);
         } else {
@@ -1558,6 +1650,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         for (int rc_plan : plan_rc) {
             if (rc_plan != PM_OK) return set_error(rc_plan, "invalid projection plan for a trial");
         }
+        host_mark("plans");
         const int rc = key_bytes == 4
                            ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
                                                  trial_best_expectation, trial_best_key, first - tb)
@@ -1575,6 +1668,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         return set_error(PM_ERR_NO_ENRICHED_BUCKETS, "no bucket reached s=" + std::to_string(params.s) + " in " +
                                                          std::to_string(out->trials_run) + " trials; lower s or raise m");
     }
+    host_mark("reduce+positions");
     unpack_consensus(st.best.cons, cfg->l, out->consensus);
     out->score = st.best.score;
     out->iterations = st.best.iters;
@@ -1590,6 +1684,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         out->total_distance = tot;
         out->within_d = within;
     }
+    host_mark("hamming");
     collect_stage_times(c, out->stage_ms);
     out->gpu_launches = c->launches - launches0;
     out->h2d_bytes = c->h2d_bytes - h2d0;

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <random>
 #include <string>
 #include <vector>
@@ -50,8 +51,53 @@ int validate_plan(int l, const int32_t* kept, int k) {
 
 namespace {
 
+// std::mt19937_64 restricted to what a plan needs: the same output stream, produced on demand.  Seeding a
+// std::mt19937_64 fills 312 state words and its first output twists all of them (~1 us); a plan consumes
+// about l-k outputs, and output i < 156 only depends on seed-chain words i, i+1 and i+156.  The chain is
+// extended as far as needed and the words are twisted one at a time; past 156 outputs the standard engine
+// takes over (same seed, 156 outputs discarded).  Bit-exactness against std::mt19937_64 is pinned by
+// tests/test_host_abi.py.
+class LazyMt64 {
+public:
+    explicit LazyMt64(uint64_t seed) : seed_(seed) { x_[0] = seed; }
+    uint64_t operator()() {
+        if (next_ >= kM) {
+            if (!full_) {
+                full_.reset(new std::mt19937_64(seed_));
+                full_->discard(kM);
+            }
+            return (*full_)();
+        }
+        const int i = next_++;
+        extend(i + kM);
+        const uint64_t y = (x_[i] & kUpper) | (x_[i + 1] & kLower);
+        uint64_t z = x_[i + kM] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        z ^= (z >> 29) & 0x5555555555555555ULL;
+        z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+        z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+        z ^= z >> 43;
+        return z;
+    }
+
+private:
+    static constexpr int kN = 312, kM = 156;
+    static constexpr uint64_t kUpper = ~0ULL << 31, kLower = (1ULL << 31) - 1ULL;
+    void extend(int upto) {  // seed chain x[i] = f * (x[i-1] ^ (x[i-1] >> 62)) + i
+        for (; filled_ < upto; ++filled_) {
+            const uint64_t prev = x_[filled_];
+            x_[filled_ + 1] = 6364136223846793005ULL * (prev ^ (prev >> 62)) + static_cast<uint64_t>(filled_ + 1);
+        }
+    }
+    uint64_t seed_;
+    uint64_t x_[kN];
+    int filled_ = 0;  // x_[0..filled_] are valid
+    int next_ = 0;
+    std::unique_ptr<std::mt19937_64> full_;
+};
+
 // Unbiased draw below n by rejecting the low tail 2^64 mod n (rng.hpp:37-50).
-uint64_t draw_below(std::mt19937_64& eng, uint64_t n) {
+template <typename Engine>
+uint64_t draw_below(Engine& eng, uint64_t n) {
     if (n == 1) return 0;
     const uint64_t low_tail = (0 - n) % n;
     uint64_t x = eng();
@@ -61,23 +107,36 @@ uint64_t draw_below(std::mt19937_64& eng, uint64_t n) {
 
 // sample_plan (projection.hpp:210-226): draw l-k distinct excluded positions by a partial
 // Fisher-Yates over 1..l (rng.hpp:62-73); the plan is the sorted complement.
-int plan_from_engine(int l, int k, std::mt19937_64& eng, int32_t* kept) {
+template <typename Engine>
+int plan_from_engine(int l, int k, Engine& eng, int32_t* kept) {
     if (k < 1 || k > l) {
         return set_error(PM_ERR_INVALID_PARAMS,
                          "plan needs 1 <= k <= l, got k=" + std::to_string(k) + ", l=" + std::to_string(l));
     }
-    std::vector<int> pool(static_cast<size_t>(l));
-    for (int i = 0; i < l; ++i) pool[static_cast<size_t>(i)] = i + 1;
+    constexpr int kStack = 64;  // no heap traffic for the motif lengths of this path
+    int pool_s[kStack];
+    char dropped_s[kStack + 1];
+    std::vector<int> pool_v;
+    std::vector<char> dropped_v;
+    int* pool = pool_s;
+    char* dropped = dropped_s;
+    if (l > kStack) {
+        pool_v.resize(static_cast<size_t>(l));
+        dropped_v.resize(static_cast<size_t>(l) + 1);
+        pool = pool_v.data();
+        dropped = dropped_v.data();
+    }
+    for (int i = 0; i < l; ++i) pool[i] = i + 1;
     const int drop = l - k;
     for (int i = 0; i < drop; ++i) {
         const int j = i + static_cast<int>(draw_below(eng, static_cast<uint64_t>(l - i)));
-        std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+        std::swap(pool[i], pool[j]);
     }
-    std::vector<char> dropped(static_cast<size_t>(l) + 1, 0);
-    for (int i = 0; i < drop; ++i) dropped[static_cast<size_t>(pool[static_cast<size_t>(i)])] = 1;
+    std::fill(dropped, dropped + l + 1, 0);
+    for (int i = 0; i < drop; ++i) dropped[pool[i]] = 1;
     int n = 0;
     for (int p = 1; p <= l; ++p) {
-        if (!dropped[static_cast<size_t>(p)]) kept[n++] = p;
+        if (!dropped[p]) kept[n++] = p;
     }
     return PM_OK;
 }
@@ -127,7 +186,7 @@ uint64_t pm_derive_seed(uint64_t master, uint64_t index) {
 
 int pm_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept) {
     clear_error();
-    std::mt19937_64 eng(rng_seed);
+    LazyMt64 eng(rng_seed);
     return plan_from_engine(l, k, eng, kept);
 }
 

@@ -60,6 +60,27 @@ def test_plan_stream_matches_reference(pm, golden, port):
         assert kept == port.sample_plan(l, k, seed)
         assert len(kept) == k and all(1 <= a < b <= l for a, b in zip(kept, kept[1:])) and 1 <= kept[0] <= l
     assert pm.sample_plan(9, 9, 3) == list(range(1, 10))  # identity plan, zero draws
+    # the library draws from an on-demand mt19937_64 (first 156 outputs straight from the seed chain, the
+    # standard engine beyond): same stream as the oracle's std::mt19937_64 on both sides of that boundary
+    def plan_from_stream(l, k, seed):  # rng.hpp:37-73 + projection.hpp:214-225 over the oracle's raw mt19937_64 outputs
+        stream = iter(int(v) for v in port.mt_outputs(seed, l + 64))
+        pool = list(range(1, l + 1))
+        for i in range(l - k):
+            n = l - i
+            low_tail = (2 ** 64 - n) % n
+            x = next(stream)
+            while x < low_tail:
+                x = next(stream)
+            j = i + (x % n if n > 1 else 0)
+            pool[i], pool[j] = pool[j], pool[i]
+        return sorted(set(range(1, l + 1)) - set(pool[: l - k]))
+
+    for seed, l, k in ((1, 31, 1), (2, 64, 3), (3, 150, 2), (4, 157, 1), (5, 158, 1), (6, 200, 10), (7, 400, 5),
+                       (2 ** 64 - 1, 160, 1), (0, 156, 1)):
+        assert pm.sample_plan(l, k, seed) == plan_from_stream(l, k, seed), (seed, l, k)
+    assert plan_from_stream(20, 7, 11) == port.sample_plan(20, 7, 11)
+    for trial in range(1, 400):
+        assert pm.trial_plan(15, 7, 7, trial) == port.trial_plan(15, 7, 7, trial)
     for bad in ((8, []), (8, [0, 1]), (8, [1, 9]), (8, [2, 2]), (8, [3, 2])):
         with pytest.raises(pm.PmError) as e:
             pm.validate_plan(*bad)
