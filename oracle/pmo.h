@@ -39,6 +39,7 @@ enum {
     PMO_ERR_NUMERICAL_UNDERFLOW = 8,   /* errors.hpp:91 */
     PMO_ERR_UNKNOWN_SYMBOL = 9,        /* errors.hpp:28 */
     PMO_ERR_INDEX_OUT_OF_RANGE = 10,   /* errors.hpp:40 */
+    PMO_ERR_SEARCH_SPACE_TOO_LARGE = 11, /* errors.hpp:65 */
     PMO_ERR_OTHER = 99
 };
 
@@ -135,6 +136,12 @@ int pmo_total_distance(const char* bases, const int64_t* offs, int t, const char
                        int32_t* per_seq_min /* t or NULL */);
 
 /* driver.hpp */
+/* exact solvers for small instances, oracle.hpp:45-98 and :120-149 (limits as in the reference: configurations / candidates) */
+int pmo_median_string(const char* bases, const int64_t* offs, int t, int l, uint64_t limit, char* median,
+                      int* total_distance);
+int pmo_naive_mfp(const char* bases, const int64_t* offs, int t, int l, uint64_t limit, int32_t* positions, int* score,
+                  char* consensus);
+
 int pmo_resolve_params(const pmo_run_config* cfg, const char* bases, const int64_t* offs, int t, pmo_run_result* params_out);
 int pmo_run(const pmo_run_config* cfg, const char* bases, const int64_t* offs, int t, pmo_run_result* out,
             int32_t* positions /* t */);

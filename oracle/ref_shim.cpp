@@ -47,6 +47,8 @@ int guarded(F&& f) {
         return fail(PMO_ERR_KMER_TOO_LONG, e);
     } catch (const DenseTableTooLargeError& e) {
         return fail(PMO_ERR_DENSE_TABLE_TOO_LARGE, e);
+    } catch (const SearchSpaceTooLargeError& e) {
+        return fail(PMO_ERR_SEARCH_SPACE_TOO_LARGE, e);
     } catch (const UnreachableError& e) {
         return fail(PMO_ERR_UNREACHABLE, e);
     } catch (const EmptyBucketError& e) {
@@ -411,6 +413,27 @@ int pmo_total_distance(const char* bases, const int64_t* offs, int t, const char
                 per_seq_min[i - 1] = best;
             }
         }
+    });
+}
+
+int pmo_median_string(const char* bases, const int64_t* offs, int t, int l, uint64_t limit, char* median,
+                      int* total_distance) {
+    return guarded([&] {
+        const SequenceSet seqs = make_set(bases, offs, t);
+        const MedianStringResult r = median_string(seqs, l, limit);
+        std::memcpy(median, r.median.c_str(), r.median.size() + 1);
+        *total_distance = r.total_distance;
+    });
+}
+
+int pmo_naive_mfp(const char* bases, const int64_t* offs, int t, int l, uint64_t limit, int32_t* positions, int* score,
+                  char* consensus) {
+    return guarded([&] {
+        const SequenceSet seqs = make_set(bases, offs, t);
+        const NaiveMfpResult r = naive_mfp(seqs, l, limit);
+        for (int i = 0; i < t; ++i) positions[i] = r.positions[static_cast<std::size_t>(i)];
+        *score = r.score;
+        std::memcpy(consensus, r.consensus.c_str(), r.consensus.size() + 1);
     });
 }
 

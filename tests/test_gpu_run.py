@@ -233,3 +233,39 @@ def test_degenerate_shapes_match_oracle(ctx, best_oracle):
         for f in fields:
             assert got[f] == want[f], (strings[0][:12], f, got[f], want[f])
         assert abs(got["expectation"] - want["expectation"]) <= EXPECTATION_TOL
+
+
+def test_fused_hash_path_equals_sort_path(pm, best_oracle, instance):
+    """run() buckets each trial with the one-CTA shared-memory histogram kernel (csrc/pm_hash_fused.cuh) when
+    the dense table fits; PM_B200_FUSED_HASH=0 forces the radix-sort path.  Per-trial outcomes must be
+    identical, on the challenge instance and on low-complexity sets whose buckets hold hundreds of members
+    (cooperative ordering) or whose key space is smaller than the CTA (k <= 4)."""
+    import os
+    rng = np.random.default_rng(21)
+    low = pmo.SeqSet.from_strings(["".join(rng.choice(list("AC"), 150, p=[0.9, 0.1])) for _ in range(6)])
+    ragged = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(40, 200)))) for _ in range(9)])
+    cases = [
+        (instance(20, 600, 15, 4, 42)[0], dict(l=15, d=4, k=7, s=4, m=6, seed=7, early_stop=0)),
+        (low, dict(l=9, d=2, k=6, s=3, m=4, seed=1, early_stop=0)),      # buckets of several hundred members
+        (low, dict(l=9, d=2, k=8, s=40, m=3, seed=2, early_stop=0)),     # 4^8 keys, high threshold, r_cap truncation
+        (ragged, dict(l=7, d=1, k=3, s=2, m=5, seed=3, early_stop=0)),   # 64 keys < 512 threads
+        (ragged, dict(l=6, d=1, k=1, s=1, m=3, seed=4, early_stop=0)),   # 4 keys
+    ]
+    for ss, kw in cases:
+        res = {}
+        for flag in ("1", "0"):
+            os.environ["PM_B200_FUSED_HASH"] = flag
+            try:
+                with pm.Context(0) as c:
+                    c.set_sequences(ss.bases, ss.offs)
+                    res[flag] = c.run(per_trial=True, **kw)
+            finally:
+                os.environ.pop("PM_B200_FUSED_HASH", None)
+        a, b = res["1"], res["0"]
+        assert a["gpu_launches"] < b["gpu_launches"]  # the fused path really ran
+        for f in INT_FIELDS + ("expectation",):
+            assert a[f] == b[f], (kw, f)
+        for f in ("trial_buckets", "trial_score", "trial_key", "trial_expectation"):
+            assert (a[f] == b[f]).all(), (kw, f)
+        want = best_oracle.run(ss, **kw)
+        assert (a["score"], a["buckets_enriched"], a["trials_run"]) == (want["score"], want["buckets_enriched"], want["trials_run"])
