@@ -41,6 +41,7 @@ typedef enum pm_status {
     PM_ERR_NUMERICAL_UNDERFLOW = 8,   /* errors.hpp:91 NumericalUnderflowError */
     PM_ERR_UNKNOWN_SYMBOL = 9,        /* errors.hpp:28 UnknownSymbolError */
     PM_ERR_INDEX_OUT_OF_RANGE = 10,   /* errors.hpp:40 IndexOutOfRangeError */
+    PM_ERR_SEARCH_SPACE_TOO_LARGE = 11, /* errors.hpp:65 SearchSpaceTooLargeError */
     PM_ERR_UNSUPPORTED = 50,          /* valid for the reference, outside this build's limits (e.g. l > 31) */
     PM_ERR_CUDA = 100,                /* a CUDA runtime call or kernel failed */
     PM_ERR_NO_DEVICE = 101,           /* no usable sm_100 device: there is no CPU fallback */
@@ -182,6 +183,11 @@ int pm_score(pm_ctx* ctx, int l, const int32_t* starts, int* score, char* consen
  * (sequence.hpp:28-38, oracle.hpp:101-115), their sum, and the number of sequences with min <= d. */
 int pm_hamming_scan(pm_ctx* ctx, const char* v, int l, int d, int32_t* per_seq_min /* t or NULL */,
                     int* total_distance, int* within_d);
+/* median_string, oracle.hpp:120-149: exhaustive search over the 4^l candidates (ascending code order, first
+ * minimiser of total_distance wins) with the XOR/popcount scan -- an exact check of a recovered motif for
+ * l <= 16. 4^l > limit -> PM_ERR_SEARCH_SPACE_TOO_LARGE (the reference's default limit is 16,777,216 = 4^12);
+ * l > 16 within the limit -> PM_ERR_UNSUPPORTED. median: l+1 bytes. */
+int pm_median_string(pm_ctx* ctx, int l, uint64_t limit, char* median, int* total_distance);
 
 /* --------------------------------------------------------------------------------------------
  * 4. The whole path: run(), driver.hpp:145-220

@@ -25,6 +25,7 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <chrono>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -48,6 +49,7 @@ struct IndexOutOfRangeError : ParamError { using ParamError::ParamError; };
 struct LengthMismatchError : ParamError { using ParamError::ParamError; };
 struct InvalidParamsError : ParamError { using ParamError::ParamError; };
 struct DenseTableTooLargeError : ParamError { using ParamError::ParamError; };
+struct SearchSpaceTooLargeError : ParamError { using ParamError::ParamError; };
 struct UnreachableError : ParamError { using ParamError::ParamError; };
 struct EmptyBucketError : ParamError { using ParamError::ParamError; };
 struct NoEnrichedBucketsError : Error { using Error::Error; };
@@ -69,6 +71,7 @@ inline void check(int rc) {
         case PM_ERR_NUMERICAL_UNDERFLOW: throw NumericalUnderflowError(msg);
         case PM_ERR_UNKNOWN_SYMBOL: throw UnknownSymbolError(msg);
         case PM_ERR_INDEX_OUT_OF_RANGE: throw IndexOutOfRangeError(msg);
+        case PM_ERR_SEARCH_SPACE_TOO_LARGE: throw SearchSpaceTooLargeError(msg);
         default: throw DeviceError(msg);
     }
 }
@@ -658,6 +661,144 @@ inline std::string truth_json(const PlantedInstance& inst) {
     o += "  \"seed\": " + std::to_string(inst.seed) + "\n";
     o += "}\n";
     return o;
+}
+
+// ---- oracle.hpp: exact solvers for small instances
+struct NaiveMfpResult {
+    StartVector positions;
+    int score = 0;
+    std::string consensus;
+};
+struct MedianStringResult {
+    std::string median;
+    int total_distance = 0;
+};
+
+/// median_string (oracle.hpp:120-149) on the device: all 4^l candidates, first minimiser of total_distance in
+/// ascending code order (XOR/popcount scan, one thread per candidate).
+inline MedianStringResult median_string(const SequenceSet& seqs, int l, std::uint64_t limit = 16777216ULL) {
+    MedianStringResult r;
+    std::string med(static_cast<std::size_t>(l > 0 ? l : 0) + 1, '\0');
+    detail::check(pm_median_string(Device::instance().bind(seqs), l, limit, med.data(), &r.total_distance));
+    med.resize(static_cast<std::size_t>(l));
+    r.median = med;
+    return r;
+}
+
+/// naive_mfp (oracle.hpp:45-98): every start vector in odometer order, first maximum of the profile score.
+/// Exponential ground truth for toy instances; plain host C++ (not part of the accelerated path), the
+/// incremental profile update of the reference restated on rank arrays.
+inline NaiveMfpResult naive_mfp(const SequenceSet& seqs, int l, std::uint64_t limit = 100000000ULL) {
+    const int t = seqs.count();
+    std::uint64_t product = 1;  // configuration_count, oracle.hpp:28-39
+    for (int i = 1; i <= t; ++i) {
+        const std::uint64_t w = static_cast<std::uint64_t>(seqs.window_count(i, l));
+        if (w == 0 || product > limit / w) {
+            product = limit + 1;
+            break;
+        }
+        product *= w;
+    }
+    if (product > limit) {
+        throw SearchSpaceTooLargeError("naive search needs more than " + std::to_string(limit) +
+                                       " configurations; lower t, n, or raise the limit");
+    }
+    auto rank = [](char c) { return c == 'A' ? 0 : c == 'C' ? 1 : c == 'T' ? 2 : 3; };  // alphabet.hpp:33-36
+    std::vector<int> prof(static_cast<std::size_t>(4 * l), 0);
+    StartVector pos(static_cast<std::size_t>(t), 1);
+    for (int i = 1; i <= t; ++i) {
+        for (int c = 0; c < l; ++c) ++prof[static_cast<std::size_t>(4 * c + rank(seqs.sequence(i)[static_cast<std::size_t>(c)]))];
+    }
+    auto move_row = [&](int i, int j, int j2) {
+        const std::string& s = seqs.sequence(i);
+        for (int c = 0; c < l; ++c) {
+            --prof[static_cast<std::size_t>(4 * c + rank(s[static_cast<std::size_t>(j - 1 + c)]))];
+            ++prof[static_cast<std::size_t>(4 * c + rank(s[static_cast<std::size_t>(j2 - 1 + c)]))];
+        }
+    };
+    NaiveMfpResult best;
+    best.score = -1;
+    for (;;) {
+        int sc = 0;
+        for (int c = 0; c < l; ++c) {
+            sc += std::max(std::max(prof[static_cast<std::size_t>(4 * c)], prof[static_cast<std::size_t>(4 * c + 1)]),
+                           std::max(prof[static_cast<std::size_t>(4 * c + 2)], prof[static_cast<std::size_t>(4 * c + 3)]));
+        }
+        if (sc > best.score) {
+            best.score = sc;
+            best.positions = pos;
+        }
+        int i = t;
+        while (i >= 1 && pos[static_cast<std::size_t>(i - 1)] == seqs.window_count(i, l)) {
+            move_row(i, pos[static_cast<std::size_t>(i - 1)], 1);
+            pos[static_cast<std::size_t>(i - 1)] = 1;
+            --i;
+        }
+        if (i < 1) break;
+        move_row(i, pos[static_cast<std::size_t>(i - 1)], pos[static_cast<std::size_t>(i - 1)] + 1);
+        ++pos[static_cast<std::size_t>(i - 1)];
+    }
+    best.consensus = consensus(seqs, best.positions, l);
+    return best;
+}
+
+// ---- driver.hpp:222-302: benchmark() -- the projection pipeline against both exact solvers, TSV report
+struct BenchConfig {
+    int instances = 20;
+    int t = 3;
+    int n = 10;
+    int l = 3;
+    int d = 1;
+    std::uint64_t seed = 1;
+    RunConfig run;  // l, d, and seed are overwritten per instance
+    std::uint64_t naive_limit = 100000000ULL;
+    std::uint64_t median_limit = 16777216ULL;
+};
+
+namespace detail {
+template <typename F>
+inline double timed_ms(F&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f();
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace detail
+
+inline std::string benchmark(const BenchConfig& config) {
+    if (config.instances < 1) throw InvalidParamsError("benchmark needs at least one instance");
+    std::string out = "instance\tseed\trun_score\toracle_score\tmedian_distance\tagree\trun_ms\tnaive_ms\tmedian_ms\n";
+    int agree_count = 0;
+    double total_run_ms = 0.0, total_naive_ms = 0.0, total_median_ms = 0.0;
+    for (int i = 1; i <= config.instances; ++i) {
+        const std::uint64_t inst_seed = derive_seed(config.seed, static_cast<std::uint64_t>(i));
+        const PlantedInstance inst = generate_planted(config.t, config.n, config.l, config.d, inst_seed);
+        RunConfig rc = config.run;
+        rc.l = config.l;
+        rc.d = config.d;
+        rc.seed = inst_seed;
+        int run_score = -1;  // kept when no bucket is ever enriched
+        const double run_ms = detail::timed_ms([&] {
+            try {
+                run_score = run(rc, inst.sequences).best.score;
+            } catch (const NoEnrichedBucketsError&) {
+            }
+        });
+        NaiveMfpResult naive;
+        const double naive_ms = detail::timed_ms([&] { naive = naive_mfp(inst.sequences, config.l, config.naive_limit); });
+        MedianStringResult median;
+        const double median_ms = detail::timed_ms([&] { median = median_string(inst.sequences, config.l, config.median_limit); });
+        const bool agree = run_score == naive.score;
+        agree_count += agree ? 1 : 0;
+        total_run_ms += run_ms;
+        total_naive_ms += naive_ms;
+        total_median_ms += median_ms;
+        out += std::to_string(i) + "\t" + std::to_string(inst_seed) + "\t" + std::to_string(run_score) + "\t" +
+               std::to_string(naive.score) + "\t" + std::to_string(median.total_distance) + "\t" + (agree ? "true" : "false") +
+               "\t" + detail::format_ms(run_ms) + "\t" + detail::format_ms(naive_ms) + "\t" + detail::format_ms(median_ms) + "\n";
+    }
+    out += "summary\t-\t-\t-\t-\t" + std::to_string(agree_count) + "/" + std::to_string(config.instances) + "\t" +
+           detail::format_ms(total_run_ms) + "\t" + detail::format_ms(total_naive_ms) + "\t" + detail::format_ms(total_median_ms) + "\n";
+    return out;
 }
 
 }  // namespace projmotif_b200

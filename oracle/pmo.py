@@ -25,7 +25,7 @@ ERR_NAMES = {
     0: "ok", 1: "InvalidParamsError", 2: "LengthMismatchError", 3: "KmerTooLongError",
     4: "DenseTableTooLargeError", 5: "UnreachableError", 6: "EmptyBucketError",
     7: "NoEnrichedBucketsError", 8: "NumericalUnderflowError", 9: "UnknownSymbolError",
-    10: "IndexOutOfRangeError", 99: "Error",
+    10: "IndexOutOfRangeError", 11: "SearchSpaceTooLargeError", 99: "Error",
 }
 
 
@@ -319,6 +319,21 @@ class Oracle:
         self._check(self.lib.pmo_total_distance(ss.bases, _p(ss.offs, C.c_int64), ss.t, v.encode(), len(v),
                                                 C.byref(tot), _p(per, C.c_int32)))
         return tot.value, per.tolist()
+
+    # ---- exact solvers for small instances (oracle.hpp)
+    def median_string(self, ss, l, limit=16777216):
+        med = C.create_string_buffer(l + 1)
+        dist = C.c_int()
+        self._check(self.lib.pmo_median_string(ss.bases, _p(ss.offs, C.c_int64), ss.t, l, C.c_uint64(limit), med, C.byref(dist)))
+        return med.value.decode(), dist.value
+
+    def naive_mfp(self, ss, l, limit=100000000):
+        pos = np.zeros(ss.t, dtype=np.int32)
+        sc = C.c_int()
+        cons = C.create_string_buffer(l + 1)
+        self._check(self.lib.pmo_naive_mfp(ss.bases, _p(ss.offs, C.c_int64), ss.t, l, C.c_uint64(limit), _p(pos, C.c_int32),
+                                           C.byref(sc), cons))
+        return pos.tolist(), sc.value, cons.value.decode()
 
     # ---- driver
     def config(self, **kw):

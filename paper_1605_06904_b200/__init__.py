@@ -28,7 +28,7 @@ STATUS_NAMES = {
     0: "ok", 1: "InvalidParamsError", 2: "LengthMismatchError", 3: "KmerTooLongError",
     4: "DenseTableTooLargeError", 5: "UnreachableError", 6: "EmptyBucketError",
     7: "NoEnrichedBucketsError", 8: "NumericalUnderflowError", 9: "UnknownSymbolError",
-    10: "IndexOutOfRangeError", 50: "Unsupported", 100: "CudaError", 101: "NoDevice", 102: "OutOfMemory",
+    10: "IndexOutOfRangeError", 11: "SearchSpaceTooLargeError", 50: "Unsupported", 100: "CudaError", 101: "NoDevice", 102: "OutOfMemory",
 }
 
 
@@ -108,7 +108,7 @@ EXPORTS = [
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
     "pm_ctx_launch_count", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_score",
-    "pm_hamming_scan", "pm_run", "pm_run_host",
+    "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host",
 ]
 
 _lib = None
@@ -401,6 +401,13 @@ class Context:
         within = C.c_int()
         _check(lib().pm_hamming_scan(self._h, v.encode(), len(v), d, _p(per, C.c_int32), C.byref(tot), C.byref(within)))
         return per.tolist(), tot.value, within.value
+
+    def median_string(self, l, limit=16777216):
+        """median_string, oracle.hpp:120-149, on the device (l <= 16): (median, total_distance)."""
+        med = C.create_string_buffer(l + 1)
+        dist = C.c_int()
+        _check(lib().pm_median_string(self._h, l, C.c_uint64(limit), med, C.byref(dist)))
+        return med.value.decode(), dist.value
 
     # ---- the whole path
     def run(self, per_trial=False, **kw):

@@ -1293,6 +1293,36 @@ int pm_hamming_scan(pm_ctx* c, const char* v, int l, int d, int32_t* per_seq_min
     return PM_OK;
 }
 
+int pm_median_string(pm_ctx* c, int l, uint64_t limit, char* median, int* total_distance) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    if (median == nullptr || total_distance == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null output pointer");
+    if (l < 1 || l > 31) return set_error(PM_ERR_INVALID_PARAMS, "median string needs 1 <= l <= 31");  // oracle.hpp:122-124
+    PM_TRY(prepare_windows(c, l));  // every n_i >= l (oracle.hpp:125-127)
+    const uint64_t candidates = pow4(l);
+    if (candidates > limit) {
+        return set_error(PM_ERR_SEARCH_SPACE_TOO_LARGE, "median search needs " + std::to_string(candidates) +
+                                                            " candidates, above the limit of " + std::to_string(limit));
+    }
+    if (l > 16) return set_error(PM_ERR_UNSUPPORTED, "median string on the device is limited to l <= 16 (32-bit candidate codes)");
+    PM_CUDA(cudaSetDevice(c->device));
+    unsigned long long* d_best;
+    PM_TRY(get_buf(c, S_TMP_D, 16, &d_best));
+    PM_CUDA(cudaMemsetAsync(d_best, 0xFF, sizeof(unsigned long long), c->stream));
+    const uint64_t per_tile = static_cast<uint64_t>(k::kMedianThreads) * k::kMedianCands;
+    const uint64_t tiles = (candidates + per_tile - 1) / per_tile;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(c->sm_count) * 8));
+    k::median_string_kernel<<<grid, k::kMedianThreads, 0, c->stream>>>(c->d_words, c->d_word_off, c->d_seq_len, c->t, l,
+                                                                      candidates, d_best);
+    PM_TRY(check_launch(c, "median_string"));
+    unsigned long long best = 0;
+    PM_TRY(d2h(c, &best, d_best, sizeof(best)));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    *total_distance = static_cast<int>(best >> 32);
+    unpack_consensus((best & 0xFFFFFFFFULL) << (64 - 2 * l), l, median);
+    return PM_OK;
+}
+
 // ------------------------------------------------------------------------------------------------
 // run(), driver.hpp:145-220
 // ------------------------------------------------------------------------------------------------

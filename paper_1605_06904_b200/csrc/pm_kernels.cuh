@@ -911,6 +911,71 @@ __global__ void hamming_scan_kernel(const uint64_t* __restrict__ words, const in
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// median_string (oracle.hpp:120-149): exhaustive search over the 4^l candidates for the first minimiser of
+// TotalDistance(v) = sum_i min_j hamming(v, S_ij) (oracle.hpp:101-115).  Thread = kMedianCands candidate codes
+// (a code is the l-mer itself: first base most significant, kmer.hpp:57-69); the windows of one sequence at a
+// time are expanded into shared memory as top-aligned 32-bit l-mers (l <= 16) and every thread scans them with
+// XOR/popcount.  Result: min over candidates of (distance << 32 | code), i.e. the smallest code among the
+// minimisers -- the reference's "first minimiser in ascending code order".
+// ---------------------------------------------------------------------------------------------
+constexpr int kMedianThreads = 256;
+constexpr int kMedianCands = 4;
+constexpr int kMedianChunk = 4096;  // windows staged per round (16 KB)
+
+__global__ void __launch_bounds__(kMedianThreads)
+median_string_kernel(const uint64_t* __restrict__ words, const int64_t* __restrict__ word_off,
+                     const int32_t* __restrict__ seq_len, int t, int l, uint64_t n_cand,
+                     unsigned long long* __restrict__ best) {
+    __shared__ uint32_t win[kMedianChunk];
+    const uint32_t digit_mask = (0x55555555u >> (32 - 2 * l)) << (32 - 2 * l);
+    const int up = 32 - 2 * l;
+    const uint64_t per_tile = static_cast<uint64_t>(kMedianThreads) * kMedianCands;
+    for (uint64_t tile = blockIdx.x; tile * per_tile < n_cand; tile += gridDim.x) {
+        uint32_t cand[kMedianCands];
+        int total[kMedianCands];
+#pragma unroll
+        for (int k = 0; k < kMedianCands; ++k) {
+            const uint64_t code = tile * per_tile + static_cast<uint64_t>(k) * kMedianThreads + threadIdx.x;
+            cand[k] = static_cast<uint32_t>(code) << up;  // codes past n_cand are computed and discarded
+            total[k] = 0;
+        }
+        for (int i = 0; i < t; ++i) {
+            const uint64_t* wp = words + word_off[i];
+            const int W = seq_len[i] - l + 1;
+            int seq_best[kMedianCands];
+#pragma unroll
+            for (int k = 0; k < kMedianCands; ++k) seq_best[k] = l + 1;
+            for (int start = 0; start < W; start += kMedianChunk) {
+                const int cnt = min(kMedianChunk, W - start);
+                __syncthreads();
+                for (int j = threadIdx.x; j < cnt; j += kMedianThreads) win[j] = static_cast<uint32_t>(load_window(wp, start + j) >> 32);
+                __syncthreads();
+#pragma unroll 4
+                for (int j = 0; j < cnt; ++j) {
+                    const uint32_t v = win[j];  // warp-uniform address: one broadcast load
+#pragma unroll
+                    for (int k = 0; k < kMedianCands; ++k) {
+                        const uint32_t xr = v ^ cand[k];
+                        seq_best[k] = min(seq_best[k], __popc((xr | (xr >> 1)) & digit_mask));
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kMedianCands; ++k) total[k] += seq_best[k];
+        }
+        unsigned long long mine = ~0ULL;
+#pragma unroll
+        for (int k = 0; k < kMedianCands; ++k) {
+            const uint64_t code = tile * per_tile + static_cast<uint64_t>(k) * kMedianThreads + threadIdx.x;
+            if (code < n_cand) mine = min(mine, (static_cast<unsigned long long>(total[k]) << 32) | code);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xffffffffu, mine, o));
+        if ((threadIdx.x & 31) == 0 && mine != ~0ULL) atomicMin(best, mine);
+    }
+}
+
 // profile score + consensus of one start vector (0-based starts), single CTA
 __global__ void score_kernel(const uint64_t* __restrict__ words, const int64_t* __restrict__ word_off, int t, int l,
                              const int32_t* __restrict__ starts0, int32_t* __restrict__ out_score,

@@ -1,7 +1,7 @@
 // projmotif_b200 — command-line front end of the B200 PROJECTION path, mirroring the reference's
-// `projmotif find` and `projmotif gen` (tools/projmotif.cpp:67-113, 164-187): same flags, same JSON/TSV
-// report (report.hpp schema v1), same exit codes (0 ok, 2 parameter/usage, 3 no enriched bucket,
-// 4 parse/I-O).  `oracle` and `bench` (exponential exact solvers) are out of scope.
+// `projmotif find`, `gen`, `oracle` and `bench` (tools/projmotif.cpp:67-148, 164-211): same flags, same
+// JSON/TSV reports (report.hpp schema v1), same exit codes (0 ok, 2 parameter/usage, 3 no enriched bucket,
+// 4 parse/I-O).  `oracle --method median` runs on the device; `--method naive` is the exponential host solver.
 //
 //   g++ -std=c++17 -O2 -Iinclude tools/projmotif_b200.cpp -Lpaper_1605_06904_b200 -lpm_b200 \
 //       -Wl,-rpath,$PWD/paper_1605_06904_b200 -o projmotif_b200
@@ -129,7 +129,10 @@ int usage(std::ostream& os) {
           "Usage: projmotif_b200 find -i FASTA --l L --d D [--k K] [--s S] [--m M] [--q Q] [--seed N] [--workers N]\n"
           "                           [--backend dense|grouped|auto] [--max-em-iters N] [--s-floor N] [--no-early-stop]\n"
           "                           [--format json|tsv] [--device N]\n"
-          "       projmotif_b200 gen --t T --n N --l L --d D [--seed N] -o OUT.fasta\n";
+          "       projmotif_b200 gen --t T --n N --l L --d D [--seed N] -o OUT.fasta\n"
+          "       projmotif_b200 oracle -i FASTA --l L [--method naive|median] [--limit N]\n"
+          "       projmotif_b200 bench [--instances N] [--t T] [--n N] [--l L] [--d D] [--seed N] [--s S] [--m M] [--q Q]\n"
+          "                            [--workers N] [--backend dense|grouped|auto] [--naive-limit N] [--median-limit N]\n";
     return 0;
 }
 
@@ -181,8 +184,51 @@ int main(int argc, char** argv) {
             write_file(out, pmx::serialize_fasta(inst.sequences));
             write_file(out + ".truth.json", pmx::truth_json(inst));
             std::cerr << "wrote " << out << " and " << out << ".truth.json\n";
+        } else if (cmd == "oracle") {  // tools/projmotif.cpp:115-125, 187-204
+            const Args a = parse_flags(argc, argv, 2, {"--input", "--l", "--method", "--limit", "--device"}, {}, {{"-i", "--input"}});
+            if (!a.values.count("--input")) throw UsageError("--input is required");
+            const std::string method = a.values.count("--method") ? a.values.at("--method") : "naive";
+            if (method != "naive" && method != "median") throw UsageError("--method: " + method + " not in {naive,median}");
+            const int l = required<int>(a, "--l");
+            const auto limit = opt_number<std::uint64_t>(a, "--limit");
+            if (const auto dev = opt_number<int>(a, "--device")) pmx::Device::instance().set_device(*dev);
+            const pmx::SequenceSet seqs = read_input(a.values.at("--input"));
+            std::string doc = "{\n";
+            if (method == "naive") {
+                const pmx::NaiveMfpResult res = pmx::naive_mfp(seqs, l, limit.value_or(100000000ULL));
+                doc += "  \"method\": \"naive\",\n  \"score\": " + std::to_string(res.score) + ",\n  \"positions\": " +
+                       pmx::detail::json_int_array(res.positions, "  ") + ",\n  \"consensus\": " + pmx::detail::json_string(res.consensus) + "\n";
+            } else {
+                const pmx::MedianStringResult res = pmx::median_string(seqs, l, limit.value_or(16777216ULL));
+                doc += "  \"method\": \"median\",\n  \"median\": " + pmx::detail::json_string(res.median) +
+                       ",\n  \"total_distance\": " + std::to_string(res.total_distance) + "\n";
+            }
+            std::cout << doc << "}\n";
+        } else if (cmd == "bench") {  // tools/projmotif.cpp:127-148, 205-210
+            const Args a = parse_flags(argc, argv, 2,
+                                       {"--instances", "--t", "--n", "--l", "--d", "--seed", "--s", "--m", "--q", "--workers",
+                                        "--backend", "--naive-limit", "--median-limit", "--device"},
+                                       {}, {});
+            pmx::BenchConfig bench;
+            bench.instances = opt_number<int>(a, "--instances").value_or(bench.instances);
+            bench.t = opt_number<int>(a, "--t").value_or(bench.t);
+            bench.n = opt_number<int>(a, "--n").value_or(bench.n);
+            bench.l = opt_number<int>(a, "--l").value_or(bench.l);
+            bench.d = opt_number<int>(a, "--d").value_or(bench.d);
+            bench.seed = opt_number<std::uint64_t>(a, "--seed").value_or(bench.seed);
+            bench.run.s = opt_number<int>(a, "--s").value_or(3);  // the derived threshold is unattainable at oracle scale
+            bench.run.m = opt_number<std::int64_t>(a, "--m");
+            bench.run.q = opt_number<double>(a, "--q").value_or(bench.run.q);
+            bench.run.workers = opt_number<int>(a, "--workers").value_or(env_workers());
+            const std::string backend = a.values.count("--backend") ? a.values.at("--backend") : "auto";
+            if (backend != "dense" && backend != "grouped" && backend != "auto") throw UsageError("--backend: " + backend + " not in {dense,grouped,auto}");
+            bench.run.backend = backend == "dense" ? pmx::HashBackend::dense : backend == "grouped" ? pmx::HashBackend::grouped : pmx::HashBackend::automatic;
+            bench.naive_limit = opt_number<std::uint64_t>(a, "--naive-limit").value_or(bench.naive_limit);
+            bench.median_limit = opt_number<std::uint64_t>(a, "--median-limit").value_or(bench.median_limit);
+            if (const auto dev = opt_number<int>(a, "--device")) pmx::Device::instance().set_device(*dev);
+            std::cout << pmx::benchmark(bench);
         } else {
-            throw UsageError("unknown subcommand: " + cmd + " (find, gen; the exact-solver commands are out of scope)");
+            throw UsageError("unknown subcommand: " + cmd + " (find, gen, oracle, bench)");
         }
         return 0;
     } catch (const UsageError& e) {
