@@ -621,7 +621,7 @@ size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_w
     b += (2 * TH + 2 * TH + 2 * TH + 2 * static_cast<size_t>(nwarps) + 12) * 8;              // thd, D64, L64, llpart, dscal
     b += 16 * static_cast<size_t>(G) * 8;                                                    // T2
     b += (32 * static_cast<size_t>(G) + (16 + static_cast<size_t>(nwarps)) * NV + 2 * tpad + 4) * 4;  // Cq, cpart, mprev, ubs
-    b += (256 + 8 + 20 + 12 + 4 * tpad) * 4;                                                 // prof, iscal, s_off, wrow, smeta
+    b += (256 + 8 + 20 + 16 + 4 * tpad) * 4;                                                 // prof, iscal, s_off, wrow, smeta
     b += 16;                                                                                 // cons_bits
     b += static_cast<size_t>(nwarps) * 2 * k::kPairNearCap * 2;                              // near_j
     b = (b + 15) & ~static_cast<size_t>(15);
@@ -629,6 +629,18 @@ size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_w
     b += static_cast<size_t>(total_words) * 8;                                               // TMA word stage
     b += 16;                                                                                 // mbarrier
     return b + 16;
+}
+
+int em_smem_warps_for(int t);
+
+// Warps per CTA of the pair kernel: as for the one-bucket kernel, a divisor of t so that the E-step (warp per
+// sequence) is balanced; 12 warps were measured equal (C1) or slower (C2: ten sequences per tile) than 10.
+int em_pair_warps_for(int t) {
+    if (const char* env = std::getenv("PM_B200_EM_WARPS")) {  // tuning knob
+        const long v = std::atol(env);
+        if (v >= 2 && v <= k::kPairMaxWarps) return static_cast<int>(v);
+    }
+    return em_smem_warps_for(t);
 }
 
 bool em_pair_enabled() {
@@ -734,7 +746,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         c->max_seq_len < 65536 && em_pair_enabled()) {
         // two buckets per CTA in lockstep (pm_em_pair.cuh): every t=20 configuration
         const int G = (l + 1) / 2;
-        const int nwarps = em_smem_warps_for(c->t);
+        const int nwarps = em_pair_warps_for(c->t);
         const int threads = nwarps * 32;
         const size_t smem = em_pair_smem_bytes(nwarps, G, l, c->zlen, c->t, static_cast<int>(c->total_words));
         if (smem <= 227 * 1024) {
@@ -752,6 +764,10 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
                 c->pair_cfg_per_sm = per_sm;
             }
             if (per_sm >= 1) {
+                if (const char* env = std::getenv("PM_B200_EM_PER_SM")) {  // experiment knob: fewer resident CTAs
+                    const long v = std::atol(env);
+                    if (v >= 1 && v < per_sm) per_sm = static_cast<int>(v);
+                }
                 const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
                 const unsigned int grid = std::max(1u, std::min(full, (n_work_bound + 1) / 2));
                 k::EmSmemExtra x;

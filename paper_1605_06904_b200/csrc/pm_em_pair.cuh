@@ -22,7 +22,7 @@
 namespace pm {
 namespace k {
 
-constexpr int kPairMaxWarps = 10;
+constexpr int kPairMaxWarps = 12;
 constexpr int kPairMaxSeqs = 64;     // per-sequence state (previous maxima, metadata) lives in shared memory
 constexpr int kPairMaxWords = 2048;  // packed words of the whole set, staged once per CTA by one TMA bulk copy
 constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
@@ -335,8 +335,8 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
     int* prof = reinterpret_cast<int*>(ubs + 4);              // [2][128]
     int* iscal = prof + 256;                                  // [2][4]: [0] stop [1] score [2] bad [3] iterations
     int* s_off = iscal + 8;                                   // [17] first row of each class (+3 pad)
-    int* wrow = s_off + 20;                                   // [nwarps + 1] class-row range of each warp (12 slots)
-    int* smeta = wrow + 12;                                  // [tpad][4]: word offset, windows, z offset, z slots
+    int* wrow = s_off + 20;                                   // [nwarps + 1] class-row range of each warp (16 slots)
+    int* smeta = wrow + 16;                                  // [tpad][4]: word offset, windows, z offset, z slots
     unsigned long long* cons_bits = reinterpret_cast<unsigned long long*>(smeta + 4 * tpad);  // [2]
     uint16_t* near_j = reinterpret_cast<uint16_t*>(cons_bits + 2);                            // [nwarps][2][kPairNearCap]
     // offsets are aligned as integers (smem_raw is 16-byte aligned) so that every pointer below stays a
@@ -450,14 +450,17 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                 reinterpret_cast<float*>(T2)[e2] = static_cast<float>(v);
             }
             if (iterations == 0 && !final_pass && warp >= nwarps - 2) {
-                // no window weight exceeds the sum of the column maxima: the reference point of iteration 0
+                // No window weight exceeds ub = the sum of the column maxima.  Iteration 0 takes its exponentials
+                // relative to ub - 40: e <= exp(40) cannot overflow, and a sequence whose best window lies up to 100
+                // below ub (four floored columns of theta0) still has its maximum inside the +-60 window that the
+                // fused pass needs (at ub itself 47 % of the C1 sequences fell back to the two-pass form).
                 const int b = warp - (nwarps - 2);
                 const double* L = L64 + b * TH;
                 const int c = lane + 1;
                 double m = 0.0;
                 if (lane < l) m = fmax(fmax(L[c * 4] - L[0], L[c * 4 + 1] - L[1]), fmax(L[c * 4 + 2] - L[2], L[c * 4 + 3] - L[3]));
                 m = warp_sum_d(m);
-                if (lane == 0) ubs[b] = static_cast<float>(m);
+                if (lane == 0) ubs[b] = static_cast<float>(m) - 40.f;
             }
             #pragma unroll 1
             for (int e = threadIdx.x; e < 32 * G; e += blockDim.x) Cq[e] = 0.f;
