@@ -89,6 +89,11 @@ struct pm_ctx {
     int pair_cfg_l = -1, pair_cfg_threads = 0, pair_cfg_per_sm = 0;  // same for the two-bucket kernel
     size_t pair_cfg_smem = 0;
     int32_t max_seq_len = 0;
+    // host staging of the class-group index: lives in the context so the async uploads need no sync of their own
+    std::vector<k::TileDesc> h_tiles;
+    std::vector<int> h_zoff, h_group_off;
+    std::vector<uint16_t> h_entries;
+    std::vector<std::vector<uint16_t>> h_bins;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -233,12 +238,19 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         if (v >= 256 && v <= 48000) cap = v;
     }
     auto code = [](char ch) { return (static_cast<unsigned char>(ch) >> 1) & 3; };
-    std::vector<k::TileDesc> tiles;
-    std::vector<int> zoff(static_cast<size_t>(t));
-    std::vector<int> group_off;  // 17 per tile
-    std::vector<uint16_t> entries;
-    std::vector<int> load(16 * 32), mine(16 * 32);
-    std::vector<std::vector<uint16_t>> bins(16 * 32);
+    std::vector<k::TileDesc>& tiles = c->h_tiles;
+    std::vector<int>& zoff = c->h_zoff;
+    std::vector<int>& group_off = c->h_group_off;  // 17 per tile
+    std::vector<uint16_t>& entries = c->h_entries;
+    tiles.clear();
+    zoff.assign(static_cast<size_t>(t), 0);
+    group_off.clear();
+    entries.clear();
+    // per class: residue loads stored twice in a row (load2[q][r] == load2[q][r + 32]) so that the shift search
+    // below reads contiguous runs and vectorises
+    std::vector<int> load2(16 * 64), mine(16 * 32);
+    std::vector<std::vector<uint16_t>>& bins = c->h_bins;
+    bins.resize(16 * 32);
     int64_t live_slots = 0;
     int zcap = 0, wcap = 0;
     int i = 0;
@@ -246,7 +258,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         k::TileDesc tile;
         tile.seq_begin = i;
         tile.group_base = static_cast<int>(entries.size() / 32);
-        std::fill(load.begin(), load.end(), 0);
+        std::fill(load2.begin(), load2.end(), 0);
         for (auto& b : bins) b.clear();
         int64_t cursor = k::kZPad;
         while (i < t) {
@@ -265,10 +277,10 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
             for (int sh = 0; sh < 32; ++sh) {
                 int64_t cost = 0;
                 for (int q = 0; q < 16; ++q) {
+                    const int* __restrict__ lq = load2.data() + q * 64 + sh;  // lq[r] = load[q][(r + sh) & 31]
+                    const int* __restrict__ mq = mine.data() + q * 32;
                     int mx = 0;
-                    for (int r = 0; r < 32; ++r) {
-                        mx = std::max(mx, load[static_cast<size_t>(q * 32 + ((r + sh) & 31))] + mine[static_cast<size_t>(q * 32 + r)]);
-                    }
+                    for (int r = 0; r < 32; ++r) mx = std::max(mx, lq[r] + mq[r]);
                     cost += mx;
                 }
                 if (best_cost < 0 || cost < best_cost) {
@@ -277,7 +289,11 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
                 }
             }
             for (int q = 0; q < 16; ++q) {
-                for (int r = 0; r < 32; ++r) load[static_cast<size_t>(q * 32 + ((r + best_shift) & 31))] += mine[static_cast<size_t>(q * 32 + r)];
+                for (int r = 0; r < 32; ++r) {
+                    const int dst = (r + best_shift) & 31;
+                    load2[static_cast<size_t>(q * 64 + dst)] += mine[static_cast<size_t>(q * 32 + r)];
+                    load2[static_cast<size_t>(q * 64 + dst + 32)] = load2[static_cast<size_t>(q * 64 + dst)];
+                }
             }
             cursor += best_shift;
             zoff[static_cast<size_t>(i)] = static_cast<int>(cursor);
@@ -322,7 +338,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * group_off.size()));
     PM_TRY(h2d(c, c->d_seq_zoff, zoff.data(), sizeof(int) * zoff.size()));
     PM_TRY(h2d(c, c->d_tiles, tiles.data(), sizeof(k::TileDesc) * tiles.size()));
-    PM_CUDA(cudaStreamSynchronize(c->stream));
+    // no sync here: the staging vectors belong to the context and pm_ctx_set_sequences synchronises once at its end
     c->zlen = zcap;
     c->tile_words = wcap;
     c->n_tiles = static_cast<int>(tiles.size());

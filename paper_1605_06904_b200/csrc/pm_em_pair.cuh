@@ -34,10 +34,15 @@ __device__ __noinline__ double exp_f64(double x) { return exp(x); }
 __device__ __noinline__ double log_f64(double x) { return log(x); }
 
 __device__ __forceinline__ double window_weight_rolled(const double* __restrict__ D64, uint64_t v, int l) {
-    double w = 0.0;
-#pragma unroll 2
-    for (int c = 0; c < l; ++c) w += D64[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)];
-    return w;
+    double w0 = 0.0, w1 = 0.0;  // two chains: the sum is latency-bound
+    int c = 0;
+#pragma unroll 1
+    for (; c + 1 < l; c += 2) {
+        w0 += D64[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)];
+        w1 += D64[c * 4 + 4 + (static_cast<unsigned>(v >> (60 - 2 * c)) & 3u)];
+    }
+    if (c < l) w0 += D64[c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)];
+    return w0 + w1;
 }
 
 struct SeqAcc {
@@ -253,12 +258,12 @@ __device__ __forceinline__ void pair_detect(float* __restrict__ zb, int W, int l
 template <int G>
 __device__ __forceinline__ float pair_settle(const float* __restrict__ Tb, const uint64_t* __restrict__ wp, int W, int lane,
                                              float* __restrict__ zb, uint16_t* __restrict__ my_near, SeqAcc& a, float& ref,
-                                             float& M, float& near_e, float log_z_eps, bool force_rebuild, bool want_near,
-                                             int* bad) {
+                                             float& M, float total, int n_cand, float& near_e, float log_z_eps,
+                                             bool force_rebuild, bool want_near, int* bad) {
+    // M (in/out), total and n_cand are the warp-wide max / sum / count of pass A, reduced by the caller for both
+    // buckets at once
     constexpr float kNearMargin = 4.f;
-    M = warp_max_f(a.best_w);
     if (!(M > -INFINITY) || !(M < INFINITY)) *bad = 1;
-    float total = warp_sum_f(a.s_all);
     const float shift = M - ref;
     const bool have_e = shift > -60.f && shift < 60.f && total > 0.f && total < INFINITY;
     if (!have_e) {
@@ -279,8 +284,7 @@ __device__ __forceinline__ float pair_settle(const float* __restrict__ Tb, const
         a.overflow = true;
         if (want_near) {
             // the count is an upper bound of the list length unless the maximum dropped below the margin
-            const int n = __reduce_add_sync(0xffffffffu, a.ncand);
-            if (force_rebuild || M < ref - kNearMargin || n <= kPairNearCap) {
+            if (force_rebuild || M < ref - kNearMargin || n_cand <= kPairNearCap) {
                 __syncwarp();
                 float ignore = 0.f;
                 a.s_far = 0.f, a.nnear = 0, a.overflow = false;
@@ -358,6 +362,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         smeta[4 * i + 0] = static_cast<int>(p.word_off[i] - word0);
         smeta[4 * i + 1] = p.seq_len[i] - l + 1;
         smeta[4 * i + 2] = x.seq_zoff[i];
+        smeta[4 * i + 3] = static_cast<int>(p.win_off[i]);  // first flat l-mer index of the sequence
     }
     __syncthreads();
     mbar_wait(&mbar[0], 0);
@@ -397,8 +402,12 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         for (unsigned int m = threadIdx.x; m < wd0.count + wd1.count; m += blockDim.x) {
             const int b = m >= wd0.count;
             const int64_t f = b ? p.members[wd1.mem_begin + (m - wd0.count)] : p.members[wd0.mem_begin + m];
-            const int i = seq_of_flat(p.win_off, t, f);
-            const uint64_t v = load_window(wstage + smeta[4 * i], f - p.win_off[i]);
+            int i = 0;
+            for (int hi = t; hi - i > 1;) {  // owner of flat l-mer index f: largest i with win_off[i] <= f
+                const int mid = (i + hi) >> 1;
+                if (smeta[4 * mid + 3] <= f) i = mid; else hi = mid;
+            }
+            const uint64_t v = load_window(wstage + smeta[4 * i], f - smeta[4 * i + 3]);
             #pragma unroll 1
             for (int c = 0; c < l; ++c) atomicAdd(&prof[b * 128 + c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)], 1);
         }
@@ -485,7 +494,6 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     const int chunks = (W + 31) >> 5;
                     float2* zs = zbuf + zo;
                     float* zb0 = zf + 2 * zo;
-                    float* zb1 = zb0 + 1;
                     {
                         // slots that are not window starts read as zero in the M-step gather
                         const int z_end = (i + 1 < tile.seq_end ? smeta[4 * (i + 1) + 2] : tile.zlen) - zo;
@@ -581,12 +589,22 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     // the FP64 pass is skipped in the last iteration of the budget: its likelihood can no longer
                     // stop the loop (refine.hpp:296-304), so no near list is needed there
                     const bool want_near = iterations + 1 < p.max_iters;
+                    // warp-wide max / sum / candidate count of both buckets, their shuffle chains interleaved
+                    M0 = warp_max_f(a.best_w), M1 = warp_max_f(b.best_w);
+                    float tot0 = a.s_all, tot1 = b.s_all;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        tot0 += __shfl_xor_sync(0xffffffffu, tot0, o);
+                        tot1 += __shfl_xor_sync(0xffffffffu, tot1, o);
+                    }
+                    const int nc0 = __reduce_add_sync(0xffffffffu, a.ncand), nc1 = __reduce_add_sync(0xffffffffu, b.ncand);
 #pragma unroll 1
                     for (int bb = 0; bb < 2; ++bb) {  // rolled: one copy of the code for both buckets
                         SeqAcc s = bb ? b : a;
-                        float ref = bb ? ref1 : ref0, M, ne;
+                        float ref = bb ? ref1 : ref0, M = bb ? M1 : M0, ne;
                         const float inv = pair_settle<G>(T2f + bb, wp, W, lane, zb0 + bb, near_a + bb * kPairNearCap, s, ref, M,
-                                                         ne, p.log_z_eps, first, want_near, &iscal[bb * 4 + 2]);
+                                                         bb ? tot1 : tot0, bb ? nc1 : nc0, ne, p.log_z_eps, first, want_near,
+                                                         &iscal[bb * 4 + 2]);
                         if (lane == 0) mprev[bb * tpad + i] = M;
                         if (bb) {
                             b = s, ref1 = ref, M1 = M, inv1 = inv;
@@ -612,7 +630,10 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                         }
                     }
                     __syncwarp();
-                    // ---- log sum_j exp(w_j) per bucket
+                    // ---- log sum_j exp(w_j) per bucket; the FP32 form needs log(1/total): one logf for both buckets
+                    // (odd lanes take bucket 1)
+                    const float lg = logf((lane & 1) ? inv1 : inv0);
+                    const float lg0 = __shfl_sync(0xffffffffu, lg, 0), lg1 = __shfl_sync(0xffffffffu, lg, 1);
 #pragma unroll 1
                     for (int bb = 0; bb < 2; ++bb) {
                         const SeqAcc s = bb ? b : a;
@@ -620,7 +641,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                         const uint16_t* my_near = near_a + bb * kPairNearCap;
                         // the list holds exactly the windows with e >= near_e (lane L owns entries L and L + 32)
                         const bool n_a = !s.overflow && lane < s.nnear, n_b = !s.overflow && lane + 32 < s.nnear;
-                        const float ref = bb ? ref1 : ref0, M = bb ? M1 : M0, inv = bb ? inv1 : inv0;
+                        const float ref = bb ? ref1 : ref0, M = bb ? M1 : M0;
                         double lse;
                         if (!s.overflow) {
                             // FP64 re-evaluation of the dominant windows; the far tail (each < eps of the maximum)
@@ -641,7 +662,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                             if (n_a) zb[2 * my_near[lane]] = static_cast<float>(wa / s64);
                             if (n_b) zb[2 * my_near[lane + 32]] = static_cast<float>(wb / s64);
                         } else {
-                            lse = static_cast<double>(ref) - static_cast<double>(logf(inv));  // total is relative to ref
+                            lse = static_cast<double>(ref) - static_cast<double>(bb ? lg1 : lg0);  // total is relative to ref
                         }
                         // log P(S_i) = log prod theta_bg - log W + logsumexp_j w_ij (refine.hpp:200); the first two
                         // terms are summed over the set by the thread that closes the iteration
