@@ -372,6 +372,8 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         line["time_to_motif"] = time_to_motif(pm, ctx, cfg)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)
+        if "time_to_motif" in line:
+            cpu_time_to_motif(cfg, line["time_to_motif"], line["cpu_baseline"])
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -401,6 +403,29 @@ def time_to_motif(pm, ctx, cfg):
     hit = [r for r in rows if r["found"]]
     return {"runs": rows, "ms_median": statistics.median(r["ms"] for r in hit) if hit else None,
             "note": "wall ms incl. host, batches of 16 trials, stop at the first batch whose best == planted motif"}
+
+
+def cpu_time_to_motif(cfg, ttm, baseline):
+    """The reference's time to the same trial T*: projmotif::run over trials 1..T* (workers = host cores, its
+    blocks of `workers` trials run to completion, driver.hpp:186-209) on the instances time_to_motif() solved."""
+    oracle, kind = load_cpu_oracle()
+    if kind != "reference":
+        return
+    cores = os.cpu_count() or 1
+    rows = []
+    for r in ttm["runs"]:
+        if not r["found"]:
+            continue
+        ss, motif, _ = oracle.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], r["instance_seed"])
+        t0 = time.perf_counter()
+        got = oracle.run(ss, l=cfg["l"], d=cfg["d"], k=cfg["k"], s=cfg["s"], m=r["t_star"], seed=RUN_SEED, early_stop=0,
+                         workers=cores)
+        r["cpu_ms"] = 1e3 * (time.perf_counter() - t0)
+        r["cpu_found"] = got["consensus"] == motif
+        rows.append(r["cpu_ms"])
+    if rows:
+        ttm["cpu_ms_median"] = statistics.median(rows)
+        ttm["cpu_note"] = f"projmotif::run(m = T*, workers={cores}) wall ms on the same instances ({baseline['kind']})"
 
 
 def cpu_baseline(cfg):

@@ -605,6 +605,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                         const float inv = pair_settle<G>(T2f + bb, wp, W, lane, zb0 + bb, near_a + bb * kPairNearCap, s, ref, M,
                                                          bb ? tot1 : tot0, bb ? nc1 : nc0, ne, p.log_z_eps, first, want_near,
                                                          &iscal[bb * 4 + 2]);
+                        __syncwarp();  // every lane has read this sequence's previous maximum
                         if (lane == 0) mprev[bb * tpad + i] = M;
                         if (bb) {
                             b = s, ref1 = ref, M1 = M, inv1 = inv;
@@ -716,10 +717,16 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     for (int e = threadIdx.x; e < 32 * G; e += blockDim.x) {
                         const int b = e / (16 * G), rem = e - b * 16 * G;
                         const int q = rem / G, g = rem - q * G;
+                        // the warps owning rows of class q are consecutive: start at the one holding the class's first
+                        // row (closed-form guess, corrected against wrow) and walk while rows remain
+                        const int q_lo = s_off[q], q_hi = s_off[q + 1];
+                        int w = min(static_cast<int>(static_cast<long long>(q_lo) * nwarps / max(s_off[16], 1)), nwarps - 1);
+                        while (w > 0 && wrow[w] > q_lo) --w;
+                        while (w + 1 < nwarps && wrow[w + 1] <= q_lo) ++w;
                         float sum = 0.f;
                         #pragma unroll 1
-                        for (int w = 0; w < nwarps; ++w) {
-                            if (max(wrow[w], s_off[q]) < min(wrow[w + 1], s_off[q + 1])) sum += cpart[(w + q) * NV + b * G + g];
+                        for (; w < nwarps && wrow[w] < q_hi; ++w) {
+                            if (max(wrow[w], q_lo) < min(wrow[w + 1], q_hi)) sum += cpart[(w + q) * NV + b * G + g];
                         }
                         Cq[e] += sum;
                     }
