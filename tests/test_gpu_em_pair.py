@@ -76,3 +76,28 @@ def test_pair_kernel_agrees_with_one_bucket_kernel(pm, golden, instance):
                (x["consensus"], x["score"], x["positions"], x["iterations"])
         assert np.abs(a["theta"] - b["theta"]).max() < 1e-5
         assert abs(a["expectation"] - x["expectation"]) <= EXPECTATION_TOL
+
+
+def test_long_motifs_use_the_wide_flush_path(ctx, best_oracle):
+    """l > 16 means more than eight column pairs: 32-value class flushes, l = 31 fills the whole 64-bit window."""
+    import numpy as np
+    from oracle import pmo
+    rng = np.random.default_rng(77)
+    compared = 0
+    for l in (17, 20, 24, 31):
+        t = 6
+        ss = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(l + 20, l + 120)))) for _ in range(t)])
+        k = min(l - 2, 12)
+        kept = best_oracle.sample_plan(l, k, l)
+        en = best_oracle.enriched(ss, l, kept, 1, t)[:7]
+        ctx.set_sequences(ss.bases, ss.offs)
+        got = ctx.refine(l, [e["members"] for e in en])
+        for e, a in zip(en, got):
+            w = best_oracle.refine(ss, l, e["members"], e["key"])
+            assert a["iterations"] == w.iterations
+            assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL
+            assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+            if a["positions"] == w.positions:
+                assert (a["consensus"], a["score"]) == (w.consensus, w.score)
+                compared += 1
+    assert compared >= 20
