@@ -22,7 +22,7 @@
 namespace pm {
 namespace k {
 
-constexpr int kPairMaxWarps = 12;
+constexpr int kPairMaxWarps = 10;  // 12 was measured no faster and caps the kernel at 80 registers
 constexpr int kPairMaxSeqs = 64;     // per-sequence state (previous maxima, metadata) lives in shared memory
 constexpr int kPairMaxWords = 2048;  // packed words of the whole set, staged once per CTA by one TMA bulk copy
 constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
@@ -46,10 +46,15 @@ __device__ __forceinline__ double window_weight_rolled(const double* __restrict_
 }
 
 struct SeqAcc {
-    float best_w, s_all, s_far;
+    float best_w, s_all, s_far;  // s_all doubles as the lane's second-best weight in the scouting final sweep
     int best_j, nnear, ncand;
     bool overflow;
 };
+
+// modes of pass A
+constexpr int kPassFinal = 0;  // final sweep: stores w, tracks each lane's first maximum
+constexpr int kPassExp = 1;    // EM sweep: stores e = exp(w - ref), sums, counts near candidates
+constexpr int kPassScout = 2;  // final sweep without stores: each lane's first maximum and its second-best weight
 
 __device__ __forceinline__ void near_push16(unsigned ball, bool keep, int lane, int j, uint16_t* __restrict__ my_near,
                                             int& nnear, bool& overflow) {
@@ -120,27 +125,26 @@ __device__ __forceinline__ float single_weight(const float* __restrict__ Tb, uin
     return t[0];
 }
 
-template <bool kExp, bool kTail>
+template <int kMode, bool kTail>
 __device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live, float2* __restrict__ zq, float ref2a,
                                             float ref2b, float near_thr, SeqAcc& a, SeqAcc& b);
 
-// kExp: stores e = exp(w - ref) of both buckets, sums them, counts each lane's windows with e >= near_thr.
-// !kExp (final sweep): stores w, tracks each lane's first maximum.
-template <int G, bool kExp, bool kTail>
+// one 32-window chunk of pass A in the given mode (see kPassFinal / kPassExp / kPassScout)
+template <int G, int kMode, bool kTail>
 __device__ __forceinline__ void pair_chunk(const float2* __restrict__ T2, uint32_t vh, uint32_t vl, int j, bool live,
                                            float2* __restrict__ zq, float ref2a, float ref2b, float near_thr, SeqAcc& a,
                                            SeqAcc& b) {
     float w0 = -INFINITY, w1 = -INFINITY;
     if (!kTail || live) pair_weights<G>(T2, vh, vl, w0, w1);
-    pair_finish<kExp, kTail>(w0, w1, j, live, zq, ref2a, ref2b, near_thr, a, b);
+    pair_finish<kMode, kTail>(w0, w1, j, live, zq, ref2a, ref2b, near_thr, a, b);
 }
 
 // second half of pair_chunk: from the two weights to the stored value and the running sums
-template <bool kExp, bool kTail>
+template <int kMode, bool kTail>
 __device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live, float2* __restrict__ zq, float ref2a,
                                             float ref2b, float near_thr, SeqAcc& a, SeqAcc& b) {
     if (!kTail || live) {
-        if (kExp) {
+        if (kMode == kPassExp) {
             const float e0 = fast_ex2(fmaf(w0, kLog2e, -ref2a));
             const float e1 = fast_ex2(fmaf(w1, kLog2e, -ref2b));
             *zq = make_float2(e0, e1);
@@ -148,14 +152,18 @@ __device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live
             b.s_all += e1;
             a.ncand += e0 >= near_thr ? 1 : 0;
             b.ncand += e1 >= near_thr ? 1 : 0;
-        } else {
+        } else if (kMode == kPassFinal) {
             *zq = make_float2(w0, w1);
         }
     }
-    if (kExp) {
+    if (kMode == kPassExp) {
         a.best_w = fmaxf(a.best_w, w0);
         b.best_w = fmaxf(b.best_w, w1);
     } else {
+        if (kMode == kPassScout) {  // second-best weight seen by this lane (-inf for dead tail lanes)
+            a.s_all = fmaxf(a.s_all, fminf(w0, a.best_w));
+            b.s_all = fmaxf(b.s_all, fminf(w1, b.best_w));
+        }
         if (w0 > a.best_w) {  // strict: the earliest offset is kept
             a.best_w = w0;
             a.best_j = j;
@@ -167,7 +175,7 @@ __device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live
     }
 }
 
-template <int G, bool kExp>
+template <int G, int kMode>
 __device__ __forceinline__ void pair_pass_a(const float2* __restrict__ T2, const uint64_t* __restrict__ wp, int W, int lane,
                                             float2* __restrict__ zs, float refa, float refb, float near_thr, SeqAcc& a,
                                             SeqAcc& b) {
@@ -188,8 +196,8 @@ __device__ __forceinline__ void pair_pass_a(const float2* __restrict__ T2, const
         float w0, w1, w2, w3;
         pair_weights<G>(T2, vh1, vl1, w0, w1);
         pair_weights<G>(T2, vh2, vl2, w2, w3);
-        pair_finish<kExp, false>(w0, w1, j, true, zq, ref2a, ref2b, near_thr, a, b);
-        pair_finish<kExp, false>(w2, w3, j + 32, true, zq + 32, ref2a, ref2b, near_thr, a, b);
+        pair_finish<kMode, false>(w0, w1, j, true, zq, ref2a, ref2b, near_thr, a, b);
+        pair_finish<kMode, false>(w2, w3, j + 32, true, zq + 32, ref2a, ref2b, near_thr, a, b);
         zq += 64;
     }
     for (const int j_full = W & ~31; j < j_full; j += 32) {
@@ -197,13 +205,13 @@ __device__ __forceinline__ void pair_pass_a(const float2* __restrict__ T2, const
         uint32_t vh, vl;
         window_halves(hi, lo, lane, vh, vl);
         hi = lo;
-        pair_chunk<G, kExp, false>(T2, vh, vl, j, true, zq, ref2a, ref2b, near_thr, a, b);
+        pair_chunk<G, kMode, false>(T2, vh, vl, j, true, zq, ref2a, ref2b, near_thr, a, b);
         zq += 32;
     }
     if ((W & 31) != 0) {
         uint32_t vh, vl;
         window_halves(hi, *wq, lane, vh, vl);
-        pair_chunk<G, kExp, true>(T2, vh, vl, j, j < W, zq, ref2a, ref2b, near_thr, a, b);
+        pair_chunk<G, kMode, true>(T2, vh, vl, j, j < W, zq, ref2a, ref2b, near_thr, a, b);
     }
 }
 
@@ -503,15 +511,36 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     SeqAcc a = {-INFINITY, 0.f, 0.f, 0, 0, 0, false}, b = {-INFINITY, 0.f, 0.f, 0, 0, 0, false};
 
                     if (final_pass) {
-                        pair_pass_a<G, false>(T2, wp, W, lane, zs, 0.f, 0.f, 0.f, a, b);
-                        __syncwarp();
                         // ---- positions: per-sequence argmax, ties to the smallest offset (refine.hpp:311-316).
-                        // Windows within delta of the FP32 maximum are compared by their FP64 weights.
+                        // Windows within delta of the FP32 maximum are compared by their FP64 weights.  A scouting
+                        // sweep without stores settles the common case of a single window within delta (it IS the
+                        // argmax); only sequences with near-ties take the storing sweep and the FP64 comparison.
+                        a.s_all = -INFINITY, b.s_all = -INFINITY;
+                        pair_pass_a<G, kPassScout>(T2, wp, W, lane, zs, 0.f, 0.f, 0.f, a, b);
                         const float Mf0 = warp_max_f(a.best_w), Mf1 = warp_max_f(b.best_w);
                         if (!(Mf0 > -INFINITY) || !(Mf0 < INFINITY)) iscal[2] = 1;
                         if (!(Mf1 > -INFINITY) || !(Mf1 < INFINITY)) iscal[6] = 1;
-                        {
-                            const float lim0 = Mf0 - (1e-3f + 1e-5f * fabsf(Mf0)), lim1 = Mf1 - (1e-3f + 1e-5f * fabsf(Mf1));
+                        float lim0 = Mf0 - (1e-3f + 1e-5f * fabsf(Mf0)), lim1 = Mf1 - (1e-3f + 1e-5f * fabsf(Mf1));
+                        const unsigned near0 = __ballot_sync(0xffffffffu, a.best_w >= lim0), near1 = __ballot_sync(0xffffffffu, b.best_w >= lim1);
+                        const bool uniq0 = __popc(near0) == 1 && !__any_sync(0xffffffffu, a.s_all >= lim0);
+                        const bool uniq1 = __popc(near1) == 1 && !__any_sync(0xffffffffu, b.s_all >= lim1);
+                        if (uniq0) {  // as if the list held exactly this window
+                            a.nnear = -1;
+                            a.best_j = __shfl_sync(0xffffffffu, a.best_j, __ffs(near0) - 1);
+                        }
+                        if (uniq1) {
+                            b.nnear = -1;
+                            b.best_j = __shfl_sync(0xffffffffu, b.best_j, __ffs(near1) - 1);
+                        }
+                        if (!(uniq0 && uniq1)) {
+                            const int keep_j0 = a.best_j, keep_j1 = b.best_j;
+                            a.best_w = -INFINITY, b.best_w = -INFINITY;
+                            pair_pass_a<G, kPassFinal>(T2, wp, W, lane, zs, 0.f, 0.f, 0.f, a, b);
+                            __syncwarp();
+                            if (uniq0) a.best_j = keep_j0;
+                            if (uniq1) b.best_j = keep_j1;
+                            if (uniq0) lim0 = INFINITY;  // already settled: list nothing
+                            if (uniq1) lim1 = INFINITY;
                             for (int c = 0; c < chunks; ++c) {
                                 const int j = (c << 5) + lane;
                                 bool k0 = false, k1 = false;
@@ -530,7 +559,9 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                             const SeqAcc s = bb ? b : a;
                             const uint16_t* my_near = near_a + bb * kPairNearCap;
                             int arg;
-                            if (!s.overflow) {
+                            if (s.nnear < 0) {
+                                arg = s.best_j;  // the only window within delta of the maximum
+                            } else if (!s.overflow) {
                                 const double* D = D64 + bb * TH;
                                 double bw = -INFINITY;
                                 int bj = 0x7fffffff;
@@ -584,7 +615,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     float ref1 = first ? ubs[1] : mprev[tpad + i];
                     // iteration 0 lists nothing on the way (its reference is far above the maximum): rebuilt below
                     const float near_thr = first ? INFINITY : fast_ex2((p.log_z_eps - kNearMargin) * kLog2e);
-                    pair_pass_a<G, true>(T2, wp, W, lane, zs, ref0, ref1, near_thr, a, b);
+                    pair_pass_a<G, kPassExp>(T2, wp, W, lane, zs, ref0, ref1, near_thr, a, b);
                     float M0 = 0.f, M1 = 0.f, inv0 = 0.f, inv1 = 0.f;
                     // the FP64 pass is skipped in the last iteration of the budget: its likelihood can no longer
                     // stop the loop (refine.hpp:296-304), so no near list is needed there
