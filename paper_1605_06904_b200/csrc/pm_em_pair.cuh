@@ -258,6 +258,29 @@ __device__ __forceinline__ void pair_detect(float* __restrict__ zb, int W, int l
     }
 }
 
+// pair_detect<false> for both buckets in one sweep over the interleaved values (a bucket whose flag is off is
+// left untouched)
+__device__ __forceinline__ void pair_detect_both(const float2* __restrict__ zs, int W, int lane, bool on_a, bool on_b,
+                                                 float thr_a, float thr_b, SeqAcc& a, SeqAcc& b,
+                                                 uint16_t* __restrict__ near_a, uint16_t* __restrict__ near_b) {
+    float far_a = 0.f, far_b = 0.f;
+    int n_a = 0, n_b = 0;
+    bool ov_a = !on_a, ov_b = !on_b;  // an overflowed list takes no more entries
+    const int chunks = (W + 31) >> 5;
+    for (int c = 0; c < chunks; ++c) {
+        const int j = (c << 5) + lane;
+        float2 e = make_float2(0.f, 0.f);
+        if (j < W) e = zs[j];
+        const bool k_a = j < W && e.x >= thr_a, k_b = j < W && e.y >= thr_b;
+        far_a += k_a ? 0.f : e.x;
+        far_b += k_b ? 0.f : e.y;
+        near_push16(__ballot_sync(0xffffffffu, k_a), k_a, lane, j, near_a, n_a, ov_a);
+        near_push16(__ballot_sync(0xffffffffu, k_b), k_b, lane, j, near_b, n_b, ov_b);
+    }
+    if (on_a) a.s_far = far_a, a.nnear = n_a, a.overflow = ov_a;
+    if (on_b) b.s_far = far_b, b.nnear = n_b, b.overflow = ov_b;
+}
+
 // After pass A of one sequence, one bucket: settle the reference maximum, the near list and the normaliser.
 // Returns 1/total; ref is updated when the fallback re-based the stored values on M.  The near list (windows
 // with e >= near_e, i.e. within log_z_eps of the maximum) is built by a second light sweep over the stored
@@ -292,12 +315,8 @@ __device__ __forceinline__ float pair_settle(const float* __restrict__ Tb, const
         a.overflow = true;
         if (want_near) {
             // the count is an upper bound of the list length unless the maximum dropped below the margin
-            if (force_rebuild || M < ref - kNearMargin || n_cand <= kPairNearCap) {
-                __syncwarp();
-                float ignore = 0.f;
-                a.s_far = 0.f, a.nnear = 0, a.overflow = false;
-                pair_detect<false>(zb, W, lane, M, near_e, ignore, a.s_far, my_near, a.nnear, a.overflow);
-            }
+            // the sweep that builds the list is left to the caller, who runs it once for both buckets
+            if (force_rebuild || M < ref - kNearMargin || n_cand <= kPairNearCap) a.nnear = -2;
         }
     }
     if (!(total > 0.f)) *bad = 1;
@@ -616,7 +635,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     // iteration 0 lists nothing on the way (its reference is far above the maximum): rebuilt below
                     const float near_thr = first ? INFINITY : fast_ex2((p.log_z_eps - kNearMargin) * kLog2e);
                     pair_pass_a<G, kPassExp>(T2, wp, W, lane, zs, ref0, ref1, near_thr, a, b);
-                    float M0 = 0.f, M1 = 0.f, inv0 = 0.f, inv1 = 0.f;
+                    float M0 = 0.f, M1 = 0.f, inv0 = 0.f, inv1 = 0.f, ne0 = 0.f, ne1 = 0.f;
                     // the FP64 pass is skipped in the last iteration of the budget: its likelihood can no longer
                     // stop the loop (refine.hpp:296-304), so no near list is needed there
                     const bool want_near = iterations + 1 < p.max_iters;
@@ -639,12 +658,16 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                         __syncwarp();  // every lane has read this sequence's previous maximum
                         if (lane == 0) mprev[bb * tpad + i] = M;
                         if (bb) {
-                            b = s, ref1 = ref, M1 = M, inv1 = inv;
+                            b = s, ref1 = ref, M1 = M, inv1 = inv, ne1 = ne;
                         } else {
-                            a = s, ref0 = ref, M0 = M, inv0 = inv;
+                            a = s, ref0 = ref, M0 = M, inv0 = inv, ne0 = ne;
                         }
                     }
                     __syncwarp();
+                    if (a.nnear == -2 || b.nnear == -2) {
+                        pair_detect_both(zs, W, lane, a.nnear == -2, b.nnear == -2, ne0, ne1, a, b, near_a, near_b);
+                        __syncwarp();
+                    }
                     // pass C: z_j = e_j / sum, both buckets
                     {
                         int j = lane;
