@@ -391,6 +391,11 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         smeta[4 * i + 2] = x.seq_zoff[i];
         smeta[4 * i + 3] = static_cast<int>(p.win_off[i]);  // first flat l-mer index of the sequence
     }
+    // Slots that are not window starts (front pad, the last l-1 bases of a sequence, balancing gaps) must read as
+    // zero in the M-step gather and are never written by a sweep.  With a single tile the layout never changes:
+    // zero the buffer once; with several tiles the buffer is re-laid out per tile and those slots are re-zeroed.
+    const bool rezero = x.n_tiles > 1;
+    for (int k = threadIdx.x; k < x.zcap; k += blockDim.x) zbuf[k] = make_float2(0.f, 0.f);
     __syncthreads();
     mbar_wait(&mbar[0], 0);
 
@@ -511,8 +516,10 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     const int w = threadIdx.x - 32;
                     wrow[w] = static_cast<int>(static_cast<long long>(x.tile_group_off[tile_i * 17 + 16]) * w / nwarps);
                 }
-                for (int k = threadIdx.x, k_end = smeta[4 * tile.seq_begin + 2]; k < k_end; k += blockDim.x)
-                    zbuf[k] = make_float2(0.f, 0.f);  // front pad (dummy lanes of the class rows read it)
+                if (rezero) {  // front pad (dummy lanes of the class rows read it)
+                    for (int k = threadIdx.x, k_end = smeta[4 * tile.seq_begin + 2]; k < k_end; k += blockDim.x)
+                        zbuf[k] = make_float2(0.f, 0.f);
+                }
                 // ================= E-step: warp per sequence of the tile =================
                 for (int i = tile.seq_begin + warp; i < tile.seq_end; i += nwarps) {
                     const uint64_t* __restrict__ wp = wstage + smeta[4 * i];
@@ -521,7 +528,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     const int chunks = (W + 31) >> 5;
                     float2* zs = zbuf + zo;
                     float* zb0 = zf + 2 * zo;
-                    {
+                    if (rezero) {
                         // slots that are not window starts read as zero in the M-step gather
                         const int z_end = (i + 1 < tile.seq_end ? smeta[4 * (i + 1) + 2] : tile.zlen) - zo;
                         #pragma unroll 1
