@@ -347,7 +347,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "stage_ms_per_step": {name: stage[i] / args.steps for i, name in
                               enumerate(["keys", "sort", "enrich", "em", "reduce", "score", "upload", "d2h"])},
-        "roofline": {"bound": "fp32", "kernel": "em_refine_pair_kernel" if t <= 64 else "em_refine_smem_kernel",
+        "roofline": {"bound": "fp32", "kernel": "em_refine_pair_kernel",
                      "achieved": achieved_tflops, "peak": fp32_peak_tflops,
                      "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
                      # dram__bytes_read+write of one launch from the ncu --set full capture in profiles/ (C1 only):

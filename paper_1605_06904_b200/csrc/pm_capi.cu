@@ -89,6 +89,7 @@ struct pm_ctx {
     int pair_cfg_l = -1, pair_cfg_threads = 0, pair_cfg_per_sm = 0;  // same for the two-bucket kernel
     size_t pair_cfg_smem = 0;
     int32_t max_seq_len = 0;
+    int max_tile_seqs = 0;  // most sequences any tile of the class-group index holds
     // host staging of the class-group index: lives in the context so the async uploads need no sync of their own
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
@@ -237,6 +238,15 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         const long v = std::atol(env);
         if (v >= 256 && v <= 48000) cap = v;
     }
+    // Sequences per tile: at most kPairMaxSeqs (the pair kernel keeps a tile's metadata in shared memory), and for
+    // multi-tile sets a multiple of the ten warps of a CTA when ten or more fit (warp per sequence: a tile of
+    // twelve leaves eight warps idle for half of the E-step).
+    int tile_seq_cap = k::kPairMaxSeqs;
+    if (single > 13500) {
+        const int64_t mean_len = std::max<int64_t>(1, total / t) + 32;
+        const int64_t fit = std::max<int64_t>(1, (cap - k::kZPad) / mean_len);
+        if (fit >= 10) tile_seq_cap = static_cast<int>(std::min<int64_t>(k::kPairMaxSeqs, fit / 10 * 10));
+    }
     auto code = [](char ch) { return (static_cast<unsigned char>(ch) >> 1) & 3; };
     std::vector<k::TileDesc>& tiles = c->h_tiles;
     std::vector<int>& zoff = c->h_zoff;
@@ -264,6 +274,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         while (i < t) {
             const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
             if (cursor + 31 + n > cap) break;
+            if (i - tile.seq_begin >= tile_seq_cap) break;
             const char* sq = bases + rel[static_cast<size_t>(i)];
             // the slack before this sequence (0..31 slots) is chosen greedily so that, per class, the
             // positions spread evenly over the 32 address residues (rows of a class = its fullest residue)
@@ -340,6 +351,8 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     PM_TRY(h2d(c, c->d_tiles, tiles.data(), sizeof(k::TileDesc) * tiles.size()));
     // no sync here: the staging vectors belong to the context and pm_ctx_set_sequences synchronises once at its end
     c->zlen = zcap;
+    c->max_tile_seqs = 0;
+    for (const k::TileDesc& td : tiles) c->max_tile_seqs = std::max(c->max_tile_seqs, td.seq_end - td.seq_begin);
     c->tile_words = wcap;
     c->n_tiles = static_cast<int>(tiles.size());
     c->total_groups = static_cast<int>(live_rows);
@@ -630,8 +643,10 @@ EmSmemKernel em_pair_kernel_for(int l) {
 }
 
 // must mirror the carve-up at the top of em_refine_pair_kernel
-size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_words) {
-    const size_t TH = 4 * (static_cast<size_t>(l) + 1), tpad = (static_cast<size_t>(t) + 1) & ~static_cast<size_t>(1);
+size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_words, bool big) {
+    // big: tpad = sequences per tile (metadata only), two word stages of total_words (= largest tile) each
+    const size_t TH = 4 * (static_cast<size_t>(l) + 1);
+    const size_t tpad = big ? static_cast<size_t>(k::kPairMaxSeqs) : ((static_cast<size_t>(t) + 1) & ~static_cast<size_t>(1));
     const size_t NV = 2 * G <= 16 ? 16 : 32;
     size_t b = 0;
     b += (2 * TH + 2 * TH + 2 * TH + 2 * static_cast<size_t>(nwarps) + 12) * 8;              // thd, D64, L64, llpart, dscal
@@ -642,8 +657,8 @@ size_t em_pair_smem_bytes(int nwarps, int G, int l, int zcap, int t, int total_w
     b += static_cast<size_t>(nwarps) * 2 * k::kPairNearCap * 2;                              // near_j
     b = (b + 15) & ~static_cast<size_t>(15);
     b += ((static_cast<size_t>(zcap) + 1) & ~static_cast<size_t>(1)) * 8;                    // zbuf (float2), 16-byte multiple
-    b += static_cast<size_t>(total_words) * 8;                                               // TMA word stage
-    b += 16;                                                                                 // mbarrier
+    b += static_cast<size_t>(total_words) * 8 * (big ? 2 : 1);                               // TMA word stage(s)
+    b += 16;                                                                                 // mbarriers
     return b + 16;
 }
 
@@ -758,13 +773,15 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
     p.phase_clk = d_scal + 8;
 
-    if (c->zlen > 0 && c->t <= k::kPairMaxSeqs && c->total_words <= k::kPairMaxWords &&
-        c->max_seq_len < 65536 && em_pair_enabled()) {
-        // two buckets per CTA in lockstep (pm_em_pair.cuh): every t=20 configuration
+    if (c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs && em_pair_enabled()) {
+        // two buckets per CTA in lockstep (pm_em_pair.cuh).  Small sets keep all per-sequence state and the whole
+        // packed set in shared memory; large sets walk the tiles with per-tile state (C5: 1,000 tiles of 10).
+        const bool big = c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords;
         const int G = (l + 1) / 2;
-        const int nwarps = em_pair_warps_for(c->t);
+        const int nwarps = em_pair_warps_for(big ? std::min(c->max_tile_seqs, 10) : c->t);
         const int threads = nwarps * 32;
-        const size_t smem = em_pair_smem_bytes(nwarps, G, l, c->zlen, c->t, static_cast<int>(c->total_words));
+        const int stage_words = big ? c->tile_words : static_cast<int>(c->total_words);
+        const size_t smem = em_pair_smem_bytes(nwarps, G, l, c->zlen, c->t, stage_words, big);
         if (smem <= 227 * 1024) {
             EmSmemKernel kern = em_pair_kernel_for(l);
             int per_sm = 0;
@@ -792,9 +809,10 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
                 x.cls_entries = c->d_cls_entries;
                 x.tile_group_off = c->d_cls_group_off;
                 x.seq_zoff = c->d_seq_zoff;
-                x.mprev_g = nullptr;
+                x.mprev_g = nullptr;  // non-null selects the large-set path
                 x.zcap = c->zlen;
-                x.wcap = static_cast<int>(c->total_words);
+                x.wcap = stage_words;
+                if (big) PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * 2 * static_cast<size_t>(c->t), &x.mprev_g));
                 kern<<<grid, threads, smem, c->stream>>>(p, x);
                 return check_launch(c, "em_refine_pair");
             }

@@ -23,8 +23,9 @@ namespace pm {
 namespace k {
 
 constexpr int kPairMaxWarps = 10;  // 12 was measured no faster and caps the kernel at 80 registers
-constexpr int kPairMaxSeqs = 64;     // per-sequence state (previous maxima, metadata) lives in shared memory
-constexpr int kPairMaxWords = 2048;  // packed words of the whole set, staged once per CTA by one TMA bulk copy
+constexpr int kPairMaxSeqs = 64;     // small sets: per-sequence state (previous maxima, metadata) lives in shared memory;
+                                     // large sets: at most this many sequences per tile
+constexpr int kPairMaxWords = 2048;  // small sets: packed words of the whole set, staged once per CTA by one TMA bulk copy
 constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
 
 // The per-sequence bookkeeping around the two hot loops is large straight-line code that every warp walks
@@ -349,7 +350,12 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int l = p.l, t = p.t;
     const int TH = 4 * (l + 1);
-    const int tpad = (t + 1) & ~1;
+    // Small sets (every t=20 configuration): metadata and previous maxima of all sequences in shared memory, the
+    // whole packed set staged once.  Large sets: the same kernel walks the tiles with the metadata of the
+    // current tile only, the previous maxima in a per-CTA global scratch and the packed words of each tile
+    // double-buffered by TMA (the next tile's words arrive while the current tile is processed).
+    const bool big = x.mprev_g != nullptr;
+    const int tpad = big ? kPairMaxSeqs : ((t + 1) & ~1);
     constexpr int NV = 2 * G <= 16 ? 16 : 32;  // values per class flush (2 buckets x G column pairs, padded)
 
     // ---- shared memory carve-up (mirrored by em_pair_smem_bytes on the host)
@@ -361,8 +367,8 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
     float2* T2 = reinterpret_cast<float2*>(dscal + 12);       // [G][16] {bucket 0, bucket 1}
     float* Cq = reinterpret_cast<float*>(T2 + 16 * G);        // [2][16][G] class sums
     float* cpart = Cq + 32 * G;                               // [16 + nwarps][NV] slot = warp + class
-    float* mprev = cpart + (16 + nwarps) * NV;                // [2][tpad] previous per-sequence maxima
-    float* ubs = mprev + 2 * tpad;                            // [2] upper bound of any window weight (+2 pad)
+    float* mprev_s = cpart + (16 + nwarps) * NV;              // [2][tpad] previous per-sequence maxima (small sets)
+    float* ubs = mprev_s + 2 * tpad;                          // [2] upper bound of any window weight (+2 pad)
     int* prof = reinterpret_cast<int*>(ubs + 4);              // [2][128]
     int* iscal = prof + 256;                                  // [2][4]: [0] stop [1] score [2] bad [3] iterations
     int* s_off = iscal + 8;                                   // [17] first row of each class (+3 pad)
@@ -375,34 +381,47 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
     const unsigned int z_off = (static_cast<unsigned int>(reinterpret_cast<unsigned char*>(near_j + nwarps * 2 * kPairNearCap) - smem_raw) + 15u) & ~15u;
     float2* zbuf = reinterpret_cast<float2*>(smem_raw + z_off);
     uint64_t* wstage = reinterpret_cast<uint64_t*>(smem_raw + z_off + static_cast<unsigned int>((x.zcap + 1) & ~1) * 8u);
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wstage + x.wcap);
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wstage + static_cast<size_t>(x.wcap) * (big ? 2 : 1));
+    float* mprev = big ? x.mprev_g + static_cast<size_t>(blockIdx.x) * 2 * t : mprev_s;
+    const int mstride = big ? t : tpad;  // bucket 1's maxima follow bucket 0's
+    unsigned int visit = 0;              // tiles visited (large sets): stage = visit & 1, parity = (visit >> 1) & 1
 
     // ---- packed words of the whole set: one TMA bulk copy per CTA, resident for every bucket
     const int64_t word0 = x.tiles[0].word_begin;
     if (threadIdx.x == 0) {
         mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(&mbar[0], static_cast<unsigned>(x.wcap) * 8u);
-        tma_load_1d(wstage, p.words + word0, static_cast<unsigned>(x.wcap) * 8u, &mbar[0]);
+        // small sets: the whole set; large sets: the first tile (wcap = the largest tile)
+        const unsigned bytes = static_cast<unsigned>(big ? x.tiles[0].n_words : x.wcap) * 8u;
+        mbar_expect_tx(&mbar[0], bytes);
+        tma_load_1d(wstage, p.words + word0, bytes, &mbar[0]);
     }
-    for (int i = threadIdx.x; i < t; i += blockDim.x) {
-        smeta[4 * i + 0] = static_cast<int>(p.word_off[i] - word0);
-        smeta[4 * i + 1] = p.seq_len[i] - l + 1;
-        smeta[4 * i + 2] = x.seq_zoff[i];
-        smeta[4 * i + 3] = static_cast<int>(p.win_off[i]);  // first flat l-mer index of the sequence
+    if (!big) {
+        for (int i = threadIdx.x; i < t; i += blockDim.x) {
+            smeta[4 * i + 0] = static_cast<int>(p.word_off[i] - word0);
+            smeta[4 * i + 1] = p.seq_len[i] - l + 1;
+            smeta[4 * i + 2] = x.seq_zoff[i];
+            smeta[4 * i + 3] = static_cast<int>(p.win_off[i]);  // first flat l-mer index of the sequence
+        }
     }
     // Slots that are not window starts (front pad, the last l-1 bases of a sequence, balancing gaps) must read as
     // zero in the M-step gather and are never written by a sweep.  With a single tile the layout never changes:
     // zero the buffer once; with several tiles the buffer is re-laid out per tile and those slots are re-zeroed.
     const bool rezero = x.n_tiles > 1;
     for (int k = threadIdx.x; k < x.zcap; k += blockDim.x) zbuf[k] = make_float2(0.f, 0.f);
-    __syncthreads();
-    mbar_wait(&mbar[0], 0);
-
-    double sum_logw = 0.0;  // sum_i log W_i, used by the two threads that close an iteration
-    if (threadIdx.x >= blockDim.x - 2) {
-        for (int i = 0; i < t; ++i) sum_logw += p.seq_logw[i];
+    // sum_i log W_i, used by the two threads that close an iteration: block-wide sum, fixed order
+    double sum_logw = 0.0;
+    {
+        double part = 0.0;
+        for (int i = threadIdx.x; i < t; i += blockDim.x) part += p.seq_logw[i];
+        part = warp_sum_d(part);
+        if (lane == 0) llpart[warp] = part;
     }
+    __syncthreads();
+    for (int w = 0; w < nwarps; ++w) sum_logw += llpart[w];
+    if (!big) mbar_wait(&mbar[0], 0);
+    __syncthreads();  // llpart is reused by the iterations
     uint16_t* near_a = near_j + (warp * 2 + 0) * kPairNearCap;
     uint16_t* near_b = near_j + (warp * 2 + 1) * kPairNearCap;
     const int colshift = 62 - 2 * lane;
@@ -434,12 +453,18 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         for (unsigned int m = threadIdx.x; m < wd0.count + wd1.count; m += blockDim.x) {
             const int b = m >= wd0.count;
             const int64_t f = b ? p.members[wd1.mem_begin + (m - wd0.count)] : p.members[wd0.mem_begin + m];
-            int i = 0;
-            for (int hi = t; hi - i > 1;) {  // owner of flat l-mer index f: largest i with win_off[i] <= f
-                const int mid = (i + hi) >> 1;
-                if (smeta[4 * mid + 3] <= f) i = mid; else hi = mid;
+            uint64_t v;
+            if (!big) {
+                int i = 0;
+                for (int hi = t; hi - i > 1;) {  // owner of flat l-mer index f: largest i with win_off[i] <= f
+                    const int mid = (i + hi) >> 1;
+                    if (smeta[4 * mid + 3] <= f) i = mid; else hi = mid;
+                }
+                v = load_window(wstage + smeta[4 * i], f - smeta[4 * i + 3]);
+            } else {
+                const int i = seq_of_flat(p.win_off, t, f);
+                v = load_window(p.words + p.word_off[i], f - p.win_off[i]);
             }
-            const uint64_t v = load_window(wstage + smeta[4 * i], f - smeta[4 * i + 3]);
             #pragma unroll 1
             for (int c = 0; c < l; ++c) atomicAdd(&prof[b * 128 + c * 4 + (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u)], 1);
         }
@@ -516,21 +541,48 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     const int w = threadIdx.x - 32;
                     wrow[w] = static_cast<int>(static_cast<long long>(x.tile_group_off[tile_i * 17 + 16]) * w / nwarps);
                 }
+                const int sbase = big ? tile.seq_begin : 0;  // smeta holds sequence i at row i - sbase
+                const uint64_t* __restrict__ wtile = wstage;
+                if (big) {
+                    for (int k = threadIdx.x; k < tile.seq_end - tile.seq_begin; k += blockDim.x) {
+                        const int i = tile.seq_begin + k;
+                        smeta[4 * k + 0] = static_cast<int>(p.word_off[i] - tile.word_begin);
+                        smeta[4 * k + 1] = p.seq_len[i] - l + 1;
+                        smeta[4 * k + 2] = x.seq_zoff[i];
+                    }
+                    if (x.n_tiles > 1) {
+                        wtile = wstage + static_cast<size_t>(x.wcap) * (visit & 1);
+                        if (threadIdx.x == 0) {  // prefetch the next tile of the cyclic walk into the other stage
+                            const TileDesc nt = x.tiles[tile_i + 1 < x.n_tiles ? tile_i + 1 : 0];
+                            unsigned long long* nb = &mbar[(visit + 1) & 1];
+                            mbar_expect_tx(nb, static_cast<unsigned>(nt.n_words) * 8u);
+                            tma_load_1d(wstage + static_cast<size_t>(x.wcap) * ((visit + 1) & 1), p.words + nt.word_begin,
+                                        static_cast<unsigned>(nt.n_words) * 8u, nb);
+                        }
+                        mbar_wait(&mbar[visit & 1], (visit >> 1) & 1);
+                        ++visit;
+                    } else if (visit == 0) {
+                        mbar_wait(&mbar[0], 0);
+                        ++visit;
+                    }
+                    __syncthreads();  // metadata of the tile visible to every warp
+                }
                 if (rezero) {  // front pad (dummy lanes of the class rows read it)
-                    for (int k = threadIdx.x, k_end = smeta[4 * tile.seq_begin + 2]; k < k_end; k += blockDim.x)
+                    for (int k = threadIdx.x, k_end = smeta[4 * (tile.seq_begin - sbase) + 2]; k < k_end; k += blockDim.x)
                         zbuf[k] = make_float2(0.f, 0.f);
                 }
                 // ================= E-step: warp per sequence of the tile =================
                 for (int i = tile.seq_begin + warp; i < tile.seq_end; i += nwarps) {
-                    const uint64_t* __restrict__ wp = wstage + smeta[4 * i];
-                    const int W = smeta[4 * i + 1];
-                    const int zo = smeta[4 * i + 2];
+                    const int si = i - sbase;
+                    const uint64_t* __restrict__ wp = wtile + smeta[4 * si];
+                    const int W = smeta[4 * si + 1];
+                    const int zo = smeta[4 * si + 2];
                     const int chunks = (W + 31) >> 5;
                     float2* zs = zbuf + zo;
                     float* zb0 = zf + 2 * zo;
                     if (rezero) {
                         // slots that are not window starts read as zero in the M-step gather
-                        const int z_end = (i + 1 < tile.seq_end ? smeta[4 * (i + 1) + 2] : tile.zlen) - zo;
+                        const int z_end = (i + 1 < tile.seq_end ? smeta[4 * (si + 1) + 2] : tile.zlen) - zo;
                         #pragma unroll 1
                         for (int k = W + lane; k < z_end; k += 32) zs[k] = make_float2(0.f, 0.f);
                     }
@@ -638,7 +690,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     constexpr float kNearMargin = 4.f;
                     const bool first = iterations == 0;
                     float ref0 = first ? ubs[0] : mprev[i];
-                    float ref1 = first ? ubs[1] : mprev[tpad + i];
+                    float ref1 = first ? ubs[1] : mprev[mstride + i];
                     // iteration 0 lists nothing on the way (its reference is far above the maximum): rebuilt below
                     const float near_thr = first ? INFINITY : fast_ex2((p.log_z_eps - kNearMargin) * kLog2e);
                     pair_pass_a<G, kPassExp>(T2, wp, W, lane, zs, ref0, ref1, near_thr, a, b);
@@ -663,7 +715,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                                          bb ? tot1 : tot0, bb ? nc1 : nc0, ne, p.log_z_eps, first, want_near,
                                                          &iscal[bb * 4 + 2]);
                         __syncwarp();  // every lane has read this sequence's previous maximum
-                        if (lane == 0) mprev[bb * tpad + i] = M;
+                        if (lane == 0) mprev[bb * mstride + i] = M;
                         if (bb) {
                             b = s, ref1 = ref, M1 = M, inv1 = inv, ne1 = ne;
                         } else {
@@ -948,6 +1000,14 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
             }
         }
         PM_PHASE(6);  // score, consensus, outputs
+    }
+    // no bulk copy may still be in flight into this CTA's shared memory when it exits
+    if (big) {
+        if (x.n_tiles > 1) {
+            mbar_wait(&mbar[visit & 1], (visit >> 1) & 1);
+        } else if (visit == 0) {
+            mbar_wait(&mbar[0], 0);
+        }
     }
 }
 
