@@ -46,6 +46,34 @@ __device__ __forceinline__ double window_weight_rolled(const double* __restrict_
     return w0 + w1;
 }
 
+// Packed FP32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2, one instruction for the two buckets of a pair; the
+// results are the same round-to-nearest values as two scalar instructions).
+__device__ __forceinline__ unsigned long long f2_pack(float2 v) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(d);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(d);
+}
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+    return f2_unpack(d);
+}
+
 struct SeqAcc {
     float best_w, s_all, s_far;  // s_all doubles as the lane's second-best weight in the scouting final sweep
     int best_j, nnear, ncand;
@@ -104,10 +132,7 @@ __device__ __forceinline__ void pair_weights(const float2* __restrict__ T2, uint
 #pragma unroll
     for (int s = 1; s < G; s <<= 1) {
 #pragma unroll
-        for (int g = 0; g + s < G; g += 2 * s) {
-            t[g].x += t[g + s].x;
-            t[g].y += t[g + s].y;
-        }
+        for (int g = 0; g + s < G; g += 2 * s) t[g] = f2_add(t[g], t[g + s]);
     }
     w0 = t[0].x;
     w1 = t[0].y;
@@ -146,8 +171,9 @@ __device__ __forceinline__ void pair_finish(float w0, float w1, int j, bool live
                                             float ref2b, float near_thr, SeqAcc& a, SeqAcc& b) {
     if (!kTail || live) {
         if (kMode == kPassExp) {
-            const float e0 = fast_ex2(fmaf(w0, kLog2e, -ref2a));
-            const float e1 = fast_ex2(fmaf(w1, kLog2e, -ref2b));
+            const float2 arg = f2_fma(make_float2(w0, w1), make_float2(kLog2e, kLog2e), make_float2(-ref2a, -ref2b));
+            const float e0 = fast_ex2(arg.x);
+            const float e1 = fast_ex2(arg.y);
             *zq = make_float2(e0, e1);
             a.s_all += e0;
             b.s_all += e1;
@@ -729,19 +755,14 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     }
                     // pass C: z_j = e_j / sum, both buckets
                     {
+                        const float2 inv2 = make_float2(inv0, inv1);
                         int j = lane;
                         for (const int j4 = W - 96; j < j4; j += 128) {  // four chunks per trip: loads first, then stores
-                            float2 e0 = zs[j], e1 = zs[j + 32], e2 = zs[j + 64], e3 = zs[j + 96];
-                            e0.x *= inv0, e0.y *= inv1, e1.x *= inv0, e1.y *= inv1;
-                            e2.x *= inv0, e2.y *= inv1, e3.x *= inv0, e3.y *= inv1;
-                            zs[j] = e0, zs[j + 32] = e1, zs[j + 64] = e2, zs[j + 96] = e3;
+                            const float2 e0 = zs[j], e1 = zs[j + 32], e2 = zs[j + 64], e3 = zs[j + 96];
+                            zs[j] = f2_mul(e0, inv2), zs[j + 32] = f2_mul(e1, inv2);
+                            zs[j + 64] = f2_mul(e2, inv2), zs[j + 96] = f2_mul(e3, inv2);
                         }
-                        for (; j < W; j += 32) {
-                            float2 e = zs[j];
-                            e.x *= inv0;
-                            e.y *= inv1;
-                            zs[j] = e;
-                        }
+                        for (; j < W; j += 32) zs[j] = f2_mul(zs[j], inv2);
                     }
                     __syncwarp();
                     // ---- log sum_j exp(w_j) per bucket; the FP32 form needs log(1/total): one logf for both buckets
@@ -798,9 +819,9 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     for (int q = 0; q < 16; ++q) {
                         const int ra = max(item_lo, s_off[q]), rb = min(item_hi, s_off[q + 1]);
                         if (ra >= rb) continue;  // this warp owns no row of class q
-                        float acc[NV];
+                        float2 acc2[G];  // {bucket 0, bucket 1} per column pair: one FADD2 per gathered slot
 #pragma unroll
-                        for (int g = 0; g < NV; ++g) acc[g] = 0.f;
+                        for (int g = 0; g < G; ++g) acc2[g] = make_float2(0.f, 0.f);
                         // rows are padded at the end of the table: the two-ahead prefetch may run past rb
                         const uint16_t* __restrict__ ent = rows + static_cast<size_t>(ra) * 32;
                         int pos = ent[0], pos1 = ent[32];
@@ -809,13 +830,17 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                             const int pos2 = ent[32];
                             const float2* zp = zbuf + pos;
 #pragma unroll
-                            for (int g = 0; g < G; ++g) {
-                                const float2 v = zp[-2 * g];
-                                acc[g] += v.x;
-                                acc[G + g] += v.y;
-                            }
+                            for (int g = 0; g < G; ++g) acc2[g] = f2_add(acc2[g], zp[-2 * g]);
                             pos = pos1;
                             pos1 = pos2;
+                        }
+                        float acc[NV];
+#pragma unroll
+                        for (int g = 0; g < NV; ++g) acc[g] = 0.f;
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            acc[g] = acc2[g].x;
+                            acc[G + g] = acc2[g].y;
                         }
                         const float sum = warp_transpose_sum<NV>(acc, lane);
                         // lane L holds value (L*NV)>>5: value index v -> bucket v / G, pair v % G
