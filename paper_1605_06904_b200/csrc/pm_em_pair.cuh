@@ -1,5 +1,6 @@
-// pm_em_pair.cuh — EM refinement, TWO enriched buckets per CTA in lockstep (every t <= 64 config whose packed
-// words fit one 16 KB TMA stage: all t=20 configs of BASELINE.json).
+// pm_em_pair.cuh — EM refinement, TWO enriched buckets per CTA in lockstep: the EM kernel of every set whose
+// sequences fit a tile (small sets such as the t=20 configurations of BASELINE.json keep all per-sequence state
+// and the whole packed set in shared memory; large sets walk the tiles, see `big` below).
 //
 // Same algorithm, precision scheme and tile/class-group index as pm_em_smem.cuh (refine.hpp:90-326); what
 // changes is that everything that depends on the SEQUENCE SET only is done once for two buckets:
@@ -9,9 +10,11 @@
 //     the base position) is loaded once and each LDS.64 of the gather feeds both buckets' accumulators
 //     (rows built for distinct slots mod 32 are also conflict-free for 8-byte slots: each half-warp covers
 //     the 32 banks exactly once);
+//   * the arithmetic on the two buckets' values uses the packed FP32x2 instructions of sm_100 (FADD2, FMUL2,
+//     FFMA2): one instruction per pair, same round-to-nearest results;
 //   * loop control, prefetch of the class rows, sequence metadata.
-// Instruction count per bucket drops ~2x against the one-bucket kernel; shared-memory wavefronts per bucket
-// stay the same (8 per 32 windows in the E-step, 8 per class row in the M-step), which is the bound.
+// Instruction count per bucket is less than half of the one-bucket kernel's; shared-memory wavefronts per
+// bucket stay the same (8 per 32 windows in the E-step, 8 per class row in the M-step), which is the bound.
 //
 // Buckets of a pair iterate in lockstep.  A bucket whose likelihood gain fell below tol (refine.hpp:300) is
 // frozen: its theta is no longer updated, the lockstep sweeps it still takes part in do not change any of

@@ -138,6 +138,26 @@ int main() {
         REQUIRE(throws<NoEnrichedBucketsError>([&] { run(config, seqs); }));
     }
     REQUIRE(throws<UnknownSymbolError>([] { SequenceSet({"ACGN"}); }));
+
+    // exact solvers (test_oracle.cpp): the median string of the worked example is its motif, and the duality
+    // best score = l*t - median distance (test_oracle.cpp:71-80) holds on a toy instance
+    {
+        const MedianStringResult med = median_string(seqs, 8);
+        REQUIRE(med.median == "ATGCAACT" && med.total_distance == 3);
+        REQUIRE(throws<SearchSpaceTooLargeError>([&] { median_string(seqs, 8, 1000); }));
+        const PlantedInstance toy = generate_planted(3, 12, 4, 1, 17);
+        const NaiveMfpResult naive = naive_mfp(toy.sequences, 4);
+        const MedianStringResult toy_med = median_string(toy.sequences, 4);
+        REQUIRE(naive.score == 4 * 3 - toy_med.total_distance);
+        REQUIRE(score(toy.sequences, naive.positions, 4) == naive.score);
+        REQUIRE(throws<SearchSpaceTooLargeError>([&] { naive_mfp(toy.sequences, 4, 10); }));
+        BenchConfig bench;
+        bench.instances = 3;
+        bench.run.s = 3;
+        const std::string tsv = benchmark(bench);
+        REQUIRE(tsv.rfind("instance\tseed\trun_score", 0) == 0);
+        REQUIRE(tsv.find("summary\t-\t-\t-\t-\t") != std::string::npos);
+    }
     std::printf("host_layer_test: all checks passed\n");
     return 0;
 }
