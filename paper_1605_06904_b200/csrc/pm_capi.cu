@@ -1697,6 +1697,16 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         std::vector<k::PlanProg> progs(static_cast<size_t>(n_plans));
         std::vector<int> plan_rc(static_cast<size_t>(n_plans), PM_OK);
         auto make_range = [&](int64_t a, int64_t b) {
+            if (cfg->forced_kept == nullptr && cfg->plans == nullptr) {
+                // the reference's stream, four trials' seed chains at a time (pm_host.cpp: trial_plans)
+                std::vector<int32_t> kept(static_cast<size_t>(b - a) * static_cast<size_t>(params.k));
+                const int rc = trial_plans(cfg->l, params.k, cfg->seed, first + a, static_cast<int>(b - a), kept.data());
+                for (int64_t i = a; i < b; ++i) {
+                    plan_rc[static_cast<size_t>(i)] = rc;
+                    if (rc == PM_OK) progs[static_cast<size_t>(i)] = make_prog(kept.data() + (i - a) * params.k, params.k);
+                }
+                return;
+            }
             std::vector<int32_t> mine(static_cast<size_t>(params.k));
             for (int64_t i = a; i < b; ++i) {
                 const int64_t trial = first + i;

@@ -79,6 +79,22 @@ public:
         return z;
     }
 
+    // advances the seed chains of four engines together up to word `upto` (independent recurrences: ILP)
+    static void extend4(LazyMt64& a, LazyMt64& b, LazyMt64& c, LazyMt64& d, int upto) {
+        upto = std::min(upto, kN - 1);
+        int f = std::max(std::max(a.filled_, b.filled_), std::max(c.filled_, d.filled_));
+        a.extend(f), b.extend(f), c.extend(f), d.extend(f);
+        for (; f < upto; ++f) {
+            const uint64_t pa = a.x_[f], pb = b.x_[f], pc = c.x_[f], pd = d.x_[f];
+            const uint64_t add = static_cast<uint64_t>(f + 1);
+            a.x_[f + 1] = 6364136223846793005ULL * (pa ^ (pa >> 62)) + add;
+            b.x_[f + 1] = 6364136223846793005ULL * (pb ^ (pb >> 62)) + add;
+            c.x_[f + 1] = 6364136223846793005ULL * (pc ^ (pc >> 62)) + add;
+            d.x_[f + 1] = 6364136223846793005ULL * (pd ^ (pd >> 62)) + add;
+        }
+        a.filled_ = b.filled_ = c.filled_ = d.filled_ = f;
+    }
+
 private:
     static constexpr int kN = 312, kM = 156;
     static constexpr uint64_t kUpper = ~0ULL << 31, kLower = (1ULL << 31) - 1ULL;
@@ -140,6 +156,32 @@ int plan_from_engine(int l, int k, Engine& eng, int32_t* kept) {
     }
     return PM_OK;
 }
+
+}  // namespace
+
+int trial_plans(int l, int k, uint64_t master, int64_t first_trial, int n, int32_t* kept) {
+    int i = 0;
+    for (; i + 4 <= n; i += 4) {
+        LazyMt64 e0(pm_derive_seed(master, static_cast<uint64_t>(first_trial + i))),
+            e1(pm_derive_seed(master, static_cast<uint64_t>(first_trial + i + 1))),
+            e2(pm_derive_seed(master, static_cast<uint64_t>(first_trial + i + 2))),
+            e3(pm_derive_seed(master, static_cast<uint64_t>(first_trial + i + 3)));
+        // l - k draws (plus the odd rejection) read words up to 156 + draws; later words are filled on demand
+        LazyMt64::extend4(e0, e1, e2, e3, 156 + std::max(0, l - k) + 2);
+        LazyMt64* engines[4] = {&e0, &e1, &e2, &e3};
+        for (int j = 0; j < 4; ++j) {
+            const int rc = plan_from_engine(l, k, *engines[j], kept + static_cast<size_t>(i + j) * static_cast<size_t>(k));
+            if (rc != PM_OK) return rc;
+        }
+    }
+    for (; i < n; ++i) {
+        const int rc = pm_trial_plan(l, k, master, first_trial + i, kept + static_cast<size_t>(i) * static_cast<size_t>(k));
+        if (rc != PM_OK) return rc;
+    }
+    return PM_OK;
+}
+
+namespace {
 
 int64_t total_windows(const int64_t* offs, int t, int l) {
     int64_t x = 0;
