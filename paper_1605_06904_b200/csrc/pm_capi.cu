@@ -6,6 +6,9 @@
 // kernels and scans the per-trial summaries in ascending trial order exactly like the
 // reduction of driver.hpp:195-208.
 #include <algorithm>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -94,7 +97,6 @@ struct pm_ctx {
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
     std::vector<uint16_t> h_entries;
-    std::vector<std::vector<uint16_t>> h_bins;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -258,9 +260,11 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
     entries.clear();
     // per class: residue loads stored twice in a row (load2[q][r] == load2[q][r + 32]) so that the shift search
     // below reads contiguous runs and vectorises
-    std::vector<int> load2(16 * 64), mine(16 * 32);
-    std::vector<std::vector<uint16_t>>& bins = c->h_bins;
-    bins.resize(16 * 32);
+    // (16-bit counters: a tile has fewer than 2^15 positions; eight lanes per SSE2 operation)
+    std::vector<int16_t> load2(16 * 64), mine(16 * 32);
+    std::vector<uint8_t> qv;  // pair class of every position of the current sequence
+    std::vector<uint8_t> tile_q;      // pair class of every position of the current tile, sequence after sequence
+    std::vector<uint16_t> tile_slot;  // its z slot
     int64_t live_slots = 0;
     int zcap = 0, wcap = 0;
     int i = 0;
@@ -269,7 +273,8 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         tile.seq_begin = i;
         tile.group_base = static_cast<int>(entries.size() / 32);
         std::fill(load2.begin(), load2.end(), 0);
-        for (auto& b : bins) b.clear();
+        tile_q.clear();
+        tile_slot.clear();
         int64_t cursor = k::kZPad;
         while (i < t) {
             const int64_t n = rel[static_cast<size_t>(i) + 1] - rel[static_cast<size_t>(i)];
@@ -279,8 +284,10 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
             // the slack before this sequence (0..31 slots) is chosen greedily so that, per class, the
             // positions spread evenly over the 32 address residues (rows of a class = its fullest residue)
             std::fill(mine.begin(), mine.end(), 0);
+            qv.resize(static_cast<size_t>(n));
             for (int64_t p = 0; p < n; ++p) {
                 const int q = 4 * code(sq[p]) + (p + 1 < n ? code(sq[p + 1]) : 0);
+                qv[static_cast<size_t>(p)] = static_cast<uint8_t>(q);
                 ++mine[static_cast<size_t>(q * 32 + ((cursor + p) & 31))];
             }
             int best_shift = 0;
@@ -288,11 +295,24 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
             for (int sh = 0; sh < 32; ++sh) {
                 int64_t cost = 0;
                 for (int q = 0; q < 16; ++q) {
-                    const int* __restrict__ lq = load2.data() + q * 64 + sh;  // lq[r] = load[q][(r + sh) & 31]
-                    const int* __restrict__ mq = mine.data() + q * 32;
+                    const int16_t* __restrict__ lq = load2.data() + q * 64 + sh;  // lq[r] = load[q][(r + sh) & 31]
+                    const int16_t* __restrict__ mq = mine.data() + q * 32;
+#if defined(__SSE2__)
+                    __m128i mx8 = _mm_setzero_si128();
+                    for (int r = 0; r < 32; r += 8) {
+                        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(lq + r));
+                        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(mq + r));
+                        mx8 = _mm_max_epi16(mx8, _mm_add_epi16(a, b));
+                    }
+                    mx8 = _mm_max_epi16(mx8, _mm_srli_si128(mx8, 8));
+                    mx8 = _mm_max_epi16(mx8, _mm_srli_si128(mx8, 4));
+                    mx8 = _mm_max_epi16(mx8, _mm_srli_si128(mx8, 2));
+                    cost += static_cast<int16_t>(_mm_extract_epi16(mx8, 0));
+#else
                     int mx = 0;
                     for (int r = 0; r < 32; ++r) mx = std::max(mx, lq[r] + mq[r]);
                     cost += mx;
+#endif
                 }
                 if (best_cost < 0 || cost < best_cost) {
                     best_cost = cost;
@@ -308,9 +328,11 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
             }
             cursor += best_shift;
             zoff[static_cast<size_t>(i)] = static_cast<int>(cursor);
-            for (int64_t p = 0; p < n; ++p) {
-                const int q = 4 * code(sq[p]) + (p + 1 < n ? code(sq[p + 1]) : 0);
-                bins[static_cast<size_t>(q * 32 + ((cursor + p) & 31))].push_back(static_cast<uint16_t>(cursor + p));
+            tile_q.insert(tile_q.end(), qv.begin(), qv.end());
+            {
+                const size_t at = tile_slot.size();
+                tile_slot.resize(at + static_cast<size_t>(n));
+                for (int64_t p = 0; p < n; ++p) tile_slot[at + static_cast<size_t>(p)] = static_cast<uint16_t>(cursor + p);
             }
             cursor += n;
             live_slots += n;
@@ -324,19 +346,26 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         wcap = std::max(wcap, tile.n_words);
         zcap = std::max(zcap, tile.zlen);
         int row = 0;
+        // rows of class q = its fullest residue (load2 holds the per-residue counts of the finished tile); every
+        // row starts as dummies (zero slot of the same bank) and positions fill their residue's lane in order
+        int first_row[16];
         for (int q = 0; q < 16; ++q) {
             group_off.push_back(row);
-            size_t rows = 0;
-            for (int r = 0; r < 32; ++r) rows = std::max(rows, bins[static_cast<size_t>(q * 32 + r)].size());
-            for (size_t g = 0; g < rows; ++g) {
-                for (int r = 0; r < 32; ++r) {
-                    const std::vector<uint16_t>& b = bins[static_cast<size_t>(q * 32 + r)];
-                    entries.push_back(g < b.size() ? b[g] : static_cast<uint16_t>(32 + r));  // dummy: zero slot, same bank
-                }
-            }
-            row += static_cast<int>(rows);
+            first_row[q] = row;
+            int rows = 0;
+            for (int r = 0; r < 32; ++r) rows = std::max<int>(rows, load2[static_cast<size_t>(q * 64 + r)]);
+            row += rows;
         }
         group_off.push_back(row);
+        const size_t base = entries.size();
+        entries.resize(base + static_cast<size_t>(row) * 32);
+        for (size_t e = base; e < entries.size(); ++e) entries[e] = static_cast<uint16_t>(32 + ((e - base) & 31));
+        int16_t placed[16 * 32] = {0};
+        for (size_t p = 0; p < tile_q.size(); ++p) {
+            const int q = tile_q[p], r = tile_slot[p] & 31;
+            const int g = placed[q * 32 + r]++;
+            entries[base + (static_cast<size_t>(first_row[q]) + static_cast<size_t>(g)) * 32 + static_cast<size_t>(r)] = tile_slot[p];
+        }
         tiles.push_back(tile);
     }
     const size_t live_rows = entries.size() / 32;
@@ -974,7 +1003,9 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
         if (offs[i + 1] - offs[i] > INT32_MAX) return set_error(PM_ERR_UNSUPPORTED, "sequence longer than 2^31-1 bases");
     }
     PM_CUDA(cudaSetDevice(c->device));
+    HostMarks up_marks;
     PM_CUDA(cudaStreamSynchronize(c->stream));
+    up_marks.mark("upload: sync");
     c->t = 0;
     c->win_l = 0;
     c->zlen = 0;
@@ -1026,10 +1057,13 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     k::encode_kernel<<<grid, warps_per_block * 32, 0, c->stream>>>(d_ascii, d_offs, c->d_word_off, t, c->d_words,
                                                                  c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
     PM_TRY(check_launch(c, "encode"));
+    up_marks.mark("h2d+encode issued");
     PM_TRY(build_class_groups(c, bases + base0, rel, word_off, t));  // host index build overlaps the encode kernel
+    up_marks.mark("class groups");
     unsigned long long host_tot[5];
     PM_TRY(d2h(c, host_tot, c->d_tot_sym, sizeof(host_tot)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
+    up_marks.mark("final sync");
     if (host_tot[4] != ULLONG_MAX) {
         const int64_t bad = static_cast<int64_t>(host_tot[4]);
         int seq = 0;
