@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -97,6 +99,7 @@ struct pm_ctx {
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
     std::vector<uint16_t> h_entries;
+    std::vector<double> h_logw;
     // window index space for the current l
     int win_l = 0;
     std::vector<int64_t> win_off;
@@ -442,11 +445,12 @@ int prepare_windows(pm_ctx* c, int l) {
         return set_error(PM_ERR_INVALID_PARAMS, "sort-and-group hashing supports at most 2^32-1 l-mers");  // projection.hpp:284-287
     }
     c->uniform_w = uniform ? c->seq_len[0] - l + 1 : 0;
-    std::vector<double> logw(static_cast<size_t>(c->t));
+    // staging owned by the context (alive until the next change, which synchronises first): no sync here
+    std::vector<double>& logw = c->h_logw;
+    logw.resize(static_cast<size_t>(c->t));
     for (int i = 0; i < c->t; ++i) logw[static_cast<size_t>(i)] = std::log(static_cast<double>(c->seq_len[static_cast<size_t>(i)] - l + 1));
     PM_TRY(h2d(c, c->d_seq_logw, logw.data(), sizeof(double) * logw.size()));
     PM_TRY(h2d(c, c->d_win_off, c->win_off.data(), sizeof(int64_t) * (static_cast<size_t>(c->t) + 1)));
-    PM_CUDA(cudaStreamSynchronize(c->stream));
     c->win_l = l;
     return PM_OK;
 }
@@ -756,6 +760,23 @@ int em_warps_for(int t) {
     return 4;
 }
 
+// Function attributes are per process, not per context: the dynamic shared-memory limit of a kernel only ever
+// grows (monotone, under a lock), so a launch configured by one context stays valid whatever another one set.
+int ensure_dynamic_smem(const void* func, size_t bytes, bool max_carveout) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> allowed;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = allowed[func];
+    if (bytes > cur) {
+        PM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+        if (cur == 0 && max_carveout) {
+            PM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+        }
+        cur = bytes;
+    }
+    return PM_OK;
+}
+
 struct EmOut {
     int32_t* score = nullptr;
     int32_t* iters = nullptr;
@@ -817,8 +838,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
             if (c->pair_cfg_l == l && c->pair_cfg_smem == smem && c->pair_cfg_threads == threads) {
                 per_sm = c->pair_cfg_per_sm;
             } else {
-                PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+                PM_TRY(ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem, true));
                 PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
                 c->pair_cfg_l = l;
                 c->pair_cfg_smem = smem;
@@ -858,8 +878,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         if (c->em_cfg_l == l && c->em_cfg_smem == smem && c->em_cfg_threads == threads) {
             per_sm = c->em_cfg_per_sm;  // attributes and occupancy were set up by an earlier launch
         } else {
-            PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            PM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+            PM_TRY(ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem, true));
             PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
             c->em_cfg_l = l;
             c->em_cfg_smem = smem;
@@ -1011,8 +1030,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     c->zlen = 0;
     c->n_tiles = 0;
     c->total_groups = 0;
-    c->em_cfg_l = -1;
-    c->pair_cfg_l = -1;
+    // the cached EM launch setups stay valid: they are keyed by (l, shared-memory bytes, threads)
 
     const int64_t base0 = offs[0];
     std::vector<int64_t> rel(static_cast<size_t>(t) + 1), word_off(static_cast<size_t>(t) + 1, 0);
@@ -1483,7 +1501,7 @@ int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
     PM_TRY(get_buf(c, S_REC_SIZE, nrec, &r->size));
     PM_TRY(get_buf(c, S_NREC, static_cast<size_t>(n) + 1, &r->n_rec));
     const size_t smem = fused_hash_smem_bytes(static_cast<int>(c->total_words), keybits, r->cap_e, c->t, c->x);
-    PM_CUDA(cudaFuncSetAttribute(k::hash_bucket_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    PM_TRY(ensure_dynamic_smem(reinterpret_cast<const void*>(k::hash_bucket_fused_kernel), smem, false));
     k::FusedHashParams p;
     p.words = c->d_words;
     p.word_off = c->d_word_off;
