@@ -101,3 +101,27 @@ def test_long_motifs_use_the_wide_flush_path(ctx, best_oracle):
                 assert (a["consensus"], a["score"]) == (w.consensus, w.score)
                 compared += 1
     assert compared >= 20
+
+
+def test_large_set_path_with_frozen_buckets(ctx, best_oracle):
+    """t > 64 selects the pair kernel's large-set path (per-tile metadata, previous maxima in global memory,
+    double-buffered word stages); with max_iters = 12 the buckets of a pair stop at different iterations."""
+    import numpy as np
+    from oracle import pmo
+    rng = np.random.default_rng(5)
+    motif = "ACGTTGCA"
+    strings = []
+    for _ in range(90):
+        s = list(rng.choice(list("ACGT"), int(rng.integers(40, 90))))
+        at = int(rng.integers(0, len(s) - 8))
+        s[at:at + 8] = list(motif)
+        strings.append("".join(s))
+    ss = pmo.SeqSet.from_strings(strings)
+    kept = best_oracle.sample_plan(8, 6, 2)
+    en = best_oracle.enriched(ss, 8, kept, 3, 90 * 3)[:15]
+    want = [best_oracle.refine(ss, 8, e["members"], e["key"], max_iters=12) for e in en]
+    assert len({w.iterations for w in want}) >= 2
+    ctx.set_sequences(ss.bases, ss.offs)
+    got = ctx.refine(8, [e["members"] for e in en], max_iters=12)
+    for a, w in zip(got, want):
+        _check(a, w)
