@@ -75,7 +75,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "25",
                  "-i", str(self.gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
@@ -306,9 +306,9 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
     if rank == 0:
         sampler.start()
     ms_dev, launches, stage, lookups, _, _, result, work = timed_loop(args.steps, False)
-    clocks = sampler.stop() if rank == 0 else None
     timed_loop(max(1, min(args.warmup, 2)), True)
     ms_e2e, _, stage_e2e, _, h2d, d2h, result_e2e, _ = timed_loop(args.steps, True)
+    clocks = sampler.stop() if rank == 0 else None  # sampled across both timed loops (HBM-resident and end-to-end)
 
     if rank != 0:
         if dist is not None:
