@@ -352,7 +352,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
                      "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
                      # dram__bytes_read+write of one launch from the ncu --set full capture in profiles/ (C1 only):
                      # the kernel's working set is shared memory + L1/L2-resident tables
-                     "traffic": 858368 if args.config == "c1" and not args.trials else None,
+                     "traffic": 857088 if args.config == "c1" and not args.trials else None,
                      "traffic_source": "profiles/r1_em_refine_pair_ncu_full.txt (ncu, dram bytes per launch)",
                      "launch_ms": em_ms / max(1, em_launches // args.steps),
                      "work": "SURVEY 8(d) W_EM = sum_b (2 I_b+1) x l + 4 (I_b+1) x FP32 ops (E- and M-step), measured I_b",
