@@ -818,16 +818,18 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                 // ================= M-step of the tile: conflict-free class gather, both buckets =================
                 {
                     const int item_lo = wrow[warp], item_hi = wrow[warp + 1];
-                    const uint16_t* __restrict__ rows = x.cls_entries + static_cast<size_t>(tile.group_base) * 32 + lane;
+                    // this warp's rows [item_lo, item_hi) are contiguous in the table, class after class: the two-ahead
+                    // prefetch of the row entries runs straight through the class boundaries (the table is padded
+                    // at its end, so it may also run past item_hi)
+                    const uint16_t* __restrict__ ent =
+                        x.cls_entries + (static_cast<size_t>(tile.group_base) + static_cast<size_t>(item_lo)) * 32 + lane;
+                    int pos = ent[0], pos1 = ent[32];
                     for (int q = 0; q < 16; ++q) {
                         const int ra = max(item_lo, s_off[q]), rb = min(item_hi, s_off[q + 1]);
                         if (ra >= rb) continue;  // this warp owns no row of class q
                         float2 acc2[G];  // {bucket 0, bucket 1} per column pair: one FADD2 per gathered slot
 #pragma unroll
                         for (int g = 0; g < G; ++g) acc2[g] = make_float2(0.f, 0.f);
-                        // rows are padded at the end of the table: the two-ahead prefetch may run past rb
-                        const uint16_t* __restrict__ ent = rows + static_cast<size_t>(ra) * 32;
-                        int pos = ent[0], pos1 = ent[32];
                         for (int it = ra; it < rb; ++it) {
                             ent += 32;
                             const int pos2 = ent[32];
