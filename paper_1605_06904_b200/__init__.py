@@ -20,7 +20,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("PM_B200_LIB") or os.path.join(PKG_DIR, "libpm_b200.so")  # override: instrumented builds
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = ["pm_capi.cu", "pm_host.cpp"]
-HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_hash_fused.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
+HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_em_tc.cuh", "pm_hash_fused.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -107,7 +107,7 @@ EXPORTS = [
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
-    "pm_ctx_launch_count", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_score",
+    "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_score",
     "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host",
 ]
 
@@ -327,6 +327,13 @@ class Context:
 
     def launch_count(self):
         return int(lib().pm_ctx_launch_count(self._h))
+
+    def em_exact_counts(self):
+        """Buckets of the last refine()/run() that the tensor-core EM kernel handed to the exact kernel:
+        dict(total, likelihood_gain, range, argmax_tie, non_finite)."""
+        out = np.zeros(5, dtype=np.int64)
+        _check(lib().pm_ctx_em_exact_counts(self._h, _p(out, C.c_int64)))
+        return dict(zip(("total", "likelihood_gain", "range", "argmax_tie", "non_finite"), out.tolist()))
 
     # ---- stages
     def hash_keys(self, l, kept):

@@ -28,6 +28,7 @@
 #include "pm_kernels.cuh"
 #include "pm_em_smem.cuh"
 #include "pm_em_pair.cuh"
+#include "pm_em_tc.cuh"
 #include "pm_hash_fused.cuh"
 
 using namespace pm;
@@ -58,7 +59,8 @@ struct DevBuf {
 enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
-    S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS, S_COUNT_
+    S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
+    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_COUNT_
 };
 
 }  // namespace
@@ -95,6 +97,12 @@ struct pm_ctx {
     size_t pair_cfg_smem = 0;
     int32_t max_seq_len = 0;
     int max_tile_seqs = 0;  // most sequences any tile of the class-group index holds
+    // tensor-core EM kernel (pm_em_tc.cuh): block list of one sweep for the current (set, l)
+    int tc_l = -1, tc_n_blocks = 0, tc_e_positions = 0;
+    std::vector<k::TcBlock> h_tc_blocks;
+    k::TcBlock* d_tc_blocks = nullptr;
+    int64_t em_exact[5] = {0, 0, 0, 0, 0};  // last refine/run: buckets the tensor-core kernel handed to the exact kernel
+                                            // [0] total, then by reason: likelihood gain, range, argmax tie, non-finite
     // host staging of the class-group index: lives in the context so the async uploads need no sync of their own
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
@@ -787,10 +795,111 @@ struct EmOut {
     double* ll = nullptr;
 };
 
-// scalars on the device: [0] iter_total (u64) [1] error flag (u32 in the low half)
+
+// ---- tensor-core EM kernel (pm_em_tc.cuh) ------------------------------------------------------------------
+// PM_B200_EM_TC (test/tuning knob): 0 keeps every bucket on the pair kernel, 2 uses the tensor-core kernel even for
+// a handful of buckets (default: from 32 buckets on; below that a 128-row tile is mostly empty)
+bool em_tc_enabled(unsigned int n_work_bound) {
+    const char* env = std::getenv("PM_B200_EM_TC");
+    const int v = env ? std::atoi(env) : 1;
+    return v >= 2 || (v == 1 && n_work_bound >= 32);
+}
+
+int tc_kc_for(int l) { return std::max(8, 4 * ((l + 3) / 4)); }
+
+// gathers the flagged work items of the tensor-core launch for the exact kernel
+__global__ void tc_compact_kernel(const unsigned char* __restrict__ flag, const k::WorkDesc* __restrict__ work,
+                                  const unsigned int* __restrict__ n_work_dev, unsigned int n_work_host,
+                                  k::WorkDesc* __restrict__ out_work, unsigned int* __restrict__ out_map,
+                                  unsigned int* __restrict__ counter) {
+    const unsigned int n = n_work_dev ? *n_work_dev : n_work_host;
+    const unsigned int lane = threadIdx.x & 31u;
+    for (unsigned int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < n; base += gridDim.x * blockDim.x) {
+        const unsigned int i = base + lane;
+        const bool f = i < n && flag[i] != 0;
+        const unsigned int ball = __ballot_sync(0xffffffffu, f);
+        if (ball == 0) continue;
+        unsigned int at = 0;
+        if (lane == 0) at = atomicAdd(counter, static_cast<unsigned int>(__popc(ball)));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (f) {
+            const unsigned int o = at + __popc(ball & ((1u << lane) - 1u));
+            out_work[o] = work[i];
+            out_map[o] = i;
+        }
+    }
+}
+
+// One sweep of the tensor-core kernel as a list of blocks (see TcBlock): every sequence's even windows, then its
+// odd windows, in runs of 16 columns, cut into blocks of at most NBLK columns.
+int build_tc_blocks(pm_ctx* c, int l) {
+    if (c->tc_l == l) return PM_OK;
+    const int KC = tc_kc_for(l);
+    const int NBLK = KC <= 16 ? 128 : 96;
+    auto ru = [](int v, int m) { return (v + m - 1) / m * m; };
+    c->h_tc_blocks.clear();
+    for (int i = 0; i < c->t; ++i) {
+        const int W = c->seq_len[static_cast<size_t>(i)] - l + 1;
+        const int ne = (W + 1) / 2, no = W / 2;
+        const int ce = ru(ne, 16), co = ru(no, 16);
+        const int cp = ru(ce + co, 32);
+        const int nb = (cp + NBLK - 1) / NBLK, units = cp / 32;
+        int b0 = 0;
+        for (int b = 0; b < nb; ++b) {
+            const int ncols = 32 * (units / nb + (b < units % nb ? 1 : 0));
+            k::TcBlock B;
+            std::memset(&B, 0, sizeof(B));
+            B.seq = static_cast<uint16_t>(i);
+            B.ncols = static_cast<uint16_t>(ncols);
+            B.first = b == 0;
+            B.last = b == nb - 1;
+            int ns = 0;
+            const int e_lo = b0, e_hi = std::min(b0 + ncols, ce);
+            if (e_lo < e_hi) {
+                k::TcSeg& sg = B.seg[ns++];
+                sg.par = 0;
+                sg.i0 = static_cast<uint16_t>(e_lo);
+                sg.n = static_cast<uint16_t>(e_hi - e_lo);
+                sg.col = 0;
+                sg.valid = static_cast<uint16_t>(std::max(0, std::min(ne - e_lo, e_hi - e_lo)));
+            }
+            const int o_lo = std::max(b0, ce), o_hi = std::min(b0 + ncols, ce + co);
+            if (o_lo < o_hi) {
+                k::TcSeg& sg = B.seg[ns++];
+                sg.par = 1;
+                sg.i0 = static_cast<uint16_t>(o_lo - ce);
+                sg.n = static_cast<uint16_t>(o_hi - o_lo);
+                sg.col = static_cast<uint16_t>(o_lo - b0);
+                sg.valid = static_cast<uint16_t>(std::max(0, std::min(no - (o_lo - ce), o_hi - o_lo)));
+            }
+            c->h_tc_blocks.push_back(B);
+            b0 += ncols;
+        }
+    }
+    c->tc_n_blocks = static_cast<int>(c->h_tc_blocks.size());
+    c->tc_e_positions = ru(c->max_seq_len + k::kTcEPad, 32);
+    PM_TRY(get_buf(c, S_TC_BLOCKS, c->h_tc_blocks.size(), &c->d_tc_blocks));
+    PM_TRY(h2d(c, c->d_tc_blocks, c->h_tc_blocks.data(), sizeof(k::TcBlock) * c->h_tc_blocks.size()));
+    c->tc_l = l;
+    return PM_OK;
+}
+
+using EmTcKernel = void (*)(const k::EmParams, const k::TcExtra);
+EmTcKernel em_tc_kernel_for(int l) {
+    switch (tc_kc_for(l)) {
+        case 8: return k::em_refine_tc_kernel<8>;
+        case 12: return k::em_refine_tc_kernel<12>;
+        case 16: return k::em_refine_tc_kernel<16>;
+        default: return k::em_refine_tc_kernel<20>;
+    }
+}
+
+// scalars on the device: [0] iter_total (u64) [1] error flag (u32 in the low half) [3] buckets the tensor-core kernel
+// handed to the exact kernel (u32 in the low half) [4..7] the same by reason (a bucket can have several)
 int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k::WorkDesc* work,
               const unsigned int* n_work_dev, unsigned int n_work_host, unsigned int n_work_bound,
-              const unsigned int* members, const EmOut& o, unsigned long long* d_scal) {
+              const unsigned int* members, const EmOut& o, unsigned long long* d_scal, int max_count = 1 << 30,
+              const double* theta_in = nullptr) {
     k::EmParams p;
     std::memset(&p, 0, sizeof(p));
     p.words = c->d_words;
@@ -822,8 +931,49 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.iter_total = d_scal;
     p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
     p.phase_clk = d_scal + 8;
+    p.out_map = nullptr;
+    p.theta_in = theta_in;
 
-    if (c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs && em_pair_enabled()) {
+    const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs && em_pair_enabled();
+    const bool pair_small = pair_ok && !(c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords);
+    // Tensor-core kernel (pm_em_tc.cuh): 128 buckets per CTA.  It decides every bucket whose discrete outputs are clear
+    // of the FP32 error of its sums and flags the rest, which the pair kernel below then refines into the same slots.
+    if (pair_small && em_tc_enabled(n_work_bound) && theta_in == nullptr && l <= k::kTcMaxL && c->t <= k::kTcMaxSeqs &&
+        max_iters <= k::kTcMaxIters && max_count <= 255 && c->max_seq_len + k::kTcEPad <= 4096 && n_work_bound >= 1) {
+        PM_TRY(build_tc_blocks(c, l));
+        const size_t smem = std::max<size_t>(k::tc_smem_bytes(c->t, c->tc_n_blocks, c->tc_e_positions), 120 * 1024);
+        if (smem <= 227 * 1024) {
+            EmTcKernel kern = em_tc_kernel_for(l);
+            PM_TRY(ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem, true));
+            k::TcExtra x;
+            x.blocks = c->d_tc_blocks;
+            x.n_blocks = c->tc_n_blocks;
+            x.e_positions = c->tc_e_positions;
+            x.tie_delta = 1e-3f;
+            x.ll_margin = 1e-2f;
+            x.stats = d_scal + 4;
+            unsigned int* d_cnt = reinterpret_cast<unsigned int*>(d_scal + 3);  // zeroed by the caller with the other scalars
+            k::WorkDesc* d_list;
+            unsigned int* d_map;
+            PM_TRY(get_buf(c, S_TC_FLAG, static_cast<size_t>(n_work_bound), &x.out_flag));
+            PM_TRY(get_buf(c, S_TC_WORK, static_cast<size_t>(n_work_bound), &d_list));
+            PM_TRY(get_buf(c, S_TC_MAP, static_cast<size_t>(n_work_bound), &d_map));
+            const unsigned int tiles = (n_work_bound + k::kTcRows - 1) / k::kTcRows;
+            const unsigned int grid = std::max(1u, std::min(static_cast<unsigned int>(c->sm_count), tiles));
+            kern<<<grid, k::kTcThreads, smem, c->stream>>>(p, x);
+            PM_TRY(check_launch(c, "em_refine_tc"));
+            const unsigned int cgrid = std::max(1u, std::min(1024u, (n_work_bound + 255) / 256));
+            tc_compact_kernel<<<cgrid, 256, 0, c->stream>>>(x.out_flag, work, n_work_dev, n_work_host, d_list, d_map, d_cnt);
+            PM_TRY(check_launch(c, "tc_compact"));
+            // the exact kernel takes over the flagged buckets
+            p.work = d_list;
+            p.n_work_dev = d_cnt;
+            p.n_work = 0;
+            p.out_map = d_map;
+        }
+    }
+
+    if (pair_ok) {
         // two buckets per CTA in lockstep (pm_em_pair.cuh).  Small sets keep all per-sequence state and the whole
         // packed set in shared memory; large sets walk the tiles with per-tile state (C5: 1,000 tiles of 10).
         const bool big = c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords;
@@ -1027,6 +1177,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     up_marks.mark("upload: sync");
     c->t = 0;
     c->win_l = 0;
+    c->tc_l = -1;
     c->zlen = 0;
     c->n_tiles = 0;
     c->total_groups = 0;
@@ -1137,6 +1288,12 @@ int pm_ctx_synchronize(pm_ctx* c) {
     if (c == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null context");
     PM_CUDA(cudaSetDevice(c->device));
     PM_CUDA(cudaStreamSynchronize(c->stream));
+    return PM_OK;
+}
+
+int pm_ctx_em_exact_counts(const pm_ctx* c, int64_t* out5) {
+    if (c == nullptr || out5 == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    for (int i = 0; i < 5; ++i) out5[i] = c->em_exact[i];
     return PM_OK;
 }
 
@@ -1312,12 +1469,15 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem)));
     PM_TRY(h2d(c, d_work, work.data(), sizeof(k::WorkDesc) * nb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
+    unsigned int max_count = 0;
+    for (const k::WorkDesc& w : work) max_count = std::max(max_count, w.count);
     PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
-                     static_cast<unsigned int>(n_buckets), d_mem, o, d_scal));
+                     static_cast<unsigned int>(n_buckets), d_mem, o, d_scal,
+                     static_cast<int>(std::min<unsigned int>(max_count, 1u << 30))));
     std::vector<int32_t> hs(nb), hi(nb);
     std::vector<double> he(nb);
     std::vector<uint64_t> hc(nb);
-    unsigned long long scal[2];
+    unsigned long long scal[8];
     PM_TRY(d2h(c, hs.data(), o.score, sizeof(int32_t) * nb));
     PM_TRY(d2h(c, hi.data(), o.iters, sizeof(int32_t) * nb));
     PM_TRY(d2h(c, he.data(), o.expct, sizeof(double) * nb));
@@ -1327,6 +1487,8 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     if (theta) PM_TRY(d2h(c, theta, o.theta, sizeof(double) * nb * 4 * static_cast<size_t>(l + 1)));
     if (ll_trace) PM_TRY(d2h(c, ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
+    c->em_exact[0] = static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
+    for (int r = 0; r < 4; ++r) c->em_exact[1 + r] = static_cast<int64_t>(scal[4 + r]);
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
@@ -1594,7 +1756,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     {
         StageTimer tm(c, prof, 3);
         PM_TRY(launch_em(c, l, cfg->max_em_iters, cfg->em_tol, cfg->z_epsilon, work, work_off + n_trials, 0,
-                         static_cast<unsigned int>(std::min<size_t>(nb, 1u << 30)), srt.idx, o, d_scal));
+                         static_cast<unsigned int>(std::min<size_t>(nb, 1u << 30)), srt.idx, o, d_scal, r_cap));
     }
     host_mark("launched");
     std::vector<TrialSummary> tb(static_cast<size_t>(n_trials));
@@ -1632,6 +1794,8 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
+    c->em_exact[0] += static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
+    for (int r = 0; r < 4; ++r) c->em_exact[1 + r] += static_cast<int64_t>(scal[4 + r]);
     out->em_lookup_adds += static_cast<int64_t>(scal[0]) * c->x * l;
     {
         // W_EM = sum_b (2 I_b + 1) x l lookup-adds + 4 (I_b + 1) x; scal[0] = sum_b (I_b + 1)
@@ -1737,6 +1901,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
 
     RunState st;
     bool stop = false;
+    for (int64_t& v : c->em_exact) v = 0;
     HostMarks marks;
     g_marks = &marks;
     struct MarksGuard { ~MarksGuard() { g_marks = nullptr; } } marks_guard;

@@ -463,6 +463,8 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         const bool live1 = 2 * pi + 1 < n_work;
         const unsigned int wis[2] = {2 * pi, live1 ? 2 * pi + 1 : 2 * pi};  // an odd tail refines its bucket twice
         const WorkDesc wd0 = p.work[wis[0]], wd1 = p.work[wis[1]];
+        // output slots: the work index itself, or its slot in the list the work items were compacted from
+        const unsigned int ois[2] = {p.out_map ? p.out_map[wis[0]] : wis[0], p.out_map ? p.out_map[wis[1]] : wis[1]};
         __syncthreads();
 #ifdef PM_EM_TIMING
         long long t_phase = clock64();
@@ -502,8 +504,10 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         for (int e2 = threadIdx.x; e2 < 2 * TH; e2 += blockDim.x) {
             const int b = e2 >= TH, e = e2 - b * TH;
             const int c = e >> 2, r = e & 3;
-            const double tv = c == 0 ? p.tot_sym[r] / p.tot_bases
-                                     : static_cast<double>(prof[b * 128 + (c - 1) * 4 + r]) / static_cast<double>(b ? wd1.count : wd0.count);
+            // pm_em_step starts from a caller-supplied model instead of theta0
+            const double tv = p.theta_in ? p.theta_in[static_cast<int64_t>(wis[b]) * TH + r * (l + 1) + c]
+                              : c == 0   ? p.tot_sym[r] / p.tot_bases
+                                         : static_cast<double>(prof[b * 128 + (c - 1) * 4 + r]) / static_cast<double>(b ? wd1.count : wd0.count);
             thd[e2] = tv;
             L64[e2] = log_f64(fmax(tv, 1e-9));
         }
@@ -704,7 +708,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                 }
                                 arg = bj;
                             }
-                            if (p.out_pos && lane == 0 && (bb == 0 || live1)) p.out_pos[static_cast<int64_t>(wis[bb]) * t + i] = arg + 1;
+                            if (p.out_pos && lane == 0 && (bb == 0 || live1)) p.out_pos[static_cast<int64_t>(ois[bb]) * t + i] = arg + 1;
                             if (lane < l) {
                                 const uint64_t v = load_window(wp, arg);
                                 atomicAdd(&prof[bb * 128 + lane * 4 + (static_cast<unsigned>(v >> colshift) & 3u)], 1);
@@ -977,7 +981,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     for (int r = 0; r < 4; ++r) ll += p.tot_sym[r] * dscal[bb * 6 + 2 + r];
                     ll -= sum_logw;
                     for (int w = 0; w < nwarps; ++w) ll += llpart[w * 2 + bb];
-                    if (p.out_ll && (bb == 0 || live1)) p.out_ll[static_cast<int64_t>(wis[bb]) * p.max_iters + (iterations - 1)] = ll;
+                    if (p.out_ll && (bb == 0 || live1)) p.out_ll[static_cast<int64_t>(ois[bb]) * p.max_iters + (iterations - 1)] = ll;
                     iscal[bb * 4 + 0] = (iterations >= 2 && ll - dscal[bb * 6] < p.tol) ? 1 : 0;  // refine.hpp:296-304
                     iscal[bb * 4 + 3] = iterations;
                     dscal[bb * 6] = ll;
@@ -1006,7 +1010,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
         __syncthreads();
         if (threadIdx.x < 2 && (threadIdx.x == 0 || live1)) {
             const int bb = threadIdx.x;
-            const unsigned int wi = wis[bb];
+            const unsigned int wi = ois[bb];
             double ex = 0.0;
             #pragma unroll 1
             for (int c = 1; c <= l; ++c) {
@@ -1026,7 +1030,7 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                 const int bb = e2 >= TH, e = e2 - bb * TH;
                 if (bb && !live1) continue;
                 const int c = e >> 2, r = e & 3;
-                p.out_theta[static_cast<int64_t>(wis[bb]) * 4 * (l + 1) + r * (l + 1) + c] = thd[e2];
+                p.out_theta[static_cast<int64_t>(ois[bb]) * 4 * (l + 1) + r * (l + 1) + c] = thd[e2];
             }
         }
         PM_PHASE(6);  // score, consensus, outputs

@@ -531,6 +531,8 @@ struct EmParams {
     unsigned long long* iter_total;  // sum over buckets of E-steps executed (iterations + 1)
     unsigned int* error_flag;        // set to 1 on a non-finite window weight (NumericalUnderflowError)
     unsigned long long* phase_clk;   // [8] per-phase clock sums (only with -DPM_EM_TIMING)
+    const unsigned int* out_map;     // nullptr, or output slot of each work item (re-runs of flagged buckets, pm_em_tc.cuh)
+    const double* theta_in;          // nullptr, or [work][4][l+1] starting models instead of init_model (pm_em_step)
 };
 
 template <int G>
