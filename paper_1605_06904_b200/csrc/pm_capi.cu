@@ -636,30 +636,6 @@ EmKernel em_kernel_for(int l) {
 using EmSmemKernel = void (*)(const k::EmParams, const k::EmSmemExtra);
 
 template <int G>
-EmSmemKernel em_smem_for() { return k::em_refine_smem_kernel<G>; }
-
-EmSmemKernel em_smem_kernel_for(int l) {
-    switch ((l + 1) / 2) {
-        case 1: return em_smem_for<1>();
-        case 2: return em_smem_for<2>();
-        case 3: return em_smem_for<3>();
-        case 4: return em_smem_for<4>();
-        case 5: return em_smem_for<5>();
-        case 6: return em_smem_for<6>();
-        case 7: return em_smem_for<7>();
-        case 8: return em_smem_for<8>();
-        case 9: return em_smem_for<9>();
-        case 10: return em_smem_for<10>();
-        case 11: return em_smem_for<11>();
-        case 12: return em_smem_for<12>();
-        case 13: return em_smem_for<13>();
-        case 14: return em_smem_for<14>();
-        case 15: return em_smem_for<15>();
-        default: return em_smem_for<16>();
-    }
-}
-
-template <int G>
 EmSmemKernel em_pair_for() { return k::em_refine_pair_kernel<G>; }
 
 EmSmemKernel em_pair_kernel_for(int l) {
@@ -713,26 +689,6 @@ int em_pair_warps_for(int t) {
         if (v >= 2 && v <= k::kPairMaxWarps) return static_cast<int>(v);
     }
     return em_smem_warps_for(t);
-}
-
-bool em_pair_enabled() {
-    const char* env = std::getenv("PM_B200_EM_PAIR");  // test/tuning knob: 0 selects the one-bucket kernel
-    return env == nullptr || std::atoi(env) != 0;
-}
-
-// must mirror the carve-up at the top of em_refine_smem_kernel
-size_t em_smem_bytes_v2(int nwarps, int G, int zlen, int t, int tile_words, int n_tiles) {
-    size_t b = 0;
-    b += (128 + 128 + static_cast<size_t>(nwarps) + 6) * 8;                               // thd, D64, llpart, dscal
-    b += (256 + static_cast<size_t>(nwarps) * 16 * G + 16 * static_cast<size_t>(G)) * 4;  // T, cpart, Cq
-    b += (static_cast<size_t>(nwarps) * k::kNearCap + 128 + 4 + 20) * 4;                  // near_j, prof, iscal, s_off
-    b += 8;                                                                               // cons_bits
-    b += (t <= k::kMaxFusedSeqs ? static_cast<size_t>((t + 1) & ~1) : 0) * 4;               // mprev
-    b += static_cast<size_t>(zlen) * 4;                                                   // zbuf
-    b = (b + 15) & ~static_cast<size_t>(15);
-    b += static_cast<size_t>(tile_words) * 8 * (n_tiles > 1 ? 2 : 1);                     // TMA word stage(s)
-    b += 16;                                                                              // two mbarriers
-    return b + 16;
 }
 
 int em_smem_warps_for(int t) {
@@ -934,7 +890,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.out_map = nullptr;
     p.theta_in = theta_in;
 
-    const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs && em_pair_enabled();
+    const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs;
     const bool pair_small = pair_ok && !(c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords);
     // Tensor-core kernel (pm_em_tc.cuh): 128 buckets per CTA.  It decides every bucket whose discrete outputs are clear
     // of the FP32 error of its sums and flags the rest, which the pair kernel below then refines into the same slots.
@@ -1015,43 +971,6 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
                 kern<<<grid, threads, smem, c->stream>>>(p, x);
                 return check_launch(c, "em_refine_pair");
             }
-        }
-    }
-    if (c->zlen > 0) {
-        // shared-memory kernel: z of every window resident per CTA, conflict-free class-gather M-step
-        const int G = (l + 1) / 2;
-        const int nwarps = em_smem_warps_for(c->t);
-        const int threads = nwarps * 32;
-        const size_t smem = em_smem_bytes_v2(nwarps, G, c->zlen, c->t, c->tile_words, c->n_tiles);
-        EmSmemKernel kern = em_smem_kernel_for(l);
-        int per_sm = 0;
-        if (c->em_cfg_l == l && c->em_cfg_smem == smem && c->em_cfg_threads == threads) {
-            per_sm = c->em_cfg_per_sm;  // attributes and occupancy were set up by an earlier launch
-        } else {
-            PM_TRY(ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem, true));
-            PM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-            c->em_cfg_l = l;
-            c->em_cfg_smem = smem;
-            c->em_cfg_threads = threads;
-            c->em_cfg_per_sm = per_sm;
-        }
-        if (per_sm >= 1) {
-            const unsigned int full = static_cast<unsigned int>(c->sm_count * per_sm);
-            const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
-            k::EmSmemExtra x;
-            x.tiles = c->d_tiles;
-            x.n_tiles = c->n_tiles;
-            x.cls_entries = c->d_cls_entries;
-            x.tile_group_off = c->d_cls_group_off;
-            x.seq_zoff = c->d_seq_zoff;
-            x.mprev_g = nullptr;
-            x.zcap = c->zlen;
-            x.wcap = c->tile_words;
-            if (c->t > k::kMaxFusedSeqs) {
-                PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * static_cast<size_t>(c->t), &x.mprev_g));
-            }
-            kern<<<grid, threads, smem, c->stream>>>(p, x);
-            return check_launch(c, "em_refine_smem");
         }
     }
     const int nwarps = em_warps_for(c->t);
@@ -1782,6 +1701,10 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     }
     host_mark("gpu-wait");
     collect_stage_times(c, out->stage_ms);
+#ifdef PM_TC_TIMING
+    std::fprintf(stderr, "[tc clocks, CTA 0 softmax thread] total %llu  wait S %llu  wait O %llu  updates %llu | EM passes %llu  MAX passes %llu  final %llu | sequence close %llu\n",
+                 scal[8], scal[9], scal[10], scal[11], scal[12], scal[13], scal[14], scal[15]);
+#endif
 #ifdef PM_EM_TIMING
     {
         unsigned long long tot = 0;

@@ -29,7 +29,7 @@
 #pragma once
 #include <cuda_bf16.h>
 
-#include "pm_em_smem.cuh"
+#include "pm_em_pair.cuh"
 
 namespace pm {
 namespace k {
@@ -91,6 +91,18 @@ __device__ __forceinline__ void tc_wait(unsigned long long* bar, unsigned parity
         "r"(parity)
         : "memory");
 }
+// one lane of a converged warp (the compiler keeps the operands of the guarded instructions in uniform registers)
+__device__ __forceinline__ bool tc_elect() {
+    uint32_t pred;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.b32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -112,6 +124,13 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint32_t a_tmem, uint32_
         : "memory");
 }
 
+// {e1, e0} -> packed bf16x2 (e0 in the low half: the lower K index)
+__device__ __forceinline__ uint32_t tc_pack_bf16(float e0, float e1) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(e1), "f"(e0));
+    return d;
+}
+
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
@@ -124,6 +143,114 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
                  "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
                  : "memory");
 }
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+                   "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+                   "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+                   "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),
+                 "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+                 "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]),
+                 "r"(r[31])
+                 : "memory");
+}
+
+// ---- per-chunk work of a softmax thread: 16 columns (= 16 windows of one parity) of its row ------------------
+struct TcSeqState {
+    float2 sum2a, sum2b;  // partial sums of e (EM pass): four independent chains
+    float mxa, mxb;       // running maximum of the weights: two chains (final pass: mxa only)
+    float second;         // final pass: runner-up weight
+    int best_j;           // final pass: window of the maximum
+};
+
+// EM pass: e = 2^(w - ref), running sum and maximum, e as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM
+template <bool kMasked>
+__device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint32_t* __restrict__ o, int nvalid, float ref2,
+                                            TcSeqState& st) {
+    const float2 nref = make_float2(-ref2, -ref2);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; k2 += 4) {
+        float2 w0 = make_float2(__uint_as_float(r[k2]), __uint_as_float(r[k2 + 1]));
+        float2 w1 = make_float2(__uint_as_float(r[k2 + 2]), __uint_as_float(r[k2 + 3]));
+        if (kMasked) {
+            if (k2 >= nvalid) w0.x = -INFINITY;
+            if (k2 + 1 >= nvalid) w0.y = -INFINITY;
+            if (k2 + 2 >= nvalid) w1.x = -INFINITY;
+            if (k2 + 3 >= nvalid) w1.y = -INFINITY;
+        }
+        st.mxa = fmaxf(st.mxa, fmaxf(w0.x, w0.y));
+        st.mxb = fmaxf(st.mxb, fmaxf(w1.x, w1.y));
+        const float2 a0 = f2_add(w0, nref), a1 = f2_add(w1, nref);
+        const float2 e0 = make_float2(fast_ex2(a0.x), fast_ex2(a0.y));  // 2^-inf = 0 for masked columns
+        const float2 e1 = make_float2(fast_ex2(a1.x), fast_ex2(a1.y));
+        st.sum2a = f2_add(st.sum2a, e0);
+        st.sum2b = f2_add(st.sum2b, e1);
+        const uint32_t h0 = tc_pack_bf16(e0.x, e0.y), h1 = tc_pack_bf16(e1.x, e1.y);
+        const float2 hf0 = make_float2(__uint_as_float(h0 << 16), __uint_as_float(h0 & 0xFFFF0000u));
+        const float2 hf1 = make_float2(__uint_as_float(h1 << 16), __uint_as_float(h1 & 0xFFFF0000u));
+        const float2 l0 = f2_fma(hf0, make_float2(-1.f, -1.f), e0);  // exact residuals
+        const float2 l1 = f2_fma(hf1, make_float2(-1.f, -1.f), e1);
+        o[k2 >> 1] = h0;
+        o[(k2 >> 1) + 1] = h1;
+        o[8 + (k2 >> 1)] = tc_pack_bf16(l0.x, l0.y);
+        o[8 + (k2 >> 1) + 1] = tc_pack_bf16(l1.x, l1.y);
+    }
+}
+
+// MAX pass: running maximum only
+template <bool kMasked>
+__device__ __forceinline__ void tc_max_chunk(const uint32_t* __restrict__ r, int nvalid, TcSeqState& st) {
+#pragma unroll
+    for (int k2 = 0; k2 < 16; k2 += 4) {
+        float w0 = __uint_as_float(r[k2]), w1 = __uint_as_float(r[k2 + 1]), w2 = __uint_as_float(r[k2 + 2]), w3 = __uint_as_float(r[k2 + 3]);
+        if (kMasked) {
+            if (k2 >= nvalid) w0 = -INFINITY;
+            if (k2 + 1 >= nvalid) w1 = -INFINITY;
+            if (k2 + 2 >= nvalid) w2 = -INFINITY;
+            if (k2 + 3 >= nvalid) w3 = -INFINITY;
+        }
+        st.mxa = fmaxf(st.mxa, fmaxf(w0, w1));
+        st.mxb = fmaxf(st.mxb, fmaxf(w2, w3));
+    }
+}
+
+// final pass: maximum (mxa), its window, and the runner-up weight
+template <bool kMasked>
+__device__ __forceinline__ void tc_final_chunk(const uint32_t* __restrict__ r, int nvalid, int j0, TcSeqState& st) {
+    // a chunk whose maximum is below the running runner-up changes nothing
+    float cma = -INFINITY, cmb = -INFINITY;
+#pragma unroll
+    for (int k2 = 0; k2 < 16; k2 += 4) {
+        float w0 = __uint_as_float(r[k2]), w1 = __uint_as_float(r[k2 + 1]), w2 = __uint_as_float(r[k2 + 2]), w3 = __uint_as_float(r[k2 + 3]);
+        if (kMasked) {
+            if (k2 >= nvalid) w0 = -INFINITY;
+            if (k2 + 1 >= nvalid) w1 = -INFINITY;
+            if (k2 + 2 >= nvalid) w2 = -INFINITY;
+            if (k2 + 3 >= nvalid) w3 = -INFINITY;
+        }
+        cma = fmaxf(cma, fmaxf(w0, w1));
+        cmb = fmaxf(cmb, fmaxf(w2, w3));
+    }
+    if (fmaxf(cma, cmb) > st.second) {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            const float w = (!kMasked || k2 < nvalid) ? __uint_as_float(r[k2]) : -INFINITY;
+            if (w > st.mxa) {
+                st.second = st.mxa;
+                st.mxa = w;
+                st.best_j = j0 + 2 * k2;
+            } else {
+                st.second = fmaxf(st.second, w);
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void tc_ld4(uint32_t taddr, uint32_t* r) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(taddr));
 }
@@ -145,12 +272,6 @@ __device__ __forceinline__ void tc_split3(float x, uint32_t& hi, uint32_t& mid, 
     lo = __bfloat16_as_ushort(l);
 }
 
-// {e1, e0} -> packed bf16x2 (e0 in the low half: the lower K index)
-__device__ __forceinline__ uint32_t tc_pack_bf16(float e0, float e1) {
-    uint32_t d;
-    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(e1), "f"(e0));
-    return d;
-}
 
 // A tile is refined in PASSES over the whole sequence set.  EM iteration `it` (0-based) is one EM pass (E-step fused
 // with the M-step counts); the first two iterations are preceded by a MAX pass (GEMM1 + a per-sequence maximum, no
@@ -193,6 +314,17 @@ __host__ __device__ inline size_t tc_smem_bytes(int t, int n_blocks, int e_posit
     b += 32 * 8;                                                     // mbarriers, tmem slot
     return b + 128;
 }
+
+#ifdef PM_TC_TIMING
+// clock sums of CTA 0 into p.phase_clk: [0] softmax thread total [1] its wait for S blocks [2] for the counts of a
+// sequence [3] model updates [4] MMA thread: wait for P blocks [5] for one-hot arrays [6] for models / count buffers
+// [7] MMA thread total
+#define TC_T0() const long long tc_t0_ = clock64()
+#define TC_ACC(var) var += clock64() - tc_t0_
+#else
+#define TC_T0() do {} while (0)
+#define TC_ACC(var) do {} while (0)
+#endif
 
 // ---------------------------------------------------------------------------------------------------------
 // the kernel
@@ -295,8 +427,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             }
         }
     } else if (warp == 8) {
-        // ================= MMA issuer =================
-        if (lane == 0) {
+        // ================= MMA issuer: the warp stays converged, one elected lane issues =================
+        {
             constexpr uint32_t idesc_base = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kTcRows >> 4) << 24);
             constexpr uint32_t idesc2 = idesc_base | (1u << 16) | (static_cast<uint32_t>(K >> 3) << 17);
             constexpr uint32_t hi1 = (128u >> 4) | (1u << 14);  // SBO = 128 B, descriptor version 1
@@ -304,8 +436,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             const uint32_t e_addr = smem_u32(Ebuf) >> 4;
             const uint32_t eb16 = static_cast<uint32_t>(EB) >> 4;
             unsigned int blk = 0, sq_g1 = 0, sq_g2 = 0, oq = 0, sw = 0;
+            long long tm_p = 0, tm_e = 0, tm_d = 0;
+            const long long tm_begin = clock64();
 
-            auto issue_g1 = [&](const TcBlock& B, unsigned int buf, unsigned int sq) {
+            // terms: 3 = full precision; the MAX passes only need a reference within a few units: the leading term
+            auto issue_g1 = [&](const TcBlock& B, unsigned int buf, unsigned int sq, bool one_term) {
                 const uint32_t tS = tmem + cS + buf * NBLK;
 #pragma unroll 1
                 for (int sgi = 0; sgi < 2; ++sgi) {
@@ -314,15 +449,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     const uint32_t lo = ((e_addr + ((sq & 1) * 2 + sg.par) * eb16 + sg.i0) & 0x3FFFu) | (1u << 16);  // LBO = 16 B
                     const uint32_t idesc = idesc_base | (static_cast<uint32_t>(sg.n >> 3) << 17);
                     const uint32_t d = tS + sg.col;
+                    if (tc_elect()) {
 #pragma unroll
-                    for (int term = 0; term < 3; ++term) {
+                        for (int kb = 0; kb < KC / 4; ++kb) tc_mma(d, tmem + cD + 8 * kb, lo + 2 * kb, hi1, idesc, kb != 0);
+                        if (!one_term) {
 #pragma unroll
-                        for (int kb = 0; kb < KC / 4; ++kb) {
-                            tc_mma(d, tmem + cD + term * 2 * KC + 8 * kb, lo + 2 * kb, hi1, idesc, (term | kb) != 0);
+                            for (int term = 1; term < 3; ++term) {
+#pragma unroll
+                                for (int kb = 0; kb < KC / 4; ++kb) tc_mma(d, tmem + cD + term * 2 * KC + 8 * kb, lo + 2 * kb, hi1, idesc, true);
+                            }
                         }
                     }
+                    __syncwarp();
                 }
-                tc_commit(&s_full[buf]);
+                if (tc_elect()) tc_commit(&s_full[buf]);
+                __syncwarp();
             };
 
             for (unsigned int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -330,13 +471,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     const TcPass pass = tc_pass(ps, p.max_iters);
                     const bool with_counts = pass.kind == kTcPassEm;  // otherwise GEMM1 only
                     if (pass.new_model) {
+                        TC_T0();
                         tc_wait(&d_full[0], sw & 1);
+                        TC_ACC(tm_d);
                         ++sw;
                         tc_fence_after();
                     }
                     // first block of the sweep
-                    tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
-                    issue_g1(blocks[0], blk & 1, sq_g1);
+                    {
+                        TC_T0();
+                        tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
+                        TC_ACC(tm_e);
+                    }
+                    issue_g1(blocks[0], blk & 1, sq_g1, pass.kind == kTcPassMax);
                     if (blocks[0].last) ++sq_g1;
                     bool o_acc = false;
 #pragma unroll 1
@@ -344,15 +491,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         const TcBlock B = blocks[n];
                         if (n + 1 < NB) {
                             const TcBlock& B1 = blocks[n + 1];
-                            if (B1.first) tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
-                            issue_g1(B1, (blk + 1) & 1, sq_g1);
+                            if (B1.first) {
+                                TC_T0();
+                                tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
+                                TC_ACC(tm_e);
+                            }
+                            issue_g1(B1, (blk + 1) & 1, sq_g1, pass.kind == kTcPassMax);
                             if (B1.last) ++sq_g1;
                         }
-                        tc_wait(&p_full[blk & 1], (blk >> 1) & 1);
+                        {
+                            TC_T0();
+                            tc_wait(&p_full[blk & 1], (blk >> 1) & 1);
+                            TC_ACC(tm_p);
+                        }
                         tc_fence_after();
                         if (with_counts) {
                             if (B.first) {
+                                TC_T0();
                                 tc_wait(&o_free[oq & 1], ((oq >> 1) & 1) ^ 1);
+                                TC_ACC(tm_d);
                                 tc_fence_after();
                                 o_acc = false;
                             }
@@ -362,26 +519,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             for (int sgi = 0; sgi < 2; ++sgi) {
                                 const TcSeg sg = B.seg[sgi];
                                 const uint32_t lo0 = ((e_addr + ((sq_g2 & 1) * 2 + sg.par) * eb16 + sg.i0) & 0x3FFFu) | ((128u >> 4) << 16);  // LBO = 128 B
+                                if (tc_elect()) {
 #pragma unroll 1
-                                for (int c = 0; c < sg.valid; c += 16) {
-                                    const uint32_t a = tS + sg.col + c;
-                                    tc_mma(tO, a, lo0 + c, hi2, idesc2, o_acc);
-                                    tc_mma(tO, a + 8, lo0 + c, hi2, idesc2, true);
-                                    o_acc = true;
+                                    for (int c = 0; c < sg.valid; c += 16) {
+                                        const uint32_t a = tS + sg.col + c;
+                                        tc_mma(tO, a, lo0 + c, hi2, idesc2, o_acc || c > 0);
+                                        tc_mma(tO, a + 8, lo0 + c, hi2, idesc2, true);
+                                    }
                                 }
+                                __syncwarp();
+                                if (sg.valid > 0) o_acc = true;
                             }
                             if (B.last) {
-                                tc_commit(&o_full[oq & 1]);
+                                if (tc_elect()) tc_commit(&o_full[oq & 1]);
+                                __syncwarp();
                                 ++oq;
                             }
                         }
                         if (B.last) {
-                            tc_commit(&e_empty[sq_g2 & 1]);
+                            if (tc_elect()) tc_commit(&e_empty[sq_g2 & 1]);
+                            __syncwarp();
                             ++sq_g2;
                         }
                     }
                 }
             }
+            (void)tm_p; (void)tm_e; (void)tm_d; (void)tm_begin;
         }
         __syncwarp();
     } else {
@@ -397,6 +560,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
         for (int r = 0; r < 4; ++r) lbg_tot[r] = log(fmax(p.tot_sym[r] / p.tot_bases, 1e-9));
 
         unsigned int blk = 0, oq = 0, xq = 0;
+        long long ts_s = 0, ts_o = 0, ts_u = 0, ts_kind[3] = {0, 0, 0}, ts_close = 0;
+        const long long ts_begin = clock64();
         for (unsigned int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
             const unsigned int wi = tile * kTcRows + row;
             const bool live = wi < n_work;
@@ -437,6 +602,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 // ---- theta of this iteration -> log-odds terms in tensor memory.  Iteration 0: acc holds theta0 itself;
                 // otherwise acc holds the expected counts of the previous EM pass (M-step, refine.hpp:227-269).
                 if (pass.new_model) {
+                    TC_T0();
                     if (pass.it > 0) {
                         // background = symbol totals - expected motif counts, clamped at 0 (refine.hpp:241-253)
                         float part[4] = {0.f, 0.f, 0.f, 0.f};
@@ -474,38 +640,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         }
                     }
                     // per column: write_column (refine.hpp:256-269), expectation = sum_c max_r theta[r][c]
-                    // (refine.hpp:130-136) and the log-odds D[c][r] = log max(theta,1e-9) - log max(bg,1e-9) in log2
-                    // units as three bf16 terms
-                    double ex_part = 0.0;
+                    // (refine.hpp:130-136) and the log-odds D[c][r] = log2 max(theta,1e-9) - log2 max(bg,1e-9) as three
+                    // bf16 terms.  FP32 throughout: the counts are FP32 sums; log2f is accurate to 1 ulp (2e-6 at |D| = 20).
+                    float ex_part = 0.f;
                     uint32_t dcol[3][2 * HP];
+                    float lbg2[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) lbg2[r] = static_cast<float>(lbg[r] * 1.4426950408889634);
 #pragma unroll
                     for (int c = 0; c < HP; ++c) {
                         const bool col_live = c_lo + c < l;
-                        double v[4];
+                        float v[4];
                         if (pass.it > 0) {
-                            double cs = 0.0;
-#pragma unroll
-                            for (int r = 0; r < 4; ++r) cs += static_cast<double>(acc[4 * c + r]);
-                            double f2 = 0.0;
+                            const float cs = (acc[4 * c] + acc[4 * c + 1]) + (acc[4 * c + 2] + acc[4 * c + 3]);
+                            const float ics = 1.f / cs;
+                            float f2 = 0.f;
 #pragma unroll
                             for (int r = 0; r < 4; ++r) {
-                                v[r] = cs > 0.0 ? fmax(static_cast<double>(acc[4 * c + r]) / cs, 1e-9) : 0.25;
+                                v[r] = cs > 0.f ? fmaxf(acc[4 * c + r] * ics, 1e-9f) : 0.25f;
                                 f2 += v[r];
                             }
+                            const float if2 = 1.f / f2;
 #pragma unroll
-                            for (int r = 0; r < 4; ++r) v[r] /= f2;
+                            for (int r = 0; r < 4; ++r) v[r] *= if2;
                         } else {
 #pragma unroll
-                            for (int r = 0; r < 4; ++r) v[r] = static_cast<double>(acc[4 * c + r]);
+                            for (int r = 0; r < 4; ++r) v[r] = acc[4 * c + r];
                         }
                         float d2[4];
-                        double mx = 0.0;
+                        float mx = 0.f;
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
-                            mx = fmax(mx, v[r]);
-                            d2[r] = col_live ? static_cast<float>((log(fmax(v[r], 1e-9)) - lbg[r]) * 1.4426950408889634) : 0.f;
+                            mx = fmaxf(mx, v[r]);
+                            d2[r] = col_live ? log2f(fmaxf(v[r], 1e-9f)) - lbg2[r] : 0.f;
                             if (p.out_theta && live && col_live && final_sweep)
-                                p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + (c_lo + c + 1)] = v[r];
+                                p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + (c_lo + c + 1)] = static_cast<double>(v[r]);
                         }
                         if (col_live) ex_part += mx;
                         uint32_t h[4], m[4], lw[4];
@@ -525,24 +694,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     }
                     tc_wait_st();
                     // expectation: partner exchange
-                    reinterpret_cast<double*>(&xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row])[0] = ex_part;
+                    reinterpret_cast<double*>(&xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row])[0] = static_cast<double>(ex_part);
                     tc_fence_before();
                     tc_named_sync();
                     {
                         const double oex = reinterpret_cast<const double*>(&xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row])[0];
                         ++xq;
-                        expct = wg == 0 ? ex_part + oex : oex + ex_part;
+                        expct = wg == 0 ? static_cast<double>(ex_part) + oex : oex + static_cast<double>(ex_part);
                     }
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(&d_full[0]);
 #pragma unroll
                     for (int e = 0; e < 4 * HP; ++e) acc[e] = 0.f;
+                    TC_ACC(ts_u);
                 }
 
                 // ---- the sweep: every sequence, block by block
+#ifdef PM_TC_TIMING
+                const long long ts_pass0 = clock64();
+#endif
                 double ll = 0.0;
-                float ref2 = 0.f, sum = 0.f, mxw = -INFINITY, second = -INFINITY;
-                int best_j = 0;
+                float ref2 = 0.f;
+                TcSeqState st = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), -INFINITY, -INFINITY, -INFINITY, 0};
                 uint32_t prof8[KC];  // final sweep, warpgroup 0: symbol counts of the argmax rows (one byte per symbol)
 #pragma unroll
                 for (int c = 0; c < KC; ++c) prof8[c] = 0;
@@ -550,7 +723,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 float pend_inv = 0.f;
                 unsigned int pend_oq = 0;
                 auto fold_pending = [&]() {
-                    tc_wait(&o_full[pend_oq & 1], (pend_oq >> 1) & 1);
+                    {
+                        TC_T0();
+                        tc_wait(&o_full[pend_oq & 1], (pend_oq >> 1) & 1);
+                        TC_ACC(ts_o);
+                    }
                     tc_fence_after();
                     const uint32_t src = tO + (pend_oq & 1) * K + 4 * c_lo;
 #pragma unroll
@@ -584,59 +761,77 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     const int i = B.seq;
                     if (B.first) {
                         ref2 = mprev[i * kTcRows + row];  // this sequence's maximum in the MAX pass / previous iteration
-                        sum = 0.f;
-                        mxw = -INFINITY;
-                        second = -INFINITY;
-                        best_j = 0;
+                        st.sum2a = make_float2(0.f, 0.f);
+                        st.sum2b = make_float2(0.f, 0.f);
+                        st.mxa = -INFINITY;
+                        st.mxb = -INFINITY;
+                        st.second = -INFINITY;
+                        st.best_j = 0;
                     }
-                    tc_wait(&s_full[blk & 1], (blk >> 1) & 1);
+#ifdef PM_TC_TIMING
+                    const bool trace = blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 4) && tile == 0 && (ps == 5 || ps == 0) && n >= 10 && n < 13;
+                    long long tr[8];
+                    int trn = 0;
+                    if (trace) tr[trn++] = clock64();
+#endif
+                    {
+                        TC_T0();
+                        tc_wait(&s_full[blk & 1], (blk >> 1) & 1);
+                        TC_ACC(ts_s);
+                    }
                     tc_fence_after();
+#ifdef PM_TC_TIMING
+                    if (trace) tr[trn++] = clock64();
+#endif
                     const uint32_t tB = tS + (blk & 1) * NBLK;
                     const int half = B.ncols >> 1;
+                    const int c_begin = wg * half, c_end = c_begin + half;
 #pragma unroll 1
-                    for (int cc = wg * half; cc < (wg + 1) * half; cc += 16) {
-                        // segment of this 16-column chunk
-                        const TcSeg sg = (B.seg[1].n != 0 && cc >= B.seg[1].col) ? B.seg[1] : B.seg[0];
-                        const int rel = cc - sg.col;
-                        const int nvalid = rel < sg.n ? min(max(static_cast<int>(sg.valid) - rel, 0), 16) : 0;
-                        if (nvalid == 0) continue;  // dead columns: the MMA issuer skips them too
-                        uint32_t r[16];
-                        tc_ld16(tB + cc, r);
-                        tc_wait_ld();
-                        if (max_pass) {
-#pragma unroll
-                            for (int k2 = 0; k2 < 16; ++k2) mxw = fmaxf(mxw, k2 < nvalid ? __uint_as_float(r[k2]) : -INFINITY);
-                        } else if (em_pass) {
-                            float e[16];
-#pragma unroll
-                            for (int k2 = 0; k2 < 16; ++k2) {
-                                const float w = __uint_as_float(r[k2]);
-                                const bool ok = k2 < nvalid;
-                                mxw = fmaxf(mxw, ok ? w : -INFINITY);
-                                e[k2] = ok ? fast_ex2(w - ref2) : 0.f;
-                                sum += e[k2];
+                    for (int sgi = 0; sgi < 2; ++sgi) {
+                        // my columns of this segment: [lo, hi), of which those below vend are real windows
+                        const TcSeg sg = B.seg[sgi];
+                        const int lo = max(c_begin, static_cast<int>(sg.col)), hi = min(c_end, sg.col + sg.n);
+                        const int vend = min(hi, sg.col + sg.valid);
+                        int cc = lo;
+                        int j = 2 * (sg.i0 + lo - sg.col) + sg.par;
+#pragma unroll 1
+                        for (; cc + 32 <= vend; cc += 32, j += 64) {  // two full chunks: no masks
+                            uint32_t r[32];
+                            tc_ld32(tB + cc, r);
+                            tc_wait_ld();
+#ifdef PM_TC_TIMING
+                            if (trace && trn < 7) tr[trn++] = clock64();
+#endif
+                            if (em_pass) {
+                                uint32_t o[32];
+                                tc_em_chunk<false>(r, o, 16, ref2, st);
+                                tc_em_chunk<false>(r + 16, o + 16, 16, ref2, st);
+                                tc_st32(tB + cc, o);
+                            } else if (max_pass) {
+                                tc_max_chunk<false>(r, 16, st);
+                                tc_max_chunk<false>(r + 16, 16, st);
+                            } else {
+                                tc_final_chunk<false>(r, 16, j, st);
+                                tc_final_chunk<false>(r + 16, 16, j + 32, st);
                             }
-                            uint32_t o[16];
-#pragma unroll
-                            for (int k2 = 0; k2 < 16; k2 += 2) {
-                                const uint32_t h = tc_pack_bf16(e[k2], e[k2 + 1]);
-                                const float h0 = __uint_as_float(h << 16), h1 = __uint_as_float(h & 0xFFFF0000u);
-                                o[k2 >> 1] = h;
-                                o[8 + (k2 >> 1)] = tc_pack_bf16(e[k2] - h0, e[k2 + 1] - h1);
-                            }
-                            tc_st16(tB + cc, o);
-                        } else {
-                            const int j0 = 2 * (sg.i0 + rel) + sg.par;
-#pragma unroll
-                            for (int k2 = 0; k2 < 16; ++k2) {
-                                const float w = k2 < nvalid ? __uint_as_float(r[k2]) : -INFINITY;
-                                if (w > mxw) {
-                                    second = mxw;
-                                    mxw = w;
-                                    best_j = j0 + 2 * k2;
-                                } else {
-                                    second = fmaxf(second, w);
-                                }
+#ifdef PM_TC_TIMING
+                            if (trace && trn < 7) tr[trn++] = clock64();
+#endif
+                        }
+#pragma unroll 1
+                        for (; cc < vend; cc += 16, j += 32) {  // at most one full chunk and the tail (dead chunks are skipped)
+                            const int nv = min(vend - cc, 16);
+                            uint32_t r[16];
+                            tc_ld16(tB + cc, r);
+                            tc_wait_ld();
+                            if (em_pass) {
+                                uint32_t o[16];
+                                tc_em_chunk<true>(r, o, nv, ref2, st);
+                                tc_st16(tB + cc, o);
+                            } else if (max_pass) {
+                                tc_max_chunk<true>(r, nv, st);
+                            } else {
+                                tc_final_chunk<true>(r, nv, j, st);
                             }
                         }
                     }
@@ -644,12 +839,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(&p_full[blk & 1]);
+#ifdef PM_TC_TIMING
+                    if (trace) {
+                        tr[trn++] = clock64();
+                        printf("[trace] warp %d pass %d block %d ncols %d:", warp, ps, n, (int)B.ncols);
+                        for (int q = 1; q < trn; ++q) printf(" +%lld", tr[q] - tr[q - 1]);
+                        printf("  (start %lld)\n", tr[0]);
+                    }
+#endif
 
                     if (pending) fold_pending();  // the previous sequence's counts: its GEMM2 finished long ago
 
                     if (B.last) {
+                        TC_T0();
                         // ---- close the sequence: both column halves -> maximum, normaliser, likelihood term
-                        float4 mine = make_float4(sum, mxw, second, __int_as_float(best_j));
+                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), fmaxf(st.mxa, st.mxb), st.second, __int_as_float(st.best_j));
                         xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = mine;
                         tc_named_sync();
                         const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
@@ -682,9 +886,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
 #pragma unroll
                             for (int c = 0; c < KC; ++c) prof8[c] += 1u << (8 * (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u));
                         }
+                        TC_ACC(ts_close);
                     }
                 }
                 if (pending) fold_pending();
+#ifdef PM_TC_TIMING
+                ts_kind[pass.kind] += clock64() - ts_pass0;
+#endif
 
                 if (em_pass) {
                     // ---- log-likelihood of the model that entered this iteration and the stop test (refine.hpp:296-304)
@@ -735,6 +943,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 }
             }
         }
+#ifdef PM_TC_TIMING
+        if (blockIdx.x == 0 && tid == 0) {
+            atomicAdd(p.phase_clk + 0, static_cast<unsigned long long>(clock64() - ts_begin));
+            atomicAdd(p.phase_clk + 1, static_cast<unsigned long long>(ts_s));
+            atomicAdd(p.phase_clk + 2, static_cast<unsigned long long>(ts_o));
+            atomicAdd(p.phase_clk + 3, static_cast<unsigned long long>(ts_u));
+            atomicAdd(p.phase_clk + 4, static_cast<unsigned long long>(ts_kind[kTcPassEm]));
+            atomicAdd(p.phase_clk + 5, static_cast<unsigned long long>(ts_kind[kTcPassMax]));
+            atomicAdd(p.phase_clk + 6, static_cast<unsigned long long>(ts_kind[kTcPassFinal]));
+            atomicAdd(p.phase_clk + 7, static_cast<unsigned long long>(ts_close));
+        }
+#endif
     }
 
     tc_fence_before();
