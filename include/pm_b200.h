@@ -183,6 +183,23 @@ int pm_enriched_buckets(pm_ctx* ctx, int l, const int32_t* kept, int k, int s, i
 int pm_refine(pm_ctx* ctx, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
               double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
               int32_t* iterations, double* theta, double* ll_trace);
+/* The same refinement entirely in FP64, in the reference's own operation order (one CTA per bucket, not a throughput
+ * path).  run() uses it to settle candidates of equal score whose expectations differ by less than the FP32 error
+ * (detail::candidate_improves compares doubles exactly, driver.hpp:127-135). */
+int pm_refine_exact(pm_ctx* ctx, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
+                    double tol, char* consensus, int32_t* positions, int32_t* score, double* expectation,
+                    int32_t* iterations, double* theta, double* ll_trace);
+/* init_model, refine.hpp:90-127: theta0 (4 x (l+1), MotifModel layout refine.hpp:65-71) of a member list with a
+ * pseudocount; the background column holds the symbol frequencies of the whole set.  Errors: empty member list
+ * (EmptyBucket), negative pseudocount (InvalidParams). */
+int pm_init_model(pm_ctx* ctx, int l, const int32_t* members, int n_members, double pseudocount, double* theta_out);
+/* em_step, refine.hpp:216-282: one E-step + M-step from theta_in; *log_likelihood is the OOPS likelihood of theta_in
+ * (refine.hpp:209).  pm_em_step runs the production EM kernel (FP32 sums, FP64 normalisation), pm_em_step_exact the FP64
+ * kernel. */
+int pm_em_step(pm_ctx* ctx, int l, const double* theta_in, double* theta_out, double* log_likelihood);
+int pm_em_step_exact(pm_ctx* ctx, int l, const double* theta_in, double* theta_out, double* log_likelihood);
+/* expectation, refine.hpp:130-136 (host arithmetic on a 4 x (l+1) model). */
+int pm_expectation(const double* theta, int l, double* out);
 /* score / consensus of a start vector, scoring.hpp:111-131 (starts 1-based). */
 int pm_score(pm_ctx* ctx, int l, const int32_t* starts, int* score, char* consensus /* l+1 */);
 /* XOR/popcount Hamming scan of candidate v over every window: per-sequence minimum distance

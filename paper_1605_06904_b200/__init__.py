@@ -107,7 +107,8 @@ EXPORTS = [
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
-    "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_score",
+    "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_refine_exact",
+    "pm_init_model", "pm_em_step", "pm_em_step_exact", "pm_expectation", "pm_score",
     "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host",
 ]
 
@@ -252,6 +253,14 @@ def resolve_params(offs, **kw):
     return dict(k=out.k, s=out.s, m=out.m, q=out.q, t_hat=out.t_hat)
 
 
+def expectation(theta, l):
+    """expectation, refine.hpp:130-136."""
+    tin = np.ascontiguousarray(theta, dtype=np.float64).reshape(-1)
+    out = C.c_double()
+    _check(lib().pm_expectation(_p(tin, C.c_double), l, C.byref(out)))
+    return out.value
+
+
 def candidate_improves(a, b):
     """a, b: (score, expectation, key)."""
     return bool(lib().pm_candidate_improves(a[0], C.c_double(a[1]), C.c_uint64(a[2]), b[0], C.c_double(b[1]),
@@ -371,8 +380,9 @@ class Context:
         return [dict(key=int(keys[b]), size=int(sizes[b]), overflowed=bool(over[b]),
                      members=members[moff[b]:moff[b + 1]].tolist()) for b in range(n)]
 
-    def refine(self, l, member_lists, max_iters=5, tol=1e-6, z_epsilon=-1.0):
-        """refine() for a batch of buckets; member_lists: list of lists of flat l-mer indices."""
+    def refine(self, l, member_lists, max_iters=5, tol=1e-6, z_epsilon=-1.0, exact=False):
+        """refine() for a batch of buckets; member_lists: list of lists of flat l-mer indices.
+        exact=True runs the FP64 kernel (pm_refine_exact) instead of the production kernels."""
         nb = len(member_lists)
         moff = np.zeros(nb + 1, dtype=np.int64)
         for b, m in enumerate(member_lists):
@@ -385,15 +395,36 @@ class Context:
         its = np.zeros(max(nb, 1), dtype=np.int32)
         theta = np.zeros((max(nb, 1), 4, l + 1), dtype=np.float64)
         ll = np.zeros((max(nb, 1), max_iters), dtype=np.float64)
-        _check(lib().pm_refine(self._h, l, _p(members, C.c_int32), _p(moff, C.c_int64), nb, max_iters, C.c_double(tol),
-                               C.c_double(z_epsilon), cons, _p(pos, C.c_int32), _p(score, C.c_int32),
-                               _p(exp_, C.c_double), _p(its, C.c_int32), _p(theta, C.c_double), _p(ll, C.c_double)))
+        if exact:
+            _check(lib().pm_refine_exact(self._h, l, _p(members, C.c_int32), _p(moff, C.c_int64), nb, max_iters,
+                                         C.c_double(tol), cons, _p(pos, C.c_int32), _p(score, C.c_int32),
+                                         _p(exp_, C.c_double), _p(its, C.c_int32), _p(theta, C.c_double), _p(ll, C.c_double)))
+        else:
+            _check(lib().pm_refine(self._h, l, _p(members, C.c_int32), _p(moff, C.c_int64), nb, max_iters, C.c_double(tol),
+                                   C.c_double(z_epsilon), cons, _p(pos, C.c_int32), _p(score, C.c_int32),
+                                   _p(exp_, C.c_double), _p(its, C.c_int32), _p(theta, C.c_double), _p(ll, C.c_double)))
         out = []
         for b in range(nb):
             out.append(dict(consensus=cons.raw[32 * b: 32 * b + l].decode(), positions=pos[b].tolist(),
                             score=int(score[b]), expectation=float(exp_[b]), iterations=int(its[b]),
                             theta=theta[b].copy(), ll_trace=ll[b, : int(its[b])].tolist()))
         return out
+
+    def init_model(self, l, members, pseudocount=0.0):
+        """init_model, refine.hpp:90-127 -> theta0 as a (4, l+1) array (column 0 = background)."""
+        m = _i32(members)
+        theta = np.zeros((4, l + 1), dtype=np.float64)
+        _check(lib().pm_init_model(self._h, l, _p(m, C.c_int32), len(m), C.c_double(pseudocount), _p(theta, C.c_double)))
+        return theta
+
+    def em_step(self, l, theta, exact=False):
+        """em_step, refine.hpp:216-282 -> (theta', log-likelihood of theta)."""
+        tin = np.ascontiguousarray(theta, dtype=np.float64).reshape(-1)
+        tout = np.zeros_like(tin)
+        ll = C.c_double()
+        fn = lib().pm_em_step_exact if exact else lib().pm_em_step
+        _check(fn(self._h, l, _p(tin, C.c_double), _p(tout, C.c_double), C.byref(ll)))
+        return tout.reshape(4, l + 1), ll.value
 
     def score(self, l, starts):
         st = _i32(starts)

@@ -29,6 +29,7 @@
 #include "pm_em_smem.cuh"
 #include "pm_em_pair.cuh"
 #include "pm_em_tc.cuh"
+#include "pm_em_f64.cuh"
 #include "pm_hash_fused.cuh"
 
 using namespace pm;
@@ -60,7 +61,9 @@ enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
     S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
-    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_COUNT_
+    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_THETA_IN, S_NCLOSE,
+    // the FP64 path has its own scratch: run() calls it while a batch's buffers are still live
+    S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
 };
 
 }  // namespace
@@ -986,6 +989,50 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     return check_launch(c, "em_refine");
 }
 
+// refine() in FP64 (pm_em_f64.cuh), one CTA per work item.  steps_only: exactly max_iters em_step()s from theta_in.
+int launch_em_f64(pm_ctx* c, int l, int max_iters, double tol, const k::WorkDesc* work, unsigned int n_work,
+                  const unsigned int* members, const EmOut& o, unsigned long long* d_scal, const double* theta_in,
+                  bool steps_only, const unsigned int* out_map = nullptr) {
+    k::EmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.seq_len = c->d_seq_len;
+    p.win_off = c->d_win_off;
+    p.seq_sym = c->d_seq_sym;
+    p.seq_logw = c->d_seq_logw;
+    for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
+    p.tot_bases = static_cast<double>(c->total_bases);
+    p.t = c->t;
+    p.l = l;
+    p.max_iters = max_iters;
+    p.tol = tol;
+    p.work = work;
+    p.n_work_dev = nullptr;
+    p.n_work = n_work;
+    p.members = members;
+    p.out_score = o.score;
+    p.out_iters = o.iters;
+    p.out_exp = o.expct;
+    p.out_cons = o.cons;
+    p.out_pos = o.pos;
+    p.out_theta = o.theta;
+    p.out_ll = o.ll;
+    p.iter_total = d_scal;
+    p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
+    p.out_map = out_map;
+    p.theta_in = theta_in;
+    k::F64Extra x;
+    const size_t per_cta = static_cast<size_t>(std::max<int64_t>(c->x, 1));
+    const unsigned int grid = static_cast<unsigned int>(std::max<size_t>(
+        1, std::min<size_t>({static_cast<size_t>(n_work), static_cast<size_t>(2 * c->sm_count), (512u << 20) / (per_cta * 8)})));
+    PM_TRY(get_buf(c, S_F64_Z, per_cta * grid, &x.zbuf));
+    x.x = c->x;
+    x.steps_only = steps_only ? 1 : 0;
+    k::em_refine_f64_kernel<<<grid, k::kF64Threads, 0, c->stream>>>(p, x);
+    return check_launch(c, "em_refine_f64");
+}
+
 void unpack_consensus(uint64_t bits, int l, char* out) {
     static const char sym[4] = {'A', 'C', 'T', 'G'};
     for (int c = 0; c < l; ++c) out[c] = sym[(bits >> (62 - 2 * c)) & 3];
@@ -1343,21 +1390,28 @@ int pm_enriched_buckets(pm_ctx* c, int l, const int32_t* kept, int kk, int s, in
     return PM_OK;
 }
 
-int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
-              double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
-              int32_t* iterations, double* theta, double* ll_trace) {
+}  // extern "C"
+
+namespace {
+
+// refine() for n_buckets member lists: the production kernels (exact == false) or the FP64 kernel; theta_in
+// (n_buckets models) replaces init_model and steps_only turns the call into max_iters em_step()s.
+int refine_common(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
+                  double tol, double z_epsilon, bool exact, const double* theta_in, bool steps_only, char* consensus,
+                  int32_t* positions, int32_t* score, double* expectation, int32_t* iterations, double* theta,
+                  double* ll_trace) {
     clear_error();
     PM_TRY(need_sequences(c));
+    if (c != nullptr) PM_CUDA(cudaSetDevice(c->device));
     PM_TRY(prepare_windows(c, l));
     if (max_iters < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one EM iteration");
     if (n_buckets < 1) return PM_OK;
-    PM_CUDA(cudaSetDevice(c->device));
-    const int64_t n_mem = mem_off[n_buckets];
+    const int64_t n_mem = mem_off ? mem_off[n_buckets] : 0;
     std::vector<k::WorkDesc> work(static_cast<size_t>(n_buckets));
     for (int b = 0; b < n_buckets; ++b) {
-        const int64_t cnt = mem_off[b + 1] - mem_off[b];
-        if (cnt < 1) return set_error(PM_ERR_EMPTY_BUCKET, "cannot build a motif model from an empty bucket");
-        work[static_cast<size_t>(b)].mem_begin = mem_off[b];
+        const int64_t cnt = mem_off ? mem_off[b + 1] - mem_off[b] : 0;
+        if (cnt < 1 && theta_in == nullptr) return set_error(PM_ERR_EMPTY_BUCKET, "cannot build a motif model from an empty bucket");
+        work[static_cast<size_t>(b)].mem_begin = mem_off ? mem_off[b] : 0;
         work[static_cast<size_t>(b)].key = 0;
         work[static_cast<size_t>(b)].count = static_cast<unsigned int>(cnt);
         work[static_cast<size_t>(b)].trial = b;
@@ -1366,33 +1420,45 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
         if (members[i] < 0 || members[i] >= c->x) return set_error(PM_ERR_INDEX_OUT_OF_RANGE, "member l-mer index out of range");
     }
     const size_t nb = static_cast<size_t>(n_buckets);
+    const size_t TH = 4 * static_cast<size_t>(l + 1);
     unsigned int* d_mem;
     k::WorkDesc* d_work;
     unsigned long long* d_scal;
+    double* d_theta_in = nullptr;
     EmOut o;
-    PM_TRY(get_buf(c, S_MEMBERS, static_cast<size_t>(n_mem), &d_mem));
-    PM_TRY(get_buf(c, S_WORK, nb, &d_work));
-    PM_TRY(get_buf(c, S_SCAL, 16, &d_scal));
-    PM_TRY(get_buf(c, S_OUT_SCORE, nb, &o.score));
-    PM_TRY(get_buf(c, S_OUT_ITERS, nb, &o.iters));
-    PM_TRY(get_buf(c, S_OUT_EXP, nb, &o.expct));
-    PM_TRY(get_buf(c, S_OUT_CONS, nb, &o.cons));
-    PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
-    if (theta) PM_TRY(get_buf(c, S_OUT_THETA, nb * 4 * static_cast<size_t>(l + 1), &o.theta));
+    const bool xs = exact;  // scratch set
+    PM_TRY(get_buf(c, xs ? S_X_MEMBERS : S_MEMBERS, static_cast<size_t>(std::max<int64_t>(n_mem, 1)), &d_mem));
+    PM_TRY(get_buf(c, xs ? S_X_WORK : S_WORK, nb, &d_work));
+    PM_TRY(get_buf(c, xs ? S_X_SCAL : S_SCAL, 16, &d_scal));
+    PM_TRY(get_buf(c, xs ? S_X_SCORE : S_OUT_SCORE, nb, &o.score));
+    PM_TRY(get_buf(c, xs ? S_X_ITERS : S_OUT_ITERS, nb, &o.iters));
+    PM_TRY(get_buf(c, xs ? S_X_EXP : S_OUT_EXP, nb, &o.expct));
+    PM_TRY(get_buf(c, xs ? S_X_CONS : S_OUT_CONS, nb, &o.cons));
+    PM_TRY(get_buf(c, xs ? S_X_POS : S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
+    if (theta) PM_TRY(get_buf(c, xs ? S_X_THETA : S_OUT_THETA, nb * TH, &o.theta));
+    if (theta_in) {
+        PM_TRY(get_buf(c, xs ? S_X_THETA_IN : S_THETA_IN, nb * TH, &d_theta_in));
+        PM_TRY(h2d(c, d_theta_in, theta_in, sizeof(double) * nb * TH));
+    }
     if (ll_trace) {
-        PM_TRY(get_buf(c, S_OUT_LL, nb * static_cast<size_t>(max_iters), &o.ll));
+        PM_TRY(get_buf(c, xs ? S_X_LL : S_OUT_LL, nb * static_cast<size_t>(max_iters), &o.ll));
         std::vector<double> nan_fill(nb * static_cast<size_t>(max_iters), std::numeric_limits<double>::quiet_NaN());
         PM_TRY(h2d(c, o.ll, nan_fill.data(), sizeof(double) * nan_fill.size()));
         PM_CUDA(cudaStreamSynchronize(c->stream));
     }
-    PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem)));
+    if (n_mem > 0) PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_mem)));
     PM_TRY(h2d(c, d_work, work.data(), sizeof(k::WorkDesc) * nb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
-    unsigned int max_count = 0;
-    for (const k::WorkDesc& w : work) max_count = std::max(max_count, w.count);
-    PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
-                     static_cast<unsigned int>(n_buckets), d_mem, o, d_scal,
-                     static_cast<int>(std::min<unsigned int>(max_count, 1u << 30))));
+    if (exact) {
+        PM_TRY(launch_em_f64(c, l, max_iters, tol, d_work, static_cast<unsigned int>(n_buckets), d_mem, o, d_scal, d_theta_in,
+                             steps_only));
+    } else {
+        unsigned int max_count = 0;
+        for (const k::WorkDesc& w : work) max_count = std::max(max_count, w.count);
+        PM_TRY(launch_em(c, l, max_iters, tol, z_epsilon, d_work, nullptr, static_cast<unsigned int>(n_buckets),
+                         static_cast<unsigned int>(n_buckets), d_mem, o, d_scal,
+                         static_cast<int>(std::min<unsigned int>(max_count, 1u << 30)), d_theta_in));
+    }
     std::vector<int32_t> hs(nb), hi(nb);
     std::vector<double> he(nb);
     std::vector<uint64_t> hc(nb);
@@ -1403,11 +1469,13 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
     PM_TRY(d2h(c, hc.data(), o.cons, sizeof(uint64_t) * nb));
     PM_TRY(d2h(c, scal, d_scal, sizeof(scal)));
     if (positions) PM_TRY(d2h(c, positions, o.pos, sizeof(int32_t) * nb * static_cast<size_t>(c->t)));
-    if (theta) PM_TRY(d2h(c, theta, o.theta, sizeof(double) * nb * 4 * static_cast<size_t>(l + 1)));
+    if (theta) PM_TRY(d2h(c, theta, o.theta, sizeof(double) * nb * TH));
     if (ll_trace) PM_TRY(d2h(c, ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
-    c->em_exact[0] = static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
-    for (int r = 0; r < 4; ++r) c->em_exact[1 + r] = static_cast<int64_t>(scal[4 + r]);
+    if (!exact) {
+        c->em_exact[0] = static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
+        for (int r = 0; r < 4; ++r) c->em_exact[1 + r] = static_cast<int64_t>(scal[4 + r]);
+    }
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
@@ -1417,6 +1485,96 @@ int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, 
         if (expectation) expectation[b] = he[b];
         if (consensus) unpack_consensus(hc[b], l, consensus + 32 * b);
     }
+    return PM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_refine(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
+              double tol, double z_epsilon, char* consensus, int32_t* positions, int32_t* score, double* expectation,
+              int32_t* iterations, double* theta, double* ll_trace) {
+    return refine_common(c, l, members, mem_off, n_buckets, max_iters, tol, z_epsilon, false, nullptr, false, consensus,
+                         positions, score, expectation, iterations, theta, ll_trace);
+}
+
+int pm_refine_exact(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_off, int n_buckets, int max_iters,
+                    double tol, char* consensus, int32_t* positions, int32_t* score, double* expectation,
+                    int32_t* iterations, double* theta, double* ll_trace) {
+    return refine_common(c, l, members, mem_off, n_buckets, max_iters, tol, -1.0, true, nullptr, false, consensus, positions,
+                         score, expectation, iterations, theta, ll_trace);
+}
+
+int pm_init_model(pm_ctx* c, int l, const int32_t* members, int n_members, double pseudocount, double* theta_out) {
+    clear_error();
+    PM_TRY(need_sequences(c));
+    PM_CUDA(cudaSetDevice(c->device));
+    PM_TRY(prepare_windows(c, l));
+    if (theta_out == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    if (n_members < 1) return set_error(PM_ERR_EMPTY_BUCKET, "cannot build a motif model from an empty bucket");
+    if (!(pseudocount >= 0.0)) return set_error(PM_ERR_INVALID_PARAMS, "pseudocount must be non-negative");
+    for (int i = 0; i < n_members; ++i) {
+        if (members[i] < 0 || members[i] >= c->x) return set_error(PM_ERR_INDEX_OUT_OF_RANGE, "member l-mer index out of range");
+    }
+    const size_t TH = 4 * static_cast<size_t>(l + 1);
+    k::WorkDesc wd{0, 0, static_cast<unsigned int>(n_members), 0};
+    unsigned int* d_mem;
+    k::WorkDesc* d_work;
+    double* d_theta;
+    PM_TRY(get_buf(c, S_MEMBERS, static_cast<size_t>(n_members), &d_mem));
+    PM_TRY(get_buf(c, S_WORK, 1, &d_work));
+    PM_TRY(get_buf(c, S_OUT_THETA, TH, &d_theta));
+    PM_TRY(h2d(c, d_mem, members, sizeof(int32_t) * static_cast<size_t>(n_members)));
+    PM_TRY(h2d(c, d_work, &wd, sizeof(wd)));
+    k::EmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.win_off = c->d_win_off;
+    for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
+    p.tot_bases = static_cast<double>(c->total_bases);
+    p.t = c->t;
+    p.l = l;
+    p.work = d_work;
+    p.n_work = 1;
+    p.members = d_mem;
+    p.out_theta = d_theta;
+    k::init_model_kernel<<<1, 128, 0, c->stream>>>(p, pseudocount);
+    PM_TRY(check_launch(c, "init_model"));
+    PM_TRY(d2h(c, theta_out, d_theta, sizeof(double) * TH));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    return PM_OK;
+}
+
+static int em_step_common(pm_ctx* c, int l, const double* theta_in, double* theta_out, double* log_likelihood, bool exact) {
+    if (theta_in == nullptr || theta_out == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    double ll = 0.0;
+    // one em_step() = one iteration from theta_in: theta' and the likelihood of theta_in (refine.hpp:209, :281)
+    const int rc = refine_common(c, l, nullptr, nullptr, 1, 1, 0.0, -1.0, exact, theta_in, exact, nullptr, nullptr, nullptr,
+                                 nullptr, nullptr, theta_out, &ll);
+    if (rc == PM_OK && log_likelihood) *log_likelihood = ll;
+    return rc;
+}
+
+int pm_em_step(pm_ctx* c, int l, const double* theta_in, double* theta_out, double* log_likelihood) {
+    return em_step_common(c, l, theta_in, theta_out, log_likelihood, false);
+}
+
+int pm_em_step_exact(pm_ctx* c, int l, const double* theta_in, double* theta_out, double* log_likelihood) {
+    return em_step_common(c, l, theta_in, theta_out, log_likelihood, true);
+}
+
+int pm_expectation(const double* theta, int l, double* out) {
+    clear_error();
+    if (theta == nullptr || out == nullptr || l < 1) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    double sum = 0.0;
+    for (int c = 1; c <= l; ++c) {  // refine.hpp:130-136: sum over motif columns of the column maximum
+        double mx = theta[c];
+        for (int r = 1; r < 4; ++r) mx = std::max(mx, theta[static_cast<size_t>(r) * (l + 1) + c]);
+        sum += mx;
+    }
+    *out = sum;
     return PM_OK;
 }
 
@@ -1517,21 +1675,25 @@ struct TrialSummary {  // device layout of S_TB: parallel arrays would need 6 co
     int32_t work;      // -1 when the trial has no enriched bucket
     int32_t score;
     int32_t iters;
-    int32_t pad;
+    int32_t n_close;   // other buckets of the trial whose score equals the best and whose expectation is within kTieEps
     double expct;
     uint64_t key;
     uint64_t cons;
 };
 
-__global__ void summarize_kernel(const int32_t* __restrict__ best_work, const k::WorkDesc* __restrict__ work,
-                                 const int32_t* __restrict__ score, const int32_t* __restrict__ iters,
-                                 const double* __restrict__ expct, const uint64_t* __restrict__ cons, int n_trials,
-                                 TrialSummary* __restrict__ out) {
+// Expectations of the FP32 kernels agree with the reference to ~1e-5; two candidates of equal score closer than this are
+// re-refined in FP64 before they are compared (the reference compares doubles exactly, driver.hpp:131-133).
+constexpr double kTieEps = 2e-4;
+
+__global__ void summarize_kernel(const int32_t* __restrict__ best_work, const int32_t* __restrict__ n_close,
+                                 const k::WorkDesc* __restrict__ work, const int32_t* __restrict__ score,
+                                 const int32_t* __restrict__ iters, const double* __restrict__ expct,
+                                 const uint64_t* __restrict__ cons, int n_trials, TrialSummary* __restrict__ out) {
     const int tr = blockIdx.x * blockDim.x + threadIdx.x;
     if (tr >= n_trials) return;
     TrialSummary s;
     s.work = best_work[tr];
-    s.pad = 0;
+    s.n_close = n_close[tr];
     if (s.work >= 0) {
         s.score = score[s.work];
         s.iters = iters[s.work];
@@ -1553,7 +1715,31 @@ struct RunState {
     TrialSummary best{};
     int64_t best_trial = 0;
     std::vector<int32_t> positions;
+    std::vector<int32_t> best_members;  // member list of the incumbent (kept so it can be re-refined in FP64 later)
+    bool best_exact = false;            // best.expct is the FP64 kernel's value
+    int32_t best_in_batch = -1;         // work item of the incumbent if it belongs to the batch being reduced
+    int64_t exact_refines = 0;          // FP64 re-refinements this run needed
 };
+
+// FP64 expectation (and score) of one member list: pm_em_f64.cuh through the stage path
+int exact_candidate(pm_ctx* c, const pm_run_config* cfg, const std::vector<int32_t>& members, double* expct, int32_t* score) {
+    const int64_t off[2] = {0, static_cast<int64_t>(members.size())};
+    return pm_refine_exact(c, cfg->l, members.data(), off, 1, cfg->max_em_iters, cfg->em_tol, nullptr, nullptr, score, expct,
+                           nullptr, nullptr, nullptr);
+}
+
+// member list of work item w of the current batch
+int fetch_members(pm_ctx* c, const k::WorkDesc* d_work, const unsigned int* d_members, int32_t w, std::vector<int32_t>* out,
+                  k::WorkDesc* wd_out) {
+    k::WorkDesc wd;
+    PM_TRY(d2h(c, &wd, d_work + w, sizeof(wd)));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    out->resize(wd.count);
+    PM_TRY(d2h(c, out->data(), d_members + wd.mem_begin, sizeof(int32_t) * wd.count));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    if (wd_out) *wd_out = wd;
+    return PM_OK;
+}
 
 // must mirror the carve-up at the top of hash_bucket_fused_kernel
 size_t fused_hash_smem_bytes(int n_words, int keybits, int64_t cap_e, int t, int64_t x) {
@@ -1615,8 +1801,10 @@ int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
 template <typename KeyT>
 int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
               int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
-              int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key, int64_t out_base) {
+              int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key, int64_t out_base,
+              bool more_batches) {
     const int n_trials = static_cast<int>(progs.size());
+    st->best_in_batch = -1;
     const int l = cfg->l;
     const bool prof = cfg->profile != 0;
     const int r_cap = c->t * params.s;
@@ -1670,6 +1858,8 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     if (all_positions) PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
     PM_TRY(get_buf(c, S_SCAL, 16, &d_scal));
     PM_TRY(get_buf(c, S_BEST, static_cast<size_t>(n_trials), &best_work));
+    int32_t* n_close;
+    PM_TRY(get_buf(c, S_NCLOSE, static_cast<size_t>(n_trials), &n_close));
     PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
     {
@@ -1685,10 +1875,10 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         StageTimer tr(c, prof, 4);
         const int warps_per_block = 8;
         k::trial_best_kernel<<<(n_trials + warps_per_block - 1) / warps_per_block, warps_per_block * 32, 0, c->stream>>>(
-            work_off, work, o.score, o.expct, n_trials, best_work);
+            work_off, work, o.score, o.expct, n_trials, best_work, kTieEps, n_close);
         PM_TRY(check_launch(c, "trial_best"));
-        summarize_kernel<<<(n_trials + 127) / 128, 128, 0, c->stream>>>(best_work, work, o.score, o.iters, o.expct, o.cons,
-                                                                      n_trials, d_tb);
+        summarize_kernel<<<(n_trials + 127) / 128, 128, 0, c->stream>>>(best_work, n_close, work, o.score, o.iters, o.expct,
+                                                                      o.cons, n_trials, d_tb);
         PM_TRY(check_launch(c, "summarize"));
     }
     {
@@ -1728,12 +1918,65 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         out->em_work += (2 * s_iters1 - n_buckets) * c->x * l + 4 * s_iters1 * c->x;
     }
 
+    // Trials whose best bucket the FP32 expectation cannot separate from another bucket of the same score: every such
+    // candidate is refined again in FP64 and the comparison of driver.hpp:172-174 is repeated on those values.
+    std::vector<char> tb_exact(static_cast<size_t>(n_trials), 0);
+    {
+        std::vector<unsigned int> woff;
+        for (int i = 0; i < n_trials; ++i) {
+            TrialSummary& s = tb[static_cast<size_t>(i)];
+            if (s.work < 0 || s.n_close == 0) continue;
+            if (woff.empty()) {
+                woff.resize(static_cast<size_t>(n_trials) + 1);
+                PM_TRY(d2h(c, woff.data(), work_off, sizeof(unsigned int) * woff.size()));
+                PM_CUDA(cudaStreamSynchronize(c->stream));
+            }
+            const unsigned int b = woff[static_cast<size_t>(i)], e = woff[static_cast<size_t>(i) + 1];
+            std::vector<int32_t> sc(e - b);
+            std::vector<double> ex(e - b);
+            PM_TRY(d2h(c, sc.data(), o.score + b, sizeof(int32_t) * sc.size()));
+            PM_TRY(d2h(c, ex.data(), o.expct + b, sizeof(double) * ex.size()));
+            PM_CUDA(cudaStreamSynchronize(c->stream));
+            bool have = false;
+            int32_t bw = -1;
+            double be = 0.0;
+            uint64_t bk = 0;
+            std::vector<int32_t> mem;
+            for (unsigned int w = b; w < e; ++w) {
+                if (sc[w - b] != s.score || std::fabs(ex[w - b] - s.expct) > 2.0 * kTieEps) continue;
+                k::WorkDesc wd;
+                PM_TRY(fetch_members(c, work, srt.idx, static_cast<int32_t>(w), &mem, &wd));
+                double e64 = 0.0;
+                int32_t s64 = 0;
+                PM_TRY(exact_candidate(c, cfg, mem, &e64, &s64));
+                ++st->exact_refines;
+                if (!have || pm_candidate_improves(s.score, e64, wd.key, s.score, be, bk)) {
+                    have = true;
+                    bw = static_cast<int32_t>(w);
+                    be = e64;
+                    bk = wd.key;
+                }
+            }
+            if (have) {
+                if (bw != s.work) {
+                    PM_TRY(d2h(c, &s.iters, o.iters + bw, sizeof(int32_t)));
+                    PM_TRY(d2h(c, &s.cons, o.cons + bw, sizeof(uint64_t)));
+                    PM_CUDA(cudaStreamSynchronize(c->stream));
+                }
+                s.work = bw;
+                s.expct = be;
+                s.key = bk;
+                tb_exact[static_cast<size_t>(i)] = 1;
+            }
+        }
+    }
+
     // Ascending-trial reduction, driver.hpp:195-208.
     const int perfect = l * c->t;
     int32_t new_best_work = -1;
     for (int i = 0; i < n_trials; ++i) {
         const int64_t trial = first_trial + i;
-        const TrialSummary& s = tb[static_cast<size_t>(i)];
+        TrialSummary& s = tb[static_cast<size_t>(i)];
         out->trials_run = trial;
         out->buckets_enriched += n_rec[static_cast<size_t>(i)];
         const size_t oi = static_cast<size_t>(out_base + i);
@@ -1741,11 +1984,42 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         if (trial_best_score) trial_best_score[oi] = s.score;
         if (trial_best_expectation) trial_best_expectation[oi] = s.expct;
         if (trial_best_key) trial_best_key[oi] = s.key;
-        if (s.work >= 0 && (!st->have_best || pm_candidate_improves(s.score, s.expct, s.key, st->best.score,
-                                                                    st->best.expct, st->best.key))) {
+        bool improves = false;
+        if (s.work >= 0) {
+            if (!st->have_best) {
+                improves = true;
+            } else if (s.score == st->best.score && s.expct != st->best.expct &&
+                       std::fabs(s.expct - st->best.expct) <= kTieEps) {
+                // equal score, expectations closer than the FP32 error: both in FP64 (bit-equal expectations are the
+                // same model -- identical member lists -- and stay an exact tie)
+                bool s_exact = tb_exact[static_cast<size_t>(i)] != 0;
+                if (!s_exact) {
+                    std::vector<int32_t> mem;
+                    int32_t s64 = 0;
+                    PM_TRY(fetch_members(c, work, srt.idx, s.work, &mem, nullptr));
+                    PM_TRY(exact_candidate(c, cfg, mem, &s.expct, &s64));
+                    ++st->exact_refines;
+                    tb_exact[static_cast<size_t>(i)] = 1;
+                    if (trial_best_expectation) trial_best_expectation[oi] = s.expct;
+                }
+                if (!st->best_exact) {
+                    int32_t s64 = 0;
+                    if (st->best_in_batch >= 0) PM_TRY(fetch_members(c, work, srt.idx, st->best_in_batch, &st->best_members, nullptr));
+                    PM_TRY(exact_candidate(c, cfg, st->best_members, &st->best.expct, &s64));
+                    ++st->exact_refines;
+                    st->best_exact = true;
+                }
+                improves = pm_candidate_improves(s.score, s.expct, s.key, st->best.score, st->best.expct, st->best.key) != 0;
+            } else {
+                improves = pm_candidate_improves(s.score, s.expct, s.key, st->best.score, st->best.expct, st->best.key) != 0;
+            }
+        }
+        if (improves) {
             st->have_best = true;
             st->best = s;
             st->best_trial = trial;
+            st->best_exact = tb_exact[static_cast<size_t>(i)] != 0;
+            st->best_in_batch = s.work;
             new_best_work = s.work;
         }
         if (cfg->early_stop && st->have_best && st->best.score == perfect) {
@@ -1753,6 +2027,9 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
             break;
         }
     }
+    // a later batch may have to re-refine the incumbent in FP64: keep its member list (this batch's buffers are reused)
+    if (more_batches && st->best_in_batch >= 0) PM_TRY(fetch_members(c, work, srt.idx, st->best_in_batch, &st->best_members, nullptr));
+    st->best_in_batch = -1;
     if (new_best_work >= 0 && all_positions) {
         st->positions.resize(static_cast<size_t>(c->t));
         PM_TRY(d2h(c, st->positions.data(), o.pos + static_cast<size_t>(new_best_work) * static_cast<size_t>(c->t),
@@ -1883,9 +2160,9 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         host_mark("plans");
         const int rc = key_bytes == 4
                            ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, first - tb)
+                                                 trial_best_expectation, trial_best_key, first - tb, last < te)
                            : run_batch<uint64_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, first - tb);
+                                                 trial_best_expectation, trial_best_key, first - tb, last < te);
         if (rc != PM_OK) return rc;
     }
 

@@ -855,7 +855,9 @@ __device__ __forceinline__ bool better(int sa, double ea, uint64_t ka, int sb, d
 
 __global__ void trial_best_kernel(const unsigned int* __restrict__ work_off, const WorkDesc* __restrict__ work,
                                   const int32_t* __restrict__ score, const double* __restrict__ expct, int n_trials,
-                                  int32_t* __restrict__ best_work /* -1 if the trial has no bucket */) {
+                                  int32_t* __restrict__ best_work /* -1 if the trial has no bucket */, double tie_eps,
+                                  int32_t* __restrict__ n_close /* other buckets of the trial with the best score and an
+                                                                   expectation within tie_eps of the best */) {
     const int lane = threadIdx.x & 31;
     const int tr = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (tr >= n_trials) return;
@@ -887,7 +889,16 @@ __global__ void trial_best_kernel(const unsigned int* __restrict__ work_off, con
             bk = ok;
         }
     }
-    if (lane == 0) best_work[tr] = bi;
+    // candidates the FP32 expectation cannot separate from the best (driver.hpp:131-133 compares doubles exactly)
+    int close = 0;
+    for (unsigned int w = b + lane; w < e; w += 32) {
+        if (static_cast<int>(w) != bi && score[w] == bs && fabs(expct[w] - be) <= tie_eps) ++close;
+    }
+    close = __reduce_add_sync(0xffffffffu, close);
+    if (lane == 0) {
+        best_work[tr] = bi;
+        n_close[tr] = close;
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
