@@ -156,12 +156,13 @@ int pm_ctx_packed_words(pm_ctx* ctx, uint64_t* words_out, int64_t* word_off_out 
 int pm_ctx_symbol_counts(pm_ctx* ctx, int64_t* counts4);            /* global A,C,T,G counts (refine.hpp:115-125) */
 int pm_ctx_synchronize(pm_ctx* ctx);
 int64_t pm_ctx_launch_count(const pm_ctx* ctx);                     /* kernels launched so far on this context */
-/* EM refinement runs on the tensor cores (128 buckets per CTA, pm_em_tc.cuh); a bucket whose discrete outputs are
- * not clear of the FP32 error of those sums is refined again by the exact (FP64-assisted) kernel.  out5 = counts of
- * the last pm_refine / pm_run on this context: [0] buckets refined by the exact kernel, then by reason
- * [1] likelihood gain near tol (refine.hpp:300) [2] maximum left the exponent range [3] argmax runner-up within delta
- * (refine.hpp:311-316) [4] non-finite weight. */
-int pm_ctx_em_exact_counts(const pm_ctx* ctx, int64_t* out5);
+/* EM refinement runs on the tensor cores (128 buckets per CTA, pm_em_tc.cuh).  A bucket whose discrete outputs are not
+ * clear of the FP32 error of those sums is refined again by the pair kernel (FP64 on the windows that decide), and a
+ * bucket whose stop decision (refine.hpp:300) is within the pair kernel's own likelihood error by the FP64 kernel.
+ * out6 = counts of the last pm_refine / pm_run on this context: [0] buckets handed to the pair kernel, then by reason
+ * [1] likelihood gain near tol [2] maximum left the exponent range [3] argmax runner-up within delta (refine.hpp:311-316)
+ * [4] non-finite weight; [5] buckets handed to the FP64 kernel. */
+int pm_ctx_em_exact_counts(const pm_ctx* ctx, int64_t* out6);
 
 /* --------------------------------------------------------------------------------------------
  * 3. Stage-level device entry points (each parity-testable in isolation)

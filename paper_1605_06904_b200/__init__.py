@@ -338,11 +338,11 @@ class Context:
         return int(lib().pm_ctx_launch_count(self._h))
 
     def em_exact_counts(self):
-        """Buckets of the last refine()/run() that the tensor-core EM kernel handed to the exact kernel:
-        dict(total, likelihood_gain, range, argmax_tie, non_finite)."""
-        out = np.zeros(5, dtype=np.int64)
+        """Buckets of the last refine()/run() that the tensor-core EM kernel handed to the pair kernel (total and by
+        reason) and that the pair kernel handed to the FP64 kernel (fp64)."""
+        out = np.zeros(6, dtype=np.int64)
         _check(lib().pm_ctx_em_exact_counts(self._h, _p(out, C.c_int64)))
-        return dict(zip(("total", "likelihood_gain", "range", "argmax_tie", "non_finite"), out.tolist()))
+        return dict(zip(("total", "likelihood_gain", "range", "argmax_tie", "non_finite", "fp64"), out.tolist()))
 
     # ---- stages
     def hash_keys(self, l, kept):

@@ -61,7 +61,7 @@ enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
     S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
-    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_THETA_IN, S_NCLOSE,
+    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE,
     // the FP64 path has its own scratch: run() calls it while a batch's buffers are still live
     S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
 };
@@ -104,8 +104,9 @@ struct pm_ctx {
     int tc_l = -1, tc_n_blocks = 0, tc_e_positions = 0;
     std::vector<k::TcBlock> h_tc_blocks;
     k::TcBlock* d_tc_blocks = nullptr;
-    int64_t em_exact[5] = {0, 0, 0, 0, 0};  // last refine/run: buckets the tensor-core kernel handed to the exact kernel
-                                            // [0] total, then by reason: likelihood gain, range, argmax tie, non-finite
+    int64_t em_exact[6] = {0, 0, 0, 0, 0, 0};  // last refine/run: buckets the tensor-core kernel handed to the pair kernel
+                                               // [0] total, then by reason: likelihood gain, range, argmax tie, non-finite;
+                                               // [5] buckets the pair kernel handed to the FP64 kernel
     // host staging of the class-group index: lives in the context so the async uploads need no sync of their own
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
@@ -755,6 +756,51 @@ struct EmOut {
 };
 
 
+// refine() in FP64 (pm_em_f64.cuh), one CTA per work item.  steps_only: exactly max_iters em_step()s from theta_in.
+int launch_em_f64(pm_ctx* c, int l, int max_iters, double tol, const k::WorkDesc* work, unsigned int n_work,
+                  const unsigned int* members, const EmOut& o, unsigned long long* d_scal, const double* theta_in,
+                  bool steps_only, const unsigned int* out_map = nullptr, const unsigned int* n_work_dev = nullptr) {
+    k::EmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.seq_len = c->d_seq_len;
+    p.win_off = c->d_win_off;
+    p.seq_sym = c->d_seq_sym;
+    p.seq_logw = c->d_seq_logw;
+    for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
+    p.tot_bases = static_cast<double>(c->total_bases);
+    p.t = c->t;
+    p.l = l;
+    p.max_iters = max_iters;
+    p.tol = tol;
+    p.work = work;
+    p.n_work_dev = n_work_dev;  // device-side count (re-runs of flagged buckets); n_work is then its upper bound
+    p.n_work = n_work;
+    p.members = members;
+    p.out_score = o.score;
+    p.out_iters = o.iters;
+    p.out_exp = o.expct;
+    p.out_cons = o.cons;
+    p.out_pos = o.pos;
+    p.out_theta = o.theta;
+    p.out_ll = o.ll;
+    p.iter_total = d_scal;
+    p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
+    p.out_map = out_map;
+    p.theta_in = theta_in;
+    k::F64Extra x;
+    const size_t per_cta = static_cast<size_t>(std::max<int64_t>(c->x, 1));
+    const unsigned int grid = static_cast<unsigned int>(std::max<size_t>(
+        1, std::min<size_t>({static_cast<size_t>(n_work), static_cast<size_t>(n_work_dev ? c->sm_count / 2 : 2 * c->sm_count),
+                             (512u << 20) / (per_cta * 8)})));
+    PM_TRY(get_buf(c, S_F64_Z, per_cta * grid, &x.zbuf));
+    x.x = c->x;
+    x.steps_only = steps_only ? 1 : 0;
+    k::em_refine_f64_kernel<<<grid, k::kF64Threads, 0, c->stream>>>(p, x);
+    return check_launch(c, "em_refine_f64");
+}
+
 // ---- tensor-core EM kernel (pm_em_tc.cuh) ------------------------------------------------------------------
 // PM_B200_EM_TC (test/tuning knob): 0 keeps every bucket on the pair kernel, 2 uses the tensor-core kernel even for
 // a handful of buckets (default: from 32 buckets on; below that a 128-row tile is mostly empty)
@@ -853,7 +899,8 @@ EmTcKernel em_tc_kernel_for(int l) {
     }
 }
 
-// scalars on the device: [0] iter_total (u64) [1] error flag (u32 in the low half) [3] buckets the tensor-core kernel
+// scalars on the device: [0] iter_total (u64) [1] error flag (u32 in the low half) [2] buckets refined again by the FP64
+// kernel (u32 in the low half) [3] buckets the tensor-core kernel
 // handed to the exact kernel (u32 in the low half) [4..7] the same by reason (a bucket can have several)
 int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k::WorkDesc* work,
               const unsigned int* n_work_dev, unsigned int n_work_host, unsigned int n_work_bound,
@@ -892,6 +939,8 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.phase_clk = d_scal + 8;
     p.out_map = nullptr;
     p.theta_in = theta_in;
+    p.flag_exact = nullptr;
+    const k::WorkDesc* const work_all = work;  // the TC stage below narrows p.work to the buckets it flagged
 
     const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs;
     const bool pair_small = pair_ok && !(c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords);
@@ -971,8 +1020,26 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
                 x.zcap = c->zlen;
                 x.wcap = stage_words;
                 if (big) PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * 2 * static_cast<size_t>(c->t), &x.mprev_g));
+                // third tier: stop decisions within the error of this kernel's likelihood go to the FP64 kernel
+                const bool tier3 = theta_in == nullptr && max_iters >= 3;
+                if (tier3) {
+                    PM_TRY(get_buf(c, S_F64_FLAG, static_cast<size_t>(n_work_bound), &p.flag_exact));
+                    PM_CUDA(cudaMemsetAsync(p.flag_exact, 0, static_cast<size_t>(n_work_bound), c->stream));
+                }
                 kern<<<grid, threads, smem, c->stream>>>(p, x);
-                return check_launch(c, "em_refine_pair");
+                PM_TRY(check_launch(c, "em_refine_pair"));
+                if (tier3) {
+                    k::WorkDesc* d_list2;
+                    unsigned int* d_map2;
+                    unsigned int* d_cnt2 = reinterpret_cast<unsigned int*>(d_scal + 2);
+                    PM_TRY(get_buf(c, S_F64_WORK, static_cast<size_t>(n_work_bound), &d_list2));
+                    PM_TRY(get_buf(c, S_F64_MAP, static_cast<size_t>(n_work_bound), &d_map2));
+                    const unsigned int cgrid = std::max(1u, std::min(1024u, (n_work_bound + 255) / 256));
+                    tc_compact_kernel<<<cgrid, 256, 0, c->stream>>>(p.flag_exact, work_all, n_work_dev, n_work_host, d_list2, d_map2, d_cnt2);
+                    PM_TRY(check_launch(c, "f64_compact"));
+                    PM_TRY(launch_em_f64(c, l, max_iters, tol, d_list2, n_work_bound, members, o, d_scal, nullptr, false, d_map2, d_cnt2));
+                }
+                return PM_OK;
             }
         }
     }
@@ -987,50 +1054,6 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     const unsigned int grid = std::max(1u, std::min(full, n_work_bound));
     kern<<<grid, threads, smem, c->stream>>>(p);
     return check_launch(c, "em_refine");
-}
-
-// refine() in FP64 (pm_em_f64.cuh), one CTA per work item.  steps_only: exactly max_iters em_step()s from theta_in.
-int launch_em_f64(pm_ctx* c, int l, int max_iters, double tol, const k::WorkDesc* work, unsigned int n_work,
-                  const unsigned int* members, const EmOut& o, unsigned long long* d_scal, const double* theta_in,
-                  bool steps_only, const unsigned int* out_map = nullptr) {
-    k::EmParams p;
-    std::memset(&p, 0, sizeof(p));
-    p.words = c->d_words;
-    p.word_off = c->d_word_off;
-    p.seq_len = c->d_seq_len;
-    p.win_off = c->d_win_off;
-    p.seq_sym = c->d_seq_sym;
-    p.seq_logw = c->d_seq_logw;
-    for (int r = 0; r < 4; ++r) p.tot_sym[r] = static_cast<double>(c->tot_sym[r]);
-    p.tot_bases = static_cast<double>(c->total_bases);
-    p.t = c->t;
-    p.l = l;
-    p.max_iters = max_iters;
-    p.tol = tol;
-    p.work = work;
-    p.n_work_dev = nullptr;
-    p.n_work = n_work;
-    p.members = members;
-    p.out_score = o.score;
-    p.out_iters = o.iters;
-    p.out_exp = o.expct;
-    p.out_cons = o.cons;
-    p.out_pos = o.pos;
-    p.out_theta = o.theta;
-    p.out_ll = o.ll;
-    p.iter_total = d_scal;
-    p.error_flag = reinterpret_cast<unsigned int*>(d_scal + 1);
-    p.out_map = out_map;
-    p.theta_in = theta_in;
-    k::F64Extra x;
-    const size_t per_cta = static_cast<size_t>(std::max<int64_t>(c->x, 1));
-    const unsigned int grid = static_cast<unsigned int>(std::max<size_t>(
-        1, std::min<size_t>({static_cast<size_t>(n_work), static_cast<size_t>(2 * c->sm_count), (512u << 20) / (per_cta * 8)})));
-    PM_TRY(get_buf(c, S_F64_Z, per_cta * grid, &x.zbuf));
-    x.x = c->x;
-    x.steps_only = steps_only ? 1 : 0;
-    k::em_refine_f64_kernel<<<grid, k::kF64Threads, 0, c->stream>>>(p, x);
-    return check_launch(c, "em_refine_f64");
 }
 
 void unpack_consensus(uint64_t bits, int l, char* out) {
@@ -1257,9 +1280,9 @@ int pm_ctx_synchronize(pm_ctx* c) {
     return PM_OK;
 }
 
-int pm_ctx_em_exact_counts(const pm_ctx* c, int64_t* out5) {
-    if (c == nullptr || out5 == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
-    for (int i = 0; i < 5; ++i) out5[i] = c->em_exact[i];
+int pm_ctx_em_exact_counts(const pm_ctx* c, int64_t* out6) {
+    if (c == nullptr || out6 == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    for (int i = 0; i < 6; ++i) out6[i] = c->em_exact[i];
     return PM_OK;
 }
 
@@ -1475,6 +1498,7 @@ int refine_common(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_o
     if (!exact) {
         c->em_exact[0] = static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
         for (int r = 0; r < 4; ++r) c->em_exact[1 + r] = static_cast<int64_t>(scal[4 + r]);
+        c->em_exact[5] = static_cast<int64_t>(scal[2] & 0xFFFFFFFFULL);
     }
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
@@ -1909,6 +1933,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     }
     c->em_exact[0] += static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
     for (int r = 0; r < 4; ++r) c->em_exact[1 + r] += static_cast<int64_t>(scal[4 + r]);
+    c->em_exact[5] += static_cast<int64_t>(scal[2] & 0xFFFFFFFFULL);
     out->em_lookup_adds += static_cast<int64_t>(scal[0]) * c->x * l;
     {
         // W_EM = sum_b (2 I_b + 1) x l lookup-adds + 4 (I_b + 1) x; scal[0] = sum_b (I_b + 1)

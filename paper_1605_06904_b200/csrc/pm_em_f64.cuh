@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
                 p.out_score[oi] = score;
                 p.out_cons[oi] = cons;
             }
-            atomicAdd(p.iter_total, static_cast<unsigned long long>(iterations + 1));
+            if (p.out_map == nullptr) atomicAdd(p.iter_total, static_cast<unsigned long long>(iterations + 1));  // re-runs were counted
         }
     }
 }

@@ -983,6 +983,11 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                     for (int w = 0; w < nwarps; ++w) ll += llpart[w * 2 + bb];
                     if (p.out_ll && (bb == 0 || live1)) p.out_ll[static_cast<int64_t>(ois[bb]) * p.max_iters + (iterations - 1)] = ll;
                     iscal[bb * 4 + 0] = (iterations >= 2 && ll - dscal[bb * 6] < p.tol) ? 1 : 0;  // refine.hpp:296-304
+                    // The likelihood is FP64-accurate where EM has saturated and carries FP32 sums elsewhere (<= ~2e-5): a
+                    // gain this close to tol is decided by the FP64 kernel instead (the last iteration cannot stop the loop).
+                    if (p.flag_exact && iterations >= 2 && iterations < p.max_iters && fabs((ll - dscal[bb * 6]) - p.tol) <= 1e-4 &&
+                        (bb == 0 || live1))
+                        p.flag_exact[ois[bb]] = 1;
                     iscal[bb * 4 + 3] = iterations;
                     dscal[bb * 6] = ll;
                 }

@@ -533,6 +533,8 @@ struct EmParams {
     unsigned long long* phase_clk;   // [8] per-phase clock sums (only with -DPM_EM_TIMING)
     const unsigned int* out_map;     // nullptr, or output slot of each work item (re-runs of flagged buckets, pm_em_tc.cuh)
     const double* theta_in;          // nullptr, or [work][4][l+1] starting models instead of init_model (pm_em_step)
+    unsigned char* flag_exact;       // nullptr, or [output slot]: set when a stop decision (refine.hpp:300) fell within the
+                                     // error of this kernel's likelihood; the FP64 kernel then refines the bucket again
 };
 
 template <int G>

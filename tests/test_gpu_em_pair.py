@@ -56,25 +56,27 @@ def test_result_does_not_depend_on_the_partner(ctx, best_oracle, instance):
         assert a["expectation"] == b["expectation"] and (a["theta"] == b["theta"]).all()
 
 
-def test_pair_kernel_agrees_with_one_bucket_kernel(pm, golden, instance):
-    """PM_B200_EM_PAIR=0 selects the one-bucket kernel (pm_em_smem.cuh): same discrete outputs on the
-    challenge-scale goldens, thetas within FP32 noise of each other."""
+def test_tensor_core_kernel_agrees_with_pair_kernel(pm, golden, instance):
+    """PM_B200_EM_TC=0 keeps every bucket on the pair kernel, 2 sends even a handful through the tensor-core kernel
+    (pm_em_tc.cuh): same discrete outputs on the challenge-scale goldens, thetas within FP32 noise of each other."""
     g = [x for x in golden["refine"] if x["instance"][1] == 600][:7]
     ss, _, _ = instance(*g[0]["instance"])
     res = {}
-    for flag in ("1", "0"):
-        os.environ["PM_B200_EM_PAIR"] = flag
+    for flag in ("2", "0"):
+        os.environ["PM_B200_EM_TC"] = flag
         try:
             with pm.Context(0) as c:
                 c.set_sequences(ss.bases, ss.offs)
                 res[flag] = c.refine(15, [x["members"] for x in g])
+                exact = c.em_exact_counts()["total"]
+                assert exact == 0 if flag == "0" else exact <= len(g)
         finally:
-            os.environ.pop("PM_B200_EM_PAIR", None)
-    for a, b, x in zip(res["1"], res["0"], g):
+            os.environ.pop("PM_B200_EM_TC", None)
+    for a, b, x in zip(res["2"], res["0"], g):
         assert (a["consensus"], a["score"], a["positions"], a["iterations"]) == \
                (b["consensus"], b["score"], b["positions"], b["iterations"]) == \
                (x["consensus"], x["score"], x["positions"], x["iterations"])
-        assert np.abs(a["theta"] - b["theta"]).max() < 1e-5
+        assert np.abs(a["theta"] - b["theta"]).max() < 2e-5
         assert abs(a["expectation"] - x["expectation"]) <= EXPECTATION_TOL
 
 

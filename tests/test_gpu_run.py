@@ -86,11 +86,9 @@ def test_run_matches_oracle_on_small_and_ragged_sets(ctx, best_oracle):
         kw = dict(l=l, d=1, k=l - 3, s=2, m=5, seed=round_, early_stop=0)
         ctx.set_sequences(ss.bases, ss.offs)
         got, want = ctx.run(**kw), best_oracle.run(ss, **kw)
-        for f in ("score", "buckets_enriched", "trials_run", "k", "s", "m"):
-            assert got[f] == want[f], (round_, f)
-        # equal-score candidates whose expectations differ by less than the FP32 tolerance may swap
-        if (got["best_trial"], got["source_bucket"]) == (want["best_trial"], want["source_bucket"]):
-            assert_same_result(got, want)
+        # candidates of equal score whose expectations are closer than the FP32 error are settled in FP64
+        # (pm_refine_exact), so best_trial / source_bucket are the reference's
+        assert_same_result(got, want)
 
 
 def test_results_do_not_depend_on_batching_backend_or_workers(ctx, instance):

@@ -1,6 +1,8 @@
 """Parity of each CUDA stage (through the C ABI) against the CPU oracle and the reference-generated
 goldens: bit-exact for codes, keys, grouping, enriched lists, positions, scores; theta and
 expectation within the stated FP32 tolerance (conftest.THETA_TOL / EXPECTATION_TOL)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -158,7 +160,7 @@ def test_refine_matches_reference_goldens(ctx, golden, instance):
         got = ctx.refine(items[0]["l"], [g["members"] for g in items])
         for a, g in zip(got, items):
             check_candidate(a, g["consensus"], g["positions"], g["score"], g["iterations"], g["expectation"], g["theta"])
-            np.testing.assert_allclose(a["ll_trace"], g["ll_trace"], atol=5e-2, rtol=0)
+            np.testing.assert_allclose(a["ll_trace"], g["ll_trace"], atol=1e-3, rtol=0)
 
 
 def test_refine_worked_example(ctx, example, golden):
@@ -171,7 +173,8 @@ def test_refine_worked_example(ctx, example, golden):
 
 
 def test_refine_matches_oracle_on_random_instances(ctx, best_oracle):
-    # discrete outputs are compared where the reference's own top-2 window gap is not an FP32 near-tie
+    # small random sets: EM saturates, stops early and window weights tie -- the cases the FP32 kernels hand to the
+    # FP64-assisted ones (argmax near-ties: pair kernel; stop decisions near tol: FP64 kernel).  Everything must match.
     rng = np.random.default_rng(15)
     compared = 0
     for round_ in range(12):
@@ -181,16 +184,17 @@ def test_refine_matches_oracle_on_random_instances(ctx, best_oracle):
         kept = best_oracle.sample_plan(l, k, round_)
         en = best_oracle.enriched(ss, l, kept, 1, t)[:12]
         ctx.set_sequences(ss.bases, ss.offs)
-        got = ctx.refine(l, [e["members"] for e in en])
-        for e, a in zip(en, got):
-            w = best_oracle.refine(ss, l, e["members"], e["key"])
-            assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL or a["iterations"] != w.iterations
-            if a["iterations"] == w.iterations:
-                assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
-            if (a["positions"], a["iterations"]) == (w.positions, w.iterations):
-                assert (a["consensus"], a["score"]) == (w.consensus, w.score)
+        for mode in ("2", "0"):  # through the tensor-core kernel and on the pair kernel alone
+            os.environ["PM_B200_EM_TC"] = mode
+            try:
+                got = ctx.refine(l, [e["members"] for e in en])
+            finally:
+                os.environ.pop("PM_B200_EM_TC", None)
+            for e, a in zip(en, got):
+                w = best_oracle.refine(ss, l, e["members"], e["key"])
+                check_candidate(a, w.consensus, w.positions, w.score, w.iterations, w.expectation, w.theta)
                 compared += 1
-    assert compared >= 100  # FP32 near-ties are rare, not the rule
+    assert compared >= 200
 
 
 def test_refine_single_member_and_limits(pm, ctx, best_oracle, instance):
