@@ -76,6 +76,11 @@ typedef struct pm_run_config {
     int32_t batch_trials;     /* trials per device batch; 0 = auto */
     int32_t profile;          /* 1: time each stage with CUDA events into pm_run_result.stage_ms */
     double z_epsilon;         /* M-step responsibility cut-off; <0 = default (2^-30); 0 = every window */
+    int64_t trial_stride;     /* 0/1: every trial of [trial_begin, trial_end]; N > 1: trial_begin, trial_begin+N, ... (round-robin
+                                 shards: the right split when the answer is expected within the first few trials) */
+    int32_t exact_best;       /* 1: the reported winner's expectation is the FP64 kernel's (what a cross-shard comparison of
+                                 near-equal candidates needs) */
+    int32_t _pad1;
 } pm_run_config;
 
 /* RunResult + TrialParams (driver.hpp:44-52, projection.hpp:23-31) and run statistics. */
@@ -115,6 +120,10 @@ void pm_default_config(pm_run_config* cfg);                        /* RunConfig{
 uint64_t pm_splitmix64(uint64_t x);                                /* rng.hpp:13-17 */
 uint64_t pm_derive_seed(uint64_t master, uint64_t index);          /* rng.hpp:22-24 */
 int pm_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept);/* sample_plan(l,k,Rng(seed)), projection.hpp:210-226 */
+/* sample_plan(l,k,rng) on a generator the CALLER owns (projection.hpp:210-226, rng.hpp:37-73): next_u64(state) must
+ * return the generator's next 64-bit output; the l-k draws (plus rejections) are taken from it, so consecutive calls
+ * on one generator give the reference's consecutive plans. */
+int pm_sample_plan_stream(int l, int k, uint64_t (*next_u64)(void*), void* state, int32_t* kept);
 int pm_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept); /* driver.hpp:164-165 */
 int pm_validate_plan(int l, const int32_t* kept, int k);           /* ProjectionPlan ctor, projection.hpp:36-52 */
 
@@ -221,6 +230,13 @@ int pm_median_string(pm_ctx* ctx, int l, uint64_t limit, char* median, int* tota
  * buckets (enriched count), best_score (-1 if none), best_expectation, best_key. */
 int pm_run(pm_ctx* ctx, const pm_run_config* cfg, pm_run_result* out, int32_t* positions, int64_t* trial_buckets,
            int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key);
+/* run() on SEVERAL GPUs of one node (trials are independent, driver.hpp:164: no data-path collective).  One host thread
+ * and one context per entry of `devices` (an ordinal may repeat: several contexts share that GPU); each uploads the set
+ * and runs its shard of trials 1..m -- contiguous blocks, or round-robin when strided != 0 -- and the per-shard results
+ * (a ~300-byte record and the per-trial bucket counts) are merged on the host exactly as the ascending-trial scan of
+ * driver.hpp:195-208 would, early stop included.  Same outputs as pm_run_host. */
+int pm_run_multi(const int* devices, int n_devices, int strided, const pm_run_config* cfg, const char* bases,
+                 const int64_t* offs, int t, pm_run_result* out, int32_t* positions);
 /* Same, from host buffers: upload + encode + run + read-back in one call (the e2e path). */
 int pm_run_host(pm_ctx* ctx, const pm_run_config* cfg, const char* bases, const int64_t* offs, int t,
                 pm_run_result* out, int32_t* positions);

@@ -17,15 +17,19 @@
 // All heavy work happens in libpm_b200.so on the GPU; nothing here computes the path on the CPU.
 // Link with -lpm_b200 (paper_1605_06904_b200/libpm_b200.so).
 #pragma once
+#include <algorithm>
 #include <cctype>
+#include <cmath>
 #include <charconv>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <memory>
 #include <optional>
 #include <stdexcept>
 #include <chrono>
+#include <random>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -179,6 +183,9 @@ public:
             ctx_.reset(c);
         }
         if (loaded_ != seqs.bases() || loaded_offs_ != seqs.offsets()) {
+            // a failed upload leaves the context without a set: forget the old one first
+            loaded_.clear();
+            loaded_offs_.clear();
             detail::check(pm_ctx_set_sequences(ctx_.get(), seqs.bases().data(), seqs.offsets().data(), seqs.count()));
             loaded_ = seqs.bases();
             loaded_offs_ = seqs.offsets();
@@ -201,16 +208,28 @@ private:
     int device_ = 0;
 };
 
-// ---- rng.hpp: only the seed matters to sample_plan; the stream itself lives in libpm_b200 (pm_host.cpp)
+// ---- rng.hpp:25-50: std::mt19937_64 (its output for a seed is fixed by the standard) behind a bounded draw that does
+// not depend on the standard library's distributions
 inline std::uint64_t splitmix64(std::uint64_t x) { return pm_splitmix64(x); }
 inline std::uint64_t derive_seed(std::uint64_t master, std::uint64_t index) { return pm_derive_seed(master, index); }
 class Rng {
 public:
-    explicit Rng(std::uint64_t seed) : seed_(seed) {}
-    std::uint64_t seed() const { return seed_; }
+    explicit Rng(std::uint64_t seed) : engine_(seed) {}
+    std::uint64_t next() { return engine_(); }
+    /// a value in [0, n): outputs below 2^64 mod n are discarded, the rest reduced mod n
+    std::uint64_t uniform_below(std::uint64_t n) {
+        if (n == 0) throw InvalidParamsError("uniform_below requires a nonempty range");
+        if (n == 1) return 0;
+        const std::uint64_t discard = (~n + 1) % n;
+        for (;;) {
+            const std::uint64_t x = engine_();
+            if (x >= discard) return x % n;
+        }
+    }
+    std::mt19937_64& engine() { return engine_; }
 
 private:
-    std::uint64_t seed_;
+    std::mt19937_64 engine_;
 };
 
 // ---- projection.hpp
@@ -268,9 +287,11 @@ inline int bucket_threshold(int t, int n, int l, int k, int floor = 3) {
     return bucket_threshold_for_windows(static_cast<std::uint64_t>(t) * static_cast<std::uint64_t>(n - l + 1), k, floor);
 }
 
+// sample_plan (projection.hpp:210-226) consumes the caller's generator: two calls on one Rng give two different plans
 inline ProjectionPlan sample_plan(int l, int k, Rng& rng) {
     std::vector<int> kept(static_cast<std::size_t>(k > 0 ? k : 1));
-    detail::check(pm_sample_plan(l, k, rng.seed(), kept.data()));
+    auto pull = [](void* state) -> std::uint64_t { return static_cast<Rng*>(state)->next(); };
+    detail::check(pm_sample_plan_stream(l, k, pull, &rng, kept.data()));
     kept.resize(static_cast<std::size_t>(k));
     return ProjectionPlan(l, std::move(kept));
 }
@@ -320,6 +341,94 @@ inline std::vector<EnrichedBucket> enriched_buckets(const SequenceSet& seqs, int
 }
 
 // ---- refine.hpp
+// MotifModel (refine.hpp:20-76): 4 symbol rows x (l+1) columns, column 0 = background; the storage is exactly the
+// buffer the C ABI exchanges (row-major, refine.hpp:65-71), so the stage calls below pass data() straight through.
+class MotifModel {
+public:
+    MotifModel(int sigma, int l) : sigma_(sigma), l_(l) {
+        if (sigma < 1 || l < 1) throw InvalidParamsError("model dimensions must be positive");
+        if (sigma != 4) throw InvalidParamsError("this build models the DNA alphabet only (sigma = 4)");
+        cells_.assign(static_cast<std::size_t>(sigma) * static_cast<std::size_t>(l + 1), 0.0);
+    }
+    int sigma() const { return sigma_; }
+    int motif_length() const { return l_; }
+    double& at(int rank, int column) { return cells_[slot(rank, column)]; }
+    double at(int rank, int column) const { return cells_[slot(rank, column)]; }
+    double column_max(int column) const {
+        double top = 0.0;
+        for (int r = 0; r < sigma_; ++r) top = std::max(top, at(r, column));
+        return top;
+    }
+    bool is_column_stochastic(double tol = 1e-9) const {
+        for (int c = 0; c <= l_; ++c) {
+            double total = 0.0;
+            for (int r = 0; r < sigma_; ++r) {
+                const double v = at(r, c);
+                if (!(v >= 0.0 && v <= 1.0)) return false;
+                total += v;
+            }
+            if (std::abs(total - 1.0) > tol) return false;
+        }
+        return true;
+    }
+    bool operator==(const MotifModel& o) const { return sigma_ == o.sigma_ && l_ == o.l_ && cells_ == o.cells_; }
+    double* data() { return cells_.data(); }
+    const double* data() const { return cells_.data(); }
+
+private:
+    std::size_t slot(int rank, int column) const {
+        if (rank < 0 || rank >= sigma_ || column < 0 || column > l_) {
+            throw IndexOutOfRangeError("model cell (" + std::to_string(rank) + "," + std::to_string(column) + ") outside " +
+                                       std::to_string(sigma_) + "x" + std::to_string(l_ + 1));
+        }
+        return static_cast<std::size_t>(rank) * static_cast<std::size_t>(l_ + 1) + static_cast<std::size_t>(column);
+    }
+    int sigma_, l_;
+    std::vector<double> cells_;
+};
+
+/// init_model (refine.hpp:90-127): theta0 from the members' symbol counts, background from the whole set.
+inline MotifModel init_model(const std::vector<LmerRef>& members, const SequenceSet& seqs, int l, double pseudocount = 0.0) {
+    if (members.empty()) throw EmptyBucketError("cannot build a motif model from an empty bucket");
+    if (pseudocount < 0.0) throw InvalidParamsError("pseudocount must be non-negative");
+    std::vector<std::int32_t> flat;
+    flat.reserve(members.size());
+    for (const LmerRef& r : members) flat.push_back(seqs.flat_of(r));
+    MotifModel model(4, l);
+    detail::check(pm_init_model(Device::instance().bind(seqs), l, flat.data(), static_cast<int>(flat.size()), pseudocount, model.data()));
+    return model;
+}
+
+/// expectation (refine.hpp:130-136): sum over the motif columns of the column maximum.
+inline double expectation(const MotifModel& model) {
+    double e = 0.0;
+    detail::check(pm_expectation(model.data(), model.motif_length(), &e));
+    return e;
+}
+
+struct EmStepResult {
+    MotifModel model;
+    double log_likelihood = 0.0;  // OOPS log-likelihood of the INPUT model (refine.hpp:209)
+};
+
+/// em_step (refine.hpp:216-282) with the production EM kernel; em_step_exact runs the FP64 kernel.
+inline EmStepResult em_step(const MotifModel& model, const SequenceSet& seqs, int l) {
+    if (model.motif_length() != l) {
+        throw LengthMismatchError("model built for l=" + std::to_string(model.motif_length()) + ", asked to step with l=" + std::to_string(l));
+    }
+    EmStepResult r{MotifModel(4, l), 0.0};
+    detail::check(pm_em_step(Device::instance().bind(seqs), l, model.data(), r.model.data(), &r.log_likelihood));
+    return r;
+}
+inline EmStepResult em_step_exact(const MotifModel& model, const SequenceSet& seqs, int l) {
+    if (model.motif_length() != l) {
+        throw LengthMismatchError("model built for l=" + std::to_string(model.motif_length()) + ", asked to step with l=" + std::to_string(l));
+    }
+    EmStepResult r{MotifModel(4, l), 0.0};
+    detail::check(pm_em_step_exact(Device::instance().bind(seqs), l, model.data(), r.model.data(), &r.log_likelihood));
+    return r;
+}
+
 struct RefinedCandidate {
     std::string consensus;
     StartVector positions;
@@ -402,6 +511,11 @@ struct RunConfig {
     bool early_stop = true;
     std::optional<int> t_hat;
     std::optional<std::vector<int>> forced_kept_positions;
+    // GPU build: CUDA devices to shard the trials over (empty = the calling thread's device).  The reference
+    // parallelises trials over `workers` host threads (driver.hpp:186-209); here the unit is a GPU.  strided_trials
+    // deals the trials round-robin instead of in contiguous blocks (results are identical either way).
+    std::vector<int> devices;
+    bool strided_trials = false;
 };
 
 struct RunResult {
@@ -462,7 +576,12 @@ inline RunResult run(const RunConfig& config, const SequenceSet& seqs) {
     const pm_run_config c = detail::to_c(config);
     pm_run_result r;
     std::vector<std::int32_t> pos(static_cast<std::size_t>(seqs.count()));
-    detail::check(pm_run(Device::instance().bind(seqs), &c, &r, pos.data(), nullptr, nullptr, nullptr, nullptr));
+    if (config.devices.empty()) {
+        detail::check(pm_run(Device::instance().bind(seqs), &c, &r, pos.data(), nullptr, nullptr, nullptr, nullptr));
+    } else {
+        detail::check(pm_run_multi(config.devices.data(), static_cast<int>(config.devices.size()), config.strided_trials ? 1 : 0, &c,
+                                   seqs.bases().data(), seqs.offsets().data(), seqs.count(), &r, pos.data()));
+    }
     RunResult out;
     out.best.consensus = r.consensus;
     out.best.positions.assign(pos.begin(), pos.end());
@@ -481,64 +600,75 @@ inline RunResult run(const RunConfig& config, const SequenceSet& seqs) {
     return out;
 }
 
-// ---- fasta.hpp:18-97 (host text I/O)
+// ---- FASTA text <-> SequenceSet (behaviour of fasta.hpp:18-97; host text I/O).
+// Scanner over the raw bytes: memchr finds the line ends, a record is opened by a line whose FIRST byte is '>',
+// residues are folded to upper case with one mask, blanks inside a line are skipped, CR/blank tails are dropped.
+namespace detail {
+struct FastaRecord {
+    std::string name, residues;
+};
+inline std::string_view drop_tail_blanks(const char* b, const char* e) {
+    while (e > b && (e[-1] == '\r' || e[-1] == ' ' || e[-1] == '\t')) --e;
+    return std::string_view(b, static_cast<std::size_t>(e - b));
+}
+inline void require_residues(const std::vector<FastaRecord>& recs) {
+    if (!recs.empty() && recs.back().residues.empty()) {
+        throw RecordWithoutSequenceError("record '" + recs.back().name + "' has no sequence data");
+    }
+}
+}  // namespace detail
+
 inline SequenceSet parse_fasta(std::string_view text) {
-    std::vector<std::string> names, seqs;
-    int line_no = 0;
-    std::size_t pos = 0;
-    bool in_record = false;
-    while (pos <= text.size()) {
-        const std::size_t eol = text.find('\n', pos);
-        std::string_view line = text.substr(pos, (eol == std::string_view::npos ? text.size() : eol) - pos);
-        pos = eol == std::string_view::npos ? text.size() + 1 : eol + 1;
-        ++line_no;
-        while (!line.empty() && (line.back() == '\r' || line.back() == ' ' || line.back() == '\t')) line.remove_suffix(1);
-        if (line.empty()) continue;
-        if (line.front() == '>') {
-            if (in_record && seqs.back().empty()) {
-                throw RecordWithoutSequenceError("record '" + names.back() + "' has no sequence data");
-            }
-            std::string_view header = line.substr(1);
-            while (!header.empty() && (header.front() == ' ' || header.front() == '\t')) header.remove_prefix(1);
-            names.emplace_back(header);
-            seqs.emplace_back();
-            in_record = true;
+    std::vector<detail::FastaRecord> recs;
+    const char* cur = text.data();
+    const char* const stop = cur + text.size();
+    for (int lineno = 1; cur <= stop; ++lineno) {
+        const char* nl = cur < stop ? static_cast<const char*>(std::memchr(cur, '\n', static_cast<std::size_t>(stop - cur))) : nullptr;
+        const std::string_view body = detail::drop_tail_blanks(cur, nl ? nl : stop);
+        cur = nl ? nl + 1 : stop + 1;
+        if (body.empty()) continue;
+        if (body[0] == '>') {
+            detail::require_residues(recs);
+            std::size_t from = 1;
+            while (from < body.size() && (body[from] == ' ' || body[from] == '\t')) ++from;
+            recs.push_back({std::string(body.substr(from)), std::string()});
             continue;
         }
-        if (!in_record) {
-            throw FastaFormatError("sequence data before the first '>' header at line " + std::to_string(line_no));
-        }
-        for (char raw : line) {
+        if (recs.empty()) throw FastaFormatError("sequence data before the first '>' header at line " + std::to_string(lineno));
+        detail::FastaRecord& rec = recs.back();
+        for (const char raw : body) {
             if (raw == ' ' || raw == '\t') continue;
-            const char c = static_cast<char>(std::toupper(static_cast<unsigned char>(raw)));
-            if (c != 'A' && c != 'C' && c != 'G' && c != 'T') {
-                throw UnknownSymbolError(std::string("unknown symbol '") + raw + "' in record '" + names.back() +
-                                         "' at line " + std::to_string(line_no));
+            const char up = static_cast<char>(raw & ~0x20);  // 'a'..'z' -> 'A'..'Z'; anything else fails the test below
+            if (!(up == 'A' || up == 'C' || up == 'G' || up == 'T') || (raw != up && raw != (up | 0x20))) {
+                throw UnknownSymbolError(std::string("unknown symbol '") + raw + "' in record '" + rec.name + "' at line " +
+                                         std::to_string(lineno));
             }
-            seqs.back().push_back(c);
+            rec.residues.push_back(up);
         }
     }
-    if (seqs.empty()) throw EmptyInputError("FASTA input contains no records");
-    if (in_record && seqs.back().empty()) {
-        throw RecordWithoutSequenceError("record '" + names.back() + "' has no sequence data");
+    if (recs.empty()) throw EmptyInputError("FASTA input contains no records");
+    detail::require_residues(recs);
+    std::vector<std::string> names, seqs;
+    names.reserve(recs.size());
+    seqs.reserve(recs.size());
+    for (detail::FastaRecord& r : recs) {
+        names.push_back(std::move(r.name));
+        seqs.push_back(std::move(r.residues));
     }
     return SequenceSet(std::move(seqs), std::move(names));
 }
 
 inline std::string serialize_fasta(const SequenceSet& seqs, int line_width = 60) {
     if (line_width < 1) throw InvalidParamsError("FASTA line width must be positive");
-    std::string out;
+    const std::size_t width = static_cast<std::size_t>(line_width);
+    std::string text;
     for (int i = 1; i <= seqs.count(); ++i) {
-        out += '>';
-        out += seqs.name(i);
-        out += '\n';
-        const std::string& s = seqs.sequence(i);
-        for (std::size_t start = 0; start < s.size(); start += static_cast<std::size_t>(line_width)) {
-            out += s.substr(start, static_cast<std::size_t>(line_width));
-            out += '\n';
-        }
+        const std::string& residues = seqs.sequence(i);
+        text.reserve(text.size() + seqs.name(i).size() + residues.size() + residues.size() / width + 3);
+        text.append(1, '>').append(seqs.name(i)).append(1, '\n');
+        for (std::size_t at = 0; at < residues.size(); at += width) text.append(residues, at, width).append(1, '\n');
     }
-    return out;
+    return text;
 }
 
 // ---- planted.hpp:38-101
@@ -685,64 +815,88 @@ inline MedianStringResult median_string(const SequenceSet& seqs, int l, std::uin
     return r;
 }
 
-/// naive_mfp (oracle.hpp:45-98): every start vector in odometer order, first maximum of the profile score.
-/// Exponential ground truth for toy instances; plain host C++ (not part of the accelerated path), the
-/// incremental profile update of the reference restated on rank arrays.
+/// naive_mfp (behaviour of oracle.hpp:45-98): the best-scoring start vector over ALL configurations, the first one in
+/// lexicographic order (sequence 1 most significant) among equals.  Exponential ground truth for toy instances, plain
+/// host C++.  Depth-first over the sequences with one profile per depth; the last sequence is not enumerated through
+/// the profile at all: its windows are scored against the column maxima of the prefix in O(l) each.
 inline NaiveMfpResult naive_mfp(const SequenceSet& seqs, int l, std::uint64_t limit = 100000000ULL) {
     const int t = seqs.count();
-    std::uint64_t product = 1;  // configuration_count, oracle.hpp:28-39
-    for (int i = 1; i <= t; ++i) {
-        const std::uint64_t w = static_cast<std::uint64_t>(seqs.window_count(i, l));
-        if (w == 0 || product > limit / w) {
-            product = limit + 1;
-            break;
+    {   // refuse search spaces beyond the limit (product of the window counts, saturating)
+        std::uint64_t configs = 1;
+        bool too_many = false;
+        for (int i = 1; i <= t && !too_many; ++i) {
+            const std::uint64_t w = static_cast<std::uint64_t>(seqs.window_count(i, l));
+            too_many = w == 0 || configs > limit / w;
+            if (!too_many) configs *= w;
         }
-        product *= w;
-    }
-    if (product > limit) {
-        throw SearchSpaceTooLargeError("naive search needs more than " + std::to_string(limit) +
-                                       " configurations; lower t, n, or raise the limit");
-    }
-    auto rank = [](char c) { return c == 'A' ? 0 : c == 'C' ? 1 : c == 'T' ? 2 : 3; };  // alphabet.hpp:33-36
-    std::vector<int> prof(static_cast<std::size_t>(4 * l), 0);
-    StartVector pos(static_cast<std::size_t>(t), 1);
-    for (int i = 1; i <= t; ++i) {
-        for (int c = 0; c < l; ++c) ++prof[static_cast<std::size_t>(4 * c + rank(seqs.sequence(i)[static_cast<std::size_t>(c)]))];
-    }
-    auto move_row = [&](int i, int j, int j2) {
-        const std::string& s = seqs.sequence(i);
-        for (int c = 0; c < l; ++c) {
-            --prof[static_cast<std::size_t>(4 * c + rank(s[static_cast<std::size_t>(j - 1 + c)]))];
-            ++prof[static_cast<std::size_t>(4 * c + rank(s[static_cast<std::size_t>(j2 - 1 + c)]))];
+        if (too_many) {
+            throw SearchSpaceTooLargeError("naive search needs more than " + std::to_string(limit) +
+                                           " configurations; lower t, n, or raise the limit");
         }
-    };
+    }
+    const std::size_t cells = static_cast<std::size_t>(4 * l);
+    // 2-bit codes of every sequence (A0 C1 T2 G3, alphabet.hpp:33-36)
+    std::vector<std::vector<std::uint8_t>> code(static_cast<std::size_t>(t));
+    for (int i = 0; i < t; ++i) {
+        const std::string& s = seqs.sequence(i + 1);
+        code[static_cast<std::size_t>(i)].resize(s.size());
+        for (std::size_t p = 0; p < s.size(); ++p) code[static_cast<std::size_t>(i)][p] = static_cast<std::uint8_t>((static_cast<unsigned char>(s[p]) >> 1) & 3u);
+    }
+    // depth[i] = profile of the windows chosen for sequences 0..i-1
+    std::vector<std::vector<int>> depth(static_cast<std::size_t>(t), std::vector<int>(cells, 0));
+    StartVector at(static_cast<std::size_t>(t), 0);  // 0-based start of each sequence on the current path
     NaiveMfpResult best;
     best.score = -1;
-    for (;;) {
-        int sc = 0;
-        for (int c = 0; c < l; ++c) {
-            sc += std::max(std::max(prof[static_cast<std::size_t>(4 * c)], prof[static_cast<std::size_t>(4 * c + 1)]),
-                           std::max(prof[static_cast<std::size_t>(4 * c + 2)], prof[static_cast<std::size_t>(4 * c + 3)]));
+    std::vector<int> colmax(static_cast<std::size_t>(l));
+    int level = 0;
+    at[0] = -1;
+    while (level >= 0) {
+        const std::size_t lv = static_cast<std::size_t>(level);
+        if (level == t - 1) {
+            // leaf level: every window of the last sequence against the prefix profile
+            const std::vector<int>& pre = depth[lv];
+            int base = 0;
+            for (int c = 0; c < l; ++c) {
+                const int* col = &pre[static_cast<std::size_t>(4 * c)];
+                colmax[static_cast<std::size_t>(c)] = std::max(std::max(col[0], col[1]), std::max(col[2], col[3]));
+                base += colmax[static_cast<std::size_t>(c)];
+            }
+            const std::vector<std::uint8_t>& cs = code[lv];
+            const int windows = seqs.window_count(t, l);
+            for (int j = 0; j < windows; ++j) {
+                int sc = base;
+                for (int c = 0; c < l; ++c) {
+                    // the window's symbol raises its column maximum by one exactly when it already holds the maximum
+                    sc += pre[static_cast<std::size_t>(4 * c + cs[static_cast<std::size_t>(j + c)])] == colmax[static_cast<std::size_t>(c)] ? 1 : 0;
+                }
+                if (sc > best.score) {
+                    best.score = sc;
+                    best.positions = at;
+                    best.positions[lv] = j;
+                }
+            }
+            --level;
+            continue;
         }
-        if (sc > best.score) {
-            best.score = sc;
-            best.positions = pos;
+        // inner level: advance this sequence's start; descend with the extended profile, or backtrack
+        if (++at[lv] >= seqs.window_count(level + 1, l)) {
+            --level;
+            continue;
         }
-        int i = t;
-        while (i >= 1 && pos[static_cast<std::size_t>(i - 1)] == seqs.window_count(i, l)) {
-            move_row(i, pos[static_cast<std::size_t>(i - 1)], 1);
-            pos[static_cast<std::size_t>(i - 1)] = 1;
-            --i;
-        }
-        if (i < 1) break;
-        move_row(i, pos[static_cast<std::size_t>(i - 1)], pos[static_cast<std::size_t>(i - 1)] + 1);
-        ++pos[static_cast<std::size_t>(i - 1)];
+        std::vector<int>& next = depth[lv + 1];
+        next = depth[lv];
+        const std::vector<std::uint8_t>& cs = code[lv];
+        for (int c = 0; c < l; ++c) ++next[static_cast<std::size_t>(4 * c + cs[static_cast<std::size_t>(at[lv] + c)])];
+        ++level;
+        if (level < t - 1) at[static_cast<std::size_t>(level)] = -1;
     }
+    for (int& p : best.positions) ++p;  // public positions are 1-based
     best.consensus = consensus(seqs, best.positions, l);
     return best;
 }
 
-// ---- driver.hpp:222-302: benchmark() -- the projection pipeline against both exact solvers, TSV report
+// ---- benchmark() (behaviour of driver.hpp:222-302): the projection pipeline against both exact solvers on planted toy
+// instances, one TSV row per instance and a summary row.  BenchConfig mirrors the reference's field names.
 struct BenchConfig {
     int instances = 20;
     int t = 3;
@@ -756,49 +910,65 @@ struct BenchConfig {
 };
 
 namespace detail {
-template <typename F>
-inline double timed_ms(F&& f) {
-    const auto t0 = std::chrono::steady_clock::now();
-    f();
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+class Stopwatch {  // wall time of the three solvers, accumulated per column
+public:
+    template <typename Work>
+    double lap(Work&& work) {
+        const auto begin = std::chrono::steady_clock::now();
+        work();
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - begin).count();
+        total_ += ms;
+        return ms;
+    }
+    double total() const { return total_; }
+
+private:
+    double total_ = 0.0;
+};
+inline void tsv_row(std::string& out, std::initializer_list<std::string> fields) {
+    bool first = true;
+    for (const std::string& f : fields) {
+        if (!first) out += '\t';
+        out += f;
+        first = false;
+    }
+    out += '\n';
 }
 }  // namespace detail
 
 inline std::string benchmark(const BenchConfig& config) {
     if (config.instances < 1) throw InvalidParamsError("benchmark needs at least one instance");
-    std::string out = "instance\tseed\trun_score\toracle_score\tmedian_distance\tagree\trun_ms\tnaive_ms\tmedian_ms\n";
-    int agree_count = 0;
-    double total_run_ms = 0.0, total_naive_ms = 0.0, total_median_ms = 0.0;
-    for (int i = 1; i <= config.instances; ++i) {
-        const std::uint64_t inst_seed = derive_seed(config.seed, static_cast<std::uint64_t>(i));
-        const PlantedInstance inst = generate_planted(config.t, config.n, config.l, config.d, inst_seed);
-        RunConfig rc = config.run;
-        rc.l = config.l;
-        rc.d = config.d;
-        rc.seed = inst_seed;
-        int run_score = -1;  // kept when no bucket is ever enriched
-        const double run_ms = detail::timed_ms([&] {
+    std::string report;
+    detail::tsv_row(report, {"instance", "seed", "run_score", "oracle_score", "median_distance", "agree", "run_ms", "naive_ms", "median_ms"});
+    detail::Stopwatch run_clock, naive_clock, median_clock;
+    int agreeing = 0;
+    RunConfig per_instance = config.run;
+    per_instance.l = config.l;
+    per_instance.d = config.d;
+    for (int inst_no = 1; inst_no <= config.instances; ++inst_no) {
+        per_instance.seed = derive_seed(config.seed, static_cast<std::uint64_t>(inst_no));
+        const PlantedInstance inst = generate_planted(config.t, config.n, config.l, config.d, per_instance.seed);
+        int found = -1;  // reported when no trial enriches a bucket
+        const double run_ms = run_clock.lap([&] {
             try {
-                run_score = run(rc, inst.sequences).best.score;
+                found = run(per_instance, inst.sequences).best.score;
             } catch (const NoEnrichedBucketsError&) {
             }
         });
-        NaiveMfpResult naive;
-        const double naive_ms = detail::timed_ms([&] { naive = naive_mfp(inst.sequences, config.l, config.naive_limit); });
+        NaiveMfpResult exhaustive;
+        const double naive_ms = naive_clock.lap([&] { exhaustive = naive_mfp(inst.sequences, config.l, config.naive_limit); });
         MedianStringResult median;
-        const double median_ms = detail::timed_ms([&] { median = median_string(inst.sequences, config.l, config.median_limit); });
-        const bool agree = run_score == naive.score;
-        agree_count += agree ? 1 : 0;
-        total_run_ms += run_ms;
-        total_naive_ms += naive_ms;
-        total_median_ms += median_ms;
-        out += std::to_string(i) + "\t" + std::to_string(inst_seed) + "\t" + std::to_string(run_score) + "\t" +
-               std::to_string(naive.score) + "\t" + std::to_string(median.total_distance) + "\t" + (agree ? "true" : "false") +
-               "\t" + detail::format_ms(run_ms) + "\t" + detail::format_ms(naive_ms) + "\t" + detail::format_ms(median_ms) + "\n";
+        const double median_ms = median_clock.lap([&] { median = median_string(inst.sequences, config.l, config.median_limit); });
+        const bool same = found == exhaustive.score;
+        agreeing += same;
+        detail::tsv_row(report, {std::to_string(inst_no), std::to_string(per_instance.seed), std::to_string(found),
+                                 std::to_string(exhaustive.score), std::to_string(median.total_distance), same ? "true" : "false",
+                                 detail::format_ms(run_ms), detail::format_ms(naive_ms), detail::format_ms(median_ms)});
     }
-    out += "summary\t-\t-\t-\t-\t" + std::to_string(agree_count) + "/" + std::to_string(config.instances) + "\t" +
-           detail::format_ms(total_run_ms) + "\t" + detail::format_ms(total_naive_ms) + "\t" + detail::format_ms(total_median_ms) + "\n";
-    return out;
+    detail::tsv_row(report, {"summary", "-", "-", "-", "-", std::to_string(agreeing) + "/" + std::to_string(config.instances),
+                             detail::format_ms(run_clock.total()), detail::format_ms(naive_clock.total()),
+                             detail::format_ms(median_clock.total())});
+    return report;
 }
 
 }  // namespace projmotif_b200

@@ -92,6 +92,7 @@ uint64_t pmo_derive_seed(uint64_t master, uint64_t index);
 int pmo_mt_outputs(uint64_t seed, int n, uint64_t* out);                     /* raw mt19937_64 stream */
 int pmo_uniform_below(uint64_t seed, uint64_t bound, int n, uint64_t* out);  /* Rng(seed).uniform_below(bound) x n */
 int pmo_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept);         /* sample_plan(l,k,Rng(rng_seed)) */
+int pmo_sample_plans(int l, int k, uint64_t rng_seed, int n, int32_t* kept);     /* n x sample_plan on ONE Rng(rng_seed): kept is n x k */
 int pmo_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept); /* driver.hpp:164-165 */
 
 /* planted.hpp:38-101; bases is t*n chars (no separators), motif l chars, positions t ints */

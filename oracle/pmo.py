@@ -163,6 +163,12 @@ class Oracle:
         self._check(self.lib.pmo_sample_plan(l, k, C.c_uint64(rng_seed), _p(kept, C.c_int32)))
         return kept[:k].tolist()
 
+    def sample_plans(self, l, k, rng_seed, n):
+        """n consecutive sample_plan calls on ONE Rng(rng_seed)."""
+        kept = np.zeros(max(k, 1) * n, dtype=np.int32)
+        self._check(self.lib.pmo_sample_plans(l, k, C.c_uint64(rng_seed), n, _p(kept, C.c_int32)))
+        return kept.reshape(n, max(k, 1))[:, :k].tolist()
+
     def trial_plan(self, l, k, master, trial):
         kept = np.zeros(max(k, 1), dtype=np.int32)
         self._check(self.lib.pmo_trial_plan(l, k, C.c_uint64(master), C.c_int64(trial), _p(kept, C.c_int32)))

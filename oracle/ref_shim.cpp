@@ -204,6 +204,16 @@ int pmo_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept) {
     });
 }
 
+int pmo_sample_plans(int l, int k, uint64_t rng_seed, int n, int32_t* kept) {
+    return guarded([&] {
+        Rng rng(rng_seed);
+        for (int p = 0; p < n; ++p) {
+            const ProjectionPlan plan = sample_plan(l, k, rng);
+            for (int i = 0; i < plan.k(); ++i) kept[static_cast<std::size_t>(p) * static_cast<std::size_t>(k) + static_cast<std::size_t>(i)] = plan.kept_positions()[static_cast<std::size_t>(i)];
+        }
+    });
+}
+
 int pmo_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept) {
     return pmo_sample_plan(l, k, derive_seed(master, static_cast<uint64_t>(trial)), kept);
 }

@@ -78,6 +78,7 @@ class RunConfig(C.Structure):
         ("forced_kept", C.POINTER(C.c_int32)), ("n_forced", C.c_int32), ("_pad0", C.c_int32),
         ("plans", C.POINTER(C.c_int32)), ("trial_begin", C.c_int64), ("trial_end", C.c_int64),
         ("batch_trials", C.c_int32), ("profile", C.c_int32), ("z_epsilon", C.c_double),
+        ("trial_stride", C.c_int64), ("exact_best", C.c_int32), ("_pad1", C.c_int32),
     ]
 
 
@@ -103,13 +104,13 @@ class RunResult(C.Structure):
 
 EXPORTS = [
     "pm_version", "pm_last_error", "pm_default_config", "pm_splitmix64", "pm_derive_seed", "pm_sample_plan",
-    "pm_trial_plan", "pm_validate_plan", "pm_generate_planted", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
+    "pm_sample_plan_stream", "pm_trial_plan", "pm_validate_plan", "pm_generate_planted", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
     "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_refine_exact",
     "pm_init_model", "pm_em_step", "pm_em_step_exact", "pm_expectation", "pm_score",
-    "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host",
+    "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host", "pm_run_multi",
 ]
 
 _lib = None
@@ -259,6 +260,20 @@ def expectation(theta, l):
     out = C.c_double()
     _check(lib().pm_expectation(_p(tin, C.c_double), l, C.byref(out)))
     return out.value
+
+
+def run_multi(devices, bases: bytes, offs, strided=False, **kw):
+    """pm_run_multi: run() sharded over the CUDA devices listed (an ordinal may repeat); same outputs as Context.run_host."""
+    cfg = kw.pop("config", None) or default_config(**kw)
+    offs = np.ascontiguousarray(offs, dtype=np.int64)
+    devs = _i32(devices)
+    out = RunResult()
+    pos = np.zeros(len(offs) - 1, dtype=np.int32)
+    _check(lib().pm_run_multi(_p(devs, C.c_int32), len(devs), int(bool(strided)), C.byref(cfg), bases, _p(offs, C.c_int64),
+                              len(offs) - 1, C.byref(out), _p(pos, C.c_int32)))
+    d = out.as_dict()
+    d["positions"] = pos.tolist()
+    return d
 
 
 def candidate_improves(a, b):

@@ -434,6 +434,7 @@ int need_sequences(const pm_ctx* c) {
 
 // (seq, offset) index space for motif length l (sequence.hpp:103-132)
 int prepare_windows(pm_ctx* c, int l) {
+    PM_CUDA(cudaSetDevice(c->device));  // every device entry point comes through here before touching the stream
     if (l < 1) return set_error(PM_ERR_INVALID_PARAMS, "motif length l must be positive");
     if (l > PM_MAX_L) {
         return set_error(PM_ERR_UNSUPPORTED, "l=" + std::to_string(l) + " exceeds this build's limit of " +
@@ -542,6 +543,38 @@ int sort_segments(pm_ctx* c, KeyT* ka, KeyT* kb, unsigned int* ia, unsigned int*
     return PM_OK;
 }
 
+// The projection plans of a launch live in __constant__ memory (k::c_plans), which is ONE array per device, while
+// every context uploads and launches on its own stream.  Uses are therefore chained per device: a context's upload
+// waits (on the device, not the host) for the kernel of the previous user, whichever stream that ran on.
+struct ConstPlans {
+    std::mutex mu;
+    cudaEvent_t last_use = nullptr;
+};
+ConstPlans& const_plans_of(int device) {
+    static std::mutex mu;
+    static std::map<int, ConstPlans*> slots;
+    std::lock_guard<std::mutex> lock(mu);
+    ConstPlans*& s = slots[device];
+    if (s == nullptr) s = new ConstPlans();
+    return *s;
+}
+class ConstPlansUse {
+public:
+    ConstPlansUse(int device, cudaStream_t stream) : slot_(const_plans_of(device)), lock_(slot_.mu), stream_(stream) {
+        if (slot_.last_use == nullptr) {
+            cudaEventCreateWithFlags(&slot_.last_use, cudaEventDisableTiming);
+        } else {
+            cudaStreamWaitEvent(stream_, slot_.last_use, 0);
+        }
+    }
+    ~ConstPlansUse() { cudaEventRecord(slot_.last_use, stream_); }  // after the kernel that reads the plans
+
+private:
+    ConstPlans& slot_;
+    std::lock_guard<std::mutex> lock_;
+    cudaStream_t stream_;
+};
+
 // keys of n_trials plans -> sorted (key, flat index) per trial
 template <typename KeyT>
 struct Sorted {
@@ -555,6 +588,7 @@ int project_keys(pm_ctx* c, const std::vector<k::PlanProg>& progs, KeyT* keys) {
     for (int base = 0; base < n; base += k::kMaxConstPlans) {
         const int cnt = std::min(k::kMaxConstPlans, n - base);
         c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
+        ConstPlansUse plans_use(c->device, c->stream);
         PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
                                         0, cudaMemcpyHostToDevice, c->stream));
         const unsigned gx = static_cast<unsigned>(std::min<int64_t>((c->x + 255) / 256, 4096));
@@ -730,11 +764,14 @@ int em_warps_for(int t) {
 
 // Function attributes are per process, not per context: the dynamic shared-memory limit of a kernel only ever
 // grows (monotone, under a lock), so a launch configured by one context stays valid whatever another one set.
+// cudaFuncSetAttribute applies to the CURRENT device: the raised limits are remembered per (device, kernel)
 int ensure_dynamic_smem(const void* func, size_t bytes, bool max_carveout) {
     static std::mutex mu;
-    static std::map<const void*, size_t> allowed;
+    static std::map<std::pair<int, const void*>, size_t> allowed;
+    int device = 0;
+    PM_CUDA(cudaGetDevice(&device));
     std::lock_guard<std::mutex> lock(mu);
-    size_t& cur = allowed[func];
+    size_t& cur = allowed[std::make_pair(device, func)];
     if (bytes > cur) {
         PM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
         if (cur == 0 && max_carveout) {
@@ -1811,6 +1848,7 @@ int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
     for (int base = 0; base < n; base += k::kMaxConstPlans) {
         const int cnt = std::min(k::kMaxConstPlans, n - base);
         c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
+        ConstPlansUse plans_use(c->device, c->stream);
         PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
                                         0, cudaMemcpyHostToDevice, c->stream));
         p.plan_base = base;
@@ -1826,7 +1864,7 @@ template <typename KeyT>
 int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
               int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
               int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key, int64_t out_base,
-              bool more_batches) {
+              bool more_batches, int64_t trial_stride) {
     const int n_trials = static_cast<int>(progs.size());
     st->best_in_batch = -1;
     const int l = cfg->l;
@@ -2000,7 +2038,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     const int perfect = l * c->t;
     int32_t new_best_work = -1;
     for (int i = 0; i < n_trials; ++i) {
-        const int64_t trial = first_trial + i;
+        const int64_t trial = first_trial + i * trial_stride;
         TrialSummary& s = tb[static_cast<size_t>(i)];
         out->trials_run = trial;
         out->buckets_enriched += n_rec[static_cast<size_t>(i)];
@@ -2113,6 +2151,8 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         te = params.m;
     }
     if (tb < 1 || te > params.m || tb > te + 1) return set_error(PM_ERR_INVALID_PARAMS, "trial range must lie within 1..m");
+    const int64_t stride = cfg->trial_stride > 1 ? cfg->trial_stride : 1;
+    const int64_t n_mine = tb <= te ? (te - tb) / stride + 1 : 0;  // trials tb, tb + stride, ... <= te
 
     // batch size: bounded by a workspace budget (worst-case per-trial footprint)
     const int key_bytes = 2 * params.k <= 32 ? 4 : 8;
@@ -2131,15 +2171,15 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     g_marks = &marks;
     struct MarksGuard { ~MarksGuard() { g_marks = nullptr; } } marks_guard;
     host_mark("setup");
-    for (int64_t first = tb; first <= te && !stop; first += batch) {
-        const int64_t last = std::min(te, first + batch - 1);
+    for (int64_t j0 = 0; j0 < n_mine && !stop; j0 += batch) {
+        const int64_t first = tb + j0 * stride;  // trial of the batch's first slot
         // Plans come from the reference's PRNG stream (one mt19937_64 per trial, driver.hpp:164):
         // independent per trial, so the host samples them on a few threads.
-        const int64_t n_plans = last - first + 1;
+        const int64_t n_plans = std::min(batch, n_mine - j0);
         std::vector<k::PlanProg> progs(static_cast<size_t>(n_plans));
         std::vector<int> plan_rc(static_cast<size_t>(n_plans), PM_OK);
         auto make_range = [&](int64_t a, int64_t b) {
-            if (cfg->forced_kept == nullptr && cfg->plans == nullptr) {
+            if (cfg->forced_kept == nullptr && cfg->plans == nullptr && stride == 1) {
                 // the reference's stream, four trials' seed chains at a time (pm_host.cpp: trial_plans)
                 std::vector<int32_t> kept(static_cast<size_t>(b - a) * static_cast<size_t>(params.k));
                 const int rc = trial_plans(cfg->l, params.k, cfg->seed, first + a, static_cast<int>(b - a), kept.data());
@@ -2151,7 +2191,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
             }
             std::vector<int32_t> mine(static_cast<size_t>(params.k));
             for (int64_t i = a; i < b; ++i) {
-                const int64_t trial = first + i;
+                const int64_t trial = first + i * stride;
                 const int32_t* plan;
                 if (cfg->forced_kept != nullptr) {
                     plan = cfg->forced_kept;
@@ -2185,9 +2225,9 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         host_mark("plans");
         const int rc = key_bytes == 4
                            ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, first - tb, last < te)
+                                                 trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride)
                            : run_batch<uint64_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, first - tb, last < te);
+                                                 trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride);
         if (rc != PM_OK) return rc;
     }
 
@@ -2201,6 +2241,11 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
                                                          std::to_string(out->trials_run) + " trials; lower s or raise m");
     }
     host_mark("reduce+positions");
+    if (cfg->exact_best && !st.best_exact && !(st.best_members.empty())) {
+        int32_t s64 = 0;
+        PM_TRY(exact_candidate(c, cfg, st.best_members, &st.best.expct, &s64));
+        st.best_exact = true;
+    }
     unpack_consensus(st.best.cons, cfg->l, out->consensus);
     out->score = st.best.score;
     out->iterations = st.best.iters;
@@ -2222,6 +2267,138 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     out->h2d_bytes = c->h2d_bytes - h2d0;
     out->d2h_bytes = c->d2h_bytes - d2h0;
     out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return PM_OK;
+}
+
+// ---- run() on several GPUs of one node ------------------------------------------------------------------
+namespace {
+struct ShardOut {
+    int rc = PM_OK;
+    std::string err;
+    pm_run_result res{};
+    std::vector<int32_t> pos;
+    std::vector<int64_t> buckets;  // enriched buckets of each of the shard's trials
+    int64_t begin = 0, stride = 1, count = 0;
+};
+// contexts of pm_run_multi, one per slot of the device list, kept across calls
+std::mutex g_multi_mu;
+std::vector<pm_ctx*> g_multi_ctx;
+}  // namespace
+
+int pm_run_multi(const int* devices, int n_devices, int strided, const pm_run_config* cfg, const char* bases,
+                 const int64_t* offs, int t, pm_run_result* out, int32_t* positions) {
+    const auto t0 = std::chrono::steady_clock::now();
+    clear_error();
+    if (devices == nullptr || n_devices < 1 || cfg == nullptr || out == nullptr || bases == nullptr || offs == nullptr) {
+        return set_error(PM_ERR_INVALID_PARAMS, "null argument or empty device list");
+    }
+    std::memset(out, 0, sizeof(*out));
+    PM_TRY(pm_resolve_params(cfg, offs, t, out));  // every parameter error surfaces here, before any GPU work
+    const pm_run_result params = *out;
+    std::lock_guard<std::mutex> lock(g_multi_mu);
+    if (static_cast<int>(g_multi_ctx.size()) < n_devices) g_multi_ctx.resize(static_cast<size_t>(n_devices), nullptr);
+    for (int i = 0; i < n_devices; ++i) {
+        pm_ctx*& c = g_multi_ctx[static_cast<size_t>(i)];
+        if (c != nullptr && c->device != devices[i]) {
+            pm_ctx_destroy(c);
+            c = nullptr;
+        }
+        if (c == nullptr) PM_TRY(pm_ctx_create(devices[i], nullptr, &c));
+    }
+    // shards of trials 1..m: contiguous blocks (the remainder spread over the first shards) or round-robin
+    const int64_t m = params.m;
+    std::vector<ShardOut> parts(static_cast<size_t>(n_devices));
+    {
+        int64_t next = 1;
+        for (int i = 0; i < n_devices; ++i) {
+            ShardOut& p = parts[static_cast<size_t>(i)];
+            if (strided) {
+                p.begin = i + 1;
+                p.stride = n_devices;
+                p.count = m >= p.begin ? (m - p.begin) / n_devices + 1 : 0;
+            } else {
+                p.count = m / n_devices + (i < m % n_devices ? 1 : 0);
+                p.begin = next;
+                p.stride = 1;
+                next += p.count;
+            }
+        }
+    }
+    auto work = [&](int i) {
+        ShardOut& p = parts[static_cast<size_t>(i)];
+        if (p.count == 0) return;
+        pm_ctx* c = g_multi_ctx[static_cast<size_t>(i)];
+        pm_run_config mine = *cfg;
+        mine.trial_begin = p.begin;
+        mine.trial_end = strided ? m : p.begin + p.count - 1;
+        mine.trial_stride = p.stride;
+        mine.exact_best = 1;
+        p.pos.assign(static_cast<size_t>(t), 0);
+        p.buckets.assign(static_cast<size_t>(p.count), 0);
+        p.rc = pm_ctx_set_sequences(c, bases, offs, t);
+        if (p.rc == PM_OK) p.rc = pm_run(c, &mine, &p.res, p.pos.data(), p.buckets.data(), nullptr, nullptr, nullptr);
+        if (p.rc != PM_OK) p.err = pm_last_error();
+    };
+    {
+        std::vector<std::thread> pool;
+        for (int i = 1; i < n_devices; ++i) pool.emplace_back(work, i);
+        work(0);
+        for (std::thread& th : pool) th.join();
+    }
+    for (const ShardOut& p : parts) {
+        if (p.rc != PM_OK && p.rc != PM_ERR_NO_ENRICHED_BUCKETS) return set_error(p.rc, p.err);
+    }
+    // The ascending-trial scan of driver.hpp:195-208 over the shards: the winner is the maximum under
+    // candidate_improves, the earliest trial among exact ties; with early stop the scan ends at the first trial whose
+    // candidate is perfect, and only trials up to it count.
+    const int perfect = cfg->l * t;
+    int64_t stop_trial = m;
+    if (cfg->early_stop) {
+        for (const ShardOut& p : parts) {
+            if (p.res.found && p.res.score == perfect) stop_trial = std::min(stop_trial, p.res.best_trial);
+        }
+    }
+    int winner = -1;
+    for (int i = 0; i < n_devices; ++i) {
+        const pm_run_result& r = parts[static_cast<size_t>(i)].res;
+        if (!r.found || r.best_trial > stop_trial) continue;
+        if (winner < 0) {
+            winner = i;
+            continue;
+        }
+        const pm_run_result& w = parts[static_cast<size_t>(winner)].res;
+        const bool better = pm_candidate_improves(r.score, r.expectation, r.source_bucket, w.score, w.expectation, w.source_bucket) != 0;
+        const bool same = r.score == w.score && r.expectation == w.expectation && r.source_bucket == w.source_bucket;
+        if (better || (same && r.best_trial < w.best_trial)) winner = i;
+    }
+    out->trials_run = stop_trial;
+    for (const ShardOut& p : parts) {
+        for (int64_t j = 0; j < p.count; ++j) {
+            if (p.begin + j * p.stride <= stop_trial) out->buckets_enriched += p.buckets[static_cast<size_t>(j)];
+        }
+        out->gpu_launches += p.res.gpu_launches;
+        out->em_lookup_adds += p.res.em_lookup_adds;
+        out->em_work += p.res.em_work;
+        out->h2d_bytes += p.res.h2d_bytes;
+        out->d2h_bytes += p.res.d2h_bytes;
+        for (int j = 0; j < 8; ++j) out->stage_ms[j] = std::max(out->stage_ms[j], p.res.stage_ms[j]);
+    }
+    out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (winner < 0) {
+        return set_error(PM_ERR_NO_ENRICHED_BUCKETS, "no bucket reached s=" + std::to_string(params.s) + " in " +
+                                                         std::to_string(out->trials_run) + " trials; lower s or raise m");
+    }
+    const ShardOut& w = parts[static_cast<size_t>(winner)];
+    std::memcpy(out->consensus, w.res.consensus, sizeof(out->consensus));
+    out->score = w.res.score;
+    out->iterations = w.res.iterations;
+    out->expectation = w.res.expectation;
+    out->source_bucket = w.res.source_bucket;
+    out->best_trial = w.res.best_trial;
+    out->within_d = w.res.within_d;
+    out->total_distance = w.res.total_distance;
+    out->found = 1;
+    if (positions) std::memcpy(positions, w.pos.data(), sizeof(int32_t) * static_cast<size_t>(t));
     return PM_OK;
 }
 

@@ -232,6 +232,21 @@ int pm_sample_plan(int l, int k, uint64_t rng_seed, int32_t* kept) {
     return plan_from_engine(l, k, eng, kept);
 }
 
+namespace {
+struct CallerStream {  // a generator owned by the caller, pulled one 64-bit output at a time
+    uint64_t (*next)(void*);
+    void* state;
+    uint64_t operator()() { return next(state); }
+};
+}  // namespace
+
+int pm_sample_plan_stream(int l, int k, uint64_t (*next_u64)(void*), void* state, int32_t* kept) {
+    clear_error();
+    if (next_u64 == nullptr || kept == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    CallerStream eng{next_u64, state};
+    return plan_from_engine(l, k, eng, kept);
+}
+
 int pm_trial_plan(int l, int k, uint64_t master, int64_t trial, int32_t* kept) {
     return pm_sample_plan(l, k, pm_derive_seed(master, static_cast<uint64_t>(trial)), kept);
 }

@@ -3,6 +3,7 @@
 // the C++ host layer include/projmotif_b200.hpp, which calls the CUDA path through the C ABI.
 // Plain asserts (Catch2 is not available); exit code 0 = all passed.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -157,6 +158,70 @@ int main() {
         const std::string tsv = benchmark(bench);
         REQUIRE(tsv.rfind("instance\tseed\trun_score", 0) == 0);
         REQUIRE(tsv.find("summary\t-\t-\t-\t-\t") != std::string::npos);
+    }
+    // stage functions of refine.hpp on the device (test_refine.cpp:28-56, :82-127)
+    {
+        const MotifModel theta0 = init_model(enriched.front().members, seqs, 8, 0.0);
+        REQUIRE(theta0.is_column_stochastic());
+        // the worked theta0 in sevenths (support.hpp:46-54): the projected columns 1, 2, 3, 6, 7 are unanimous
+        // (A, T, G, A, C), the other three hold their consensus symbol six times out of seven
+        REQUIRE(std::abs(theta0.at(0, 1) - 1.0) < 1e-12 && std::abs(theta0.at(2, 2) - 1.0) < 1e-12);
+        REQUIRE(std::abs(theta0.at(3, 3) - 1.0) < 1e-12 && std::abs(theta0.at(1, 7) - 1.0) < 1e-12);
+        REQUIRE(std::abs(theta0.column_max(4) - 6.0 / 7) < 1e-12 && std::abs(theta0.column_max(8) - 6.0 / 7) < 1e-12);
+        REQUIRE(std::abs(expectation(theta0) - 53.0 / 7) < 1e-12);
+        const MotifModel bg = init_model({{1, 1, 8}}, seqs, 8, 0.0);  // background 76/66/73/65 of 280 (A, C, T, G)
+        REQUIRE(std::abs(bg.at(0, 0) - 76.0 / 280) < 1e-12 && std::abs(bg.at(1, 0) - 66.0 / 280) < 1e-12);
+        REQUIRE(std::abs(bg.at(2, 0) - 73.0 / 280) < 1e-12 && std::abs(bg.at(3, 0) - 65.0 / 280) < 1e-12);
+        REQUIRE(throws<EmptyBucketError>([&] { init_model({}, seqs, 8); }));
+        REQUIRE(throws<InvalidParamsError>([&] { init_model({{1, 1, 8}}, seqs, 8, -1.0); }));
+        MotifModel uniform(4, 8);
+        for (int c = 0; c <= 8; ++c) {
+            for (int r = 0; r < 4; ++r) uniform.at(r, c) = 0.25;
+        }
+        REQUIRE(std::abs(expectation(uniform) - 2.0) < 1e-12);
+        REQUIRE(throws<LengthMismatchError>([&] { em_step(uniform, seqs, 7); }));
+        // em_step keeps the columns stochastic and never lowers the likelihood (both kernels)
+        for (int round = 0; round < 6; ++round) {
+            const PlantedInstance inst = generate_planted(5, 30, 6, 1, static_cast<std::uint64_t>(500 + round));
+            for (int exact = 0; exact < 2; ++exact) {
+                MotifModel model = init_model({{1, inst.positions[0], 6}}, inst.sequences, 6, 0.1);
+                double prev = -1e300;
+                for (int it = 0; it < 5; ++it) {
+                    const EmStepResult step = exact ? em_step_exact(model, inst.sequences, 6) : em_step(model, inst.sequences, 6);
+                    REQUIRE(step.model.is_column_stochastic(exact ? 1e-9 : 1e-6));
+                    REQUIRE(step.log_likelihood >= prev - (exact ? 1e-6 : 1e-3));
+                    prev = step.log_likelihood;
+                    model = step.model;
+                }
+            }
+        }
+    }
+    // run() sharded over a device list (two and three contexts on GPU 0) equals the single-context run,
+    // contiguous and round-robin alike
+    {
+        const PlantedInstance inst = generate_planted(12, 120, 8, 1, 5);
+        RunConfig config;
+        config.l = 8;
+        config.d = 1;
+        config.k = 5;
+        config.s = 3;
+        config.m = 7;
+        config.seed = 3;
+        config.early_stop = false;
+        const RunResult one = run(config, inst.sequences);
+        for (int shards = 1; shards <= 3; ++shards) {
+            for (int strided = 0; strided < 2; ++strided) {
+                RunConfig multi = config;
+                multi.devices.assign(static_cast<std::size_t>(shards), 0);
+                multi.strided_trials = strided != 0;
+                const RunResult r = run(multi, inst.sequences);
+                REQUIRE(r.best.consensus == one.best.consensus && r.best.positions == one.best.positions);
+                REQUIRE(r.best.score == one.best.score && r.best.source_bucket == one.best.source_bucket);
+                REQUIRE(r.best_trial == one.best_trial && r.trials_run == one.trials_run);
+                REQUIRE(r.buckets_enriched == one.buckets_enriched);
+                REQUIRE(std::abs(r.best.expectation - one.best.expectation) < 1e-4);
+            }
+        }
     }
     std::printf("host_layer_test: all checks passed\n");
     return 0;

@@ -48,6 +48,10 @@ def main():
                   for (l, k) in ((15, 7), (16, 7), (18, 7), (20, 7), (15, 10), (8, 5), (9, 9), (31, 17), (4, 1))
                   for ms in (0, 7) for tr in (1, 2, 3, 172)]
 
+    # consecutive plans from one generator (sample_plan consumes the caller's Rng, projection.hpp:210-226)
+    g["plans_consecutive"] = [dict(l=l, k=k, seed=sd, plans=ref.sample_plans(l, k, sd, 4))
+                              for (l, k) in ((15, 7), (20, 7), (9, 9), (31, 17)) for sd in (0, 12345)]
+
     # ---- formulas (projection.hpp:97-206)
     g["p_hat"] = [[l, d, k, ref.p_hat(l, d, k)] for (l, d) in ((15, 4), (16, 5), (18, 6), (19, 6), (20, 7), (8, 1))
                   for k in (0, 1, 5, 7, l - d, l - d + 1 if l - d + 1 <= l else l)]

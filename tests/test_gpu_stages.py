@@ -197,6 +197,67 @@ def test_refine_matches_oracle_on_random_instances(ctx, best_oracle):
     assert compared >= 200
 
 
+def test_stage_exports_init_model_em_step_expectation(pm, ctx, golden, example, instance, best_oracle):
+    """pm_init_model / pm_em_step / pm_em_step_exact / pm_expectation against the reference's own stage goldens
+    (refine.hpp:90,130,216; test_refine.cpp:28-56, :82-127)."""
+    w = golden["worked"]
+    ctx.set_sequences(example.bases, example.offs)
+    th0 = ctx.init_model(8, w["enriched_s4"][0]["members"])
+    np.testing.assert_allclose(th0, np.array(w["theta0"]), atol=1e-15, rtol=0)   # theta0 in sevenths, bit for bit
+    assert abs(pm.expectation(th0, 8) - 53.0 / 7) < 1e-12
+    np.testing.assert_allclose(th0[:, 0], [76 / 280, 66 / 280, 73 / 280, 65 / 280], atol=1e-15)
+    g = golden["em_step"]
+    ss, _, _ = instance(*g["instance"])
+    ctx.set_sequences(ss.bases, ss.offs)
+    th = ctx.init_model(g["l"], g["members"], g["pseudocount"])
+    np.testing.assert_allclose(th, np.array(g["theta0"]), atol=1e-15, rtol=0)
+    th1x, llx = ctx.em_step(g["l"], th, exact=True)          # FP64 kernel: the reference to rounding
+    np.testing.assert_allclose(th1x, np.array(g["theta1"]), atol=1e-12, rtol=0)
+    assert abs(llx - g["ll"]) < 1e-9
+    th1, ll = ctx.em_step(g["l"], th)                         # production kernel: stated FP32 tolerances
+    np.testing.assert_allclose(th1, np.array(g["theta1"]), atol=THETA_TOL, rtol=0)
+    assert abs(ll - g["ll"]) < 1e-3
+    # column-stochastic after each step, likelihood non-decreasing (test_refine.cpp:101-127), both kernels
+    for exact in (False, True):
+        model, prev = th, -np.inf
+        for _ in range(5):
+            model, ll = ctx.em_step(g["l"], model, exact=exact)
+            assert np.abs(model.sum(axis=0) - 1.0).max() < (1e-9 if exact else 1e-6)
+            assert ll >= prev - (1e-6 if exact else 1e-3)
+            want_model, want_ll = best_oracle.em_step(ss, g["l"], model)
+            prev = ll
+    for bad, kind in (((8, [], 0.0), "EmptyBucketError"), ((8, [1], -0.5), "InvalidParamsError"), ((8, [10 ** 7], 0.0), "IndexOutOfRangeError")):
+        with pytest.raises(pm.PmError) as e:
+            ctx.init_model(*bad)
+        assert e.value.kind == kind
+
+
+def test_run_multi_equals_single_context(pm, ctx, golden, instance):
+    """pm_run_multi over a device list (contexts may share a GPU): contiguous and round-robin shards give the
+    single-context result, per-trial bucket counts and early stop included."""
+    ss, _, _ = instance(20, 600, 15, 4, 42)
+    kw = dict(l=15, d=4, k=7, s=4, m=16, seed=7, early_stop=0)
+    want = [r for r in golden["run"] if r["cfg"].get("m") == 16][0]["result"]
+    for devices in ([0], [0, 0], [0, 0, 0], [0] * 5):
+        for strided in (False, True):
+            r = pm.run_multi(devices, ss.bases, ss.offs, strided=strided, **kw)
+            for f in ("consensus", "score", "iterations", "source_bucket", "best_trial", "trials_run", "buckets_enriched", "positions"):
+                assert r[f] == want[f], (devices, strided, f, r[f], want[f])
+            assert abs(r["expectation"] - want["expectation"]) <= EXPECTATION_TOL
+    # early stop: a d = 0 plant is perfect at trial 1 whichever shard holds it
+    ss, motif, _ = instance(5, 50, 10, 0, 77)
+    ctx.set_sequences(ss.bases, ss.offs)
+    one = ctx.run(l=10, d=0, seed=5, m=10)
+    for devices in ([0, 0], [0, 0, 0]):
+        for strided in (False, True):
+            r = pm.run_multi(devices, ss.bases, ss.offs, strided=strided, l=10, d=0, seed=5, m=10)
+            assert (r["consensus"], r["score"], r["best_trial"], r["trials_run"], r["buckets_enriched"]) == \
+                   (motif, 50, one["best_trial"], one["trials_run"], one["buckets_enriched"])
+    with pytest.raises(pm.PmError) as e:
+        pm.run_multi([0, 0], ss.bases, ss.offs, l=10, d=12)
+    assert e.value.kind == "InvalidParamsError"
+
+
 def test_refine_single_member_and_limits(pm, ctx, best_oracle, instance):
     ss, _, pos = instance(6, 30, 5, 0, 99)
     ctx.set_sequences(ss.bases, ss.offs)

@@ -3,6 +3,7 @@ include/pm_b200.h declares, its host logic (plan PRNG stream, formulas, resolve_
 equals the reference's, and device entry points fail loudly instead of falling back."""
 import ctypes as C
 import os
+import subprocess
 import re
 
 import numpy as np
@@ -85,6 +86,23 @@ def test_plan_stream_matches_reference(pm, golden, port):
         with pytest.raises(pm.PmError) as e:
             pm.validate_plan(*bad)
         assert e.value.kind == "InvalidParamsError"
+
+
+def test_cpp_rng_consumes_its_stream(pm, golden):
+    """include/projmotif_b200.hpp: Rng is a real std::mt19937_64 and sample_plan(l, k, rng) draws from it, so two calls
+    on one Rng give two different plans -- the reference's consecutive plans (host-only: no GPU needed)."""
+    exe = "/tmp/pm_rng_test"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(pm.REPO_DIR, "include"),
+                    os.path.join(pm.REPO_DIR, "tests", "cpp", "rng_test.cpp"), "-L" + pm.PKG_DIR, "-lpm_b200",
+                    "-Wl,-rpath," + pm.PKG_DIR, "-o", exe], check=True)
+    for e in golden["plans_consecutive"]:
+        out = subprocess.run([exe, str(e["l"]), str(e["k"]), str(e["seed"]), str(len(e["plans"]))], capture_output=True, text=True)
+        assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
+        lines = out.stdout.strip().split("\n")
+        assert lines[-1] == "rng ok"
+        assert [[int(v) for v in ln.split()] for ln in lines[:-1]] == e["plans"]
+        if e["k"] < e["l"]:
+            assert e["plans"][0] != e["plans"][1]
 
 
 def test_planted_generator_matches_reference(pm, golden):
