@@ -9,8 +9,8 @@ A step = one full pass of the hot path (hash -> bucket -> EM-refine -> score -> 
 batch of projection trials on synthetic planted-(l,d) data: by default config C1 of BASELINE.json
 (the (15,4) instance the metric names): t=20 x n=600, k=7, s=4, m=172 trials (the reference's own
 trial count for q=0.95), instance seed 42, run seed 7, early_stop off.  With N ranks every rank
-runs its own contiguous shard of N*m trials (weak scaling) and the per-rank bests are merged with
-one all_gather (NCCL) inside the timed step.
+runs its own contiguous shard of N*m trials (weak scaling; --scaling strong shards the config's own m) and
+the per-rank bests are merged with one all_gather (NCCL) inside the timed step.
 Prints ONE JSON line (see DESIGN.md §7 for every key).
 """
 from __future__ import annotations
@@ -37,6 +37,7 @@ CONFIGS = {
     "c1": dict(t=20, n=600, l=15, d=4, k=7, s=4, m=172, label="C1 planted (15,4) t=20 n=600 k=7 s=4"),
     "c2": dict(t=20, n=1000, l=16, d=5, k=7, s=4, m=1293, label="C2 planted (16,5) t=20 n=1000 k=7 s=4"),
     "c3": dict(t=20, n=1000, l=18, d=6, k=7, s=4, m=2218, label="C3 planted (18,6) t=20 n=1000 k=7 s=4"),
+    "c3b": dict(t=20, n=1000, l=19, d=6, k=7, s=4, m=711, label="C3b planted (19,6) t=20 n=1000 k=7 s=4"),
     "c4": dict(t=20, n=1000, l=20, d=7, k=7, s=4, m=3421, label="C4 planted (20,7) t=20 n=1000 k=7 s=4"),
     # large-scale sweep; k, s are what the reference derives for this size (k=l-d-1, s=ceil(2x/4^k)); m explicit
     "c5": dict(t=10000, n=1000, l=15, d=4, k=10, s=19, m=2, label="C5 planted (15,4) t=10000 n=1000 k=10 s=19",
@@ -54,6 +55,8 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--trials", type=int, default=0, help="trials per step per GPU (default: the config's formula m)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N*m trials per step, m per GPU; strong: the config's m trials sharded over the N GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip time-to-motif and the other-config sweep")
     return ap.parse_args()
@@ -114,8 +117,28 @@ def measured_peaks():
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        return p.get("hbm_gbs", 6650.0), p.get("sm_max_mhz", 1965.0), "measured"
-    return 6650.0, 1965.0, "fallback"
+        return p.get("hbm_gbs", 6650.0), p.get("sm_max_mhz", 1965.0), "measured", p.get("bf16_tflops", 1590.0)
+    return 6650.0, 1965.0, "fallback", 1590.0
+
+
+def workload_config(cfg, trials_per_step, world, scaling):
+    """The `config` object of the JSON line: identical for both arms (what was run, not how)."""
+    return {"workload": cfg["label"], "trials_per_step": trials_per_step, "instance_seed": INSTANCE_SEED,
+            "run_seed": RUN_SEED, "early_stop": False, "n_gpus": world, "scaling_mode": scaling}
+
+
+def recorded_traffic(kernel, config_name):
+    """DRAM bytes per launch of `kernel` from the ncu --set full capture summarised in profiles/traffic.json
+    (written by tools/ncu_traffic.py together with the commit it was taken at); None when there is no capture."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        rec = json.load(f)
+    for r in rec.get("captures", []):
+        if r.get("kernel") == kernel and r.get("config") == config_name:
+            return r.get("dram_bytes_per_launch"), f"profiles/traffic.json: {r.get('report')} at commit {r.get('commit')}"
+    return None, None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -175,17 +198,23 @@ def run_reference_arm(args, cfg, rank, world):
             vals.append(v)
         value = sum(vals) / len(vals)
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(vals),
-                "warmup": 0, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "warmup": 0, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg["label"], "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED,
-                           "note": "EXTRAPOLATED: hashing in full + refine() on sampled buckets, see cpu_baseline.sample"},
+                "config": dict(workload_config(cfg, (args.trials or cfg["m"]) * (world if args.scaling == "weak" else 1), world, args.scaling),
+                               note="EXTRAPOLATED: hashing in full + refine() on sampled buckets, see cpu_baseline.sample"),
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                                  "sample": f"extrapolated from {info}"},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}
         print(json.dumps(line), flush=True)
         return
-    sample = max(workers, 2) * (1 if cfg["n"] > 600 else 2)  # trials per step: ~1-3 s of host time
-    for _ in range(args.warmup):
+    # One step = the step of our arm: the config's own m trials (x N for the weak-scaling runs).  That is ~2.5 s of the
+    # host's 16 cores on C1; the n = 1000 configurations need minutes per step, so they run a bounded sample of the
+    # same trials instead (trial cost is i.i.d.) and say so.
+    want = (args.trials or cfg["m"]) * (world if args.scaling == "weak" else 1)
+    calib, dt = cpu_trials_per_second(oracle, kind, ss, cfg, max(workers, 2), workers)
+    budget_s = max(2.0, 150.0 / max(1, args.steps + args.warmup))  # the whole arm ends within a few minutes
+    sample = want if want / calib <= budget_s else max(workers, int(calib * budget_s) // workers * workers)
+    for _ in range(args.warmup if sample < want else min(args.warmup, 1)):
         cpu_trials_per_second(oracle, kind, ss, cfg, sample, workers)
     times = []
     for _ in range(args.steps):
@@ -193,15 +222,17 @@ def run_reference_arm(args, cfg, rank, world):
         times.append(dt)
     total = sum(times)
     value = sample * args.steps / total
+    config = workload_config(cfg, want, world, args.scaling)
+    if sample != want:
+        config["reference_sample_trials_per_step"] = sample
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["label"], "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED,
-                   "trials_per_step": sample, "note": "bounded sample of the same workload; trial cost is i.i.d."},
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps * (want / sample), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
                          "sample": f"{sample} trials/step x {args.steps} steps of projmotif::run "
-                                   f"(-O3, workers={workers}) on {cores} host cores"},
+                                   f"(-O3, workers={workers}) on {cores} host cores"
+                                   + ("" if sample == want else f"; bounded sample of the step's {want} trials")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -228,7 +259,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     m_per_gpu = args.trials or cfg["m"]
-    m_total = m_per_gpu * world
+    m_total = m_per_gpu * world if args.scaling == "weak" else m_per_gpu
     begin, end = shard_range(m_total, rank, world)
     stream = torch.cuda.current_stream()
     ctx = pm.Context(local_rank, stream.cuda_stream)
@@ -278,6 +309,7 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
 
     def timed_loop(steps, e2e):
         per_step_ms, launches, stage, lookups, h2d, d2h, work = [], 0, [0.0] * 8, 0, 0, 0, 0
+        tensor_flops = exact_buckets = fp64_buckets = 0
         result = None
         for _ in range(steps):
             flush.fill_(1)  # evict L2 between timed iterations (untimed)
@@ -294,21 +326,29 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
             launches += mine.gpu_launches
             lookups += mine.em_lookup_adds
             work += mine.em_work
+            tensor_flops += mine.em_tensor_flops
+            exact_buckets += mine.em_exact_buckets
+            fp64_buckets += mine.em_fp64_buckets
             h2d += mine.h2d_bytes
             d2h += mine.d2h_bytes
             for i in range(8):
                 stage[i] += mine.stage_ms[i]
-        return per_step_ms, launches, stage, lookups, h2d, d2h, result, work
+        return per_step_ms, launches, stage, lookups, h2d, d2h, result, work, (tensor_flops, exact_buckets, fp64_buckets)
 
     ctx.set_sequences(ss.bases, ss.offs)
     timed_loop(args.warmup, False)                      # warm-up (untimed)
     sampler = ClockSampler(local_rank)
     if rank == 0:
         sampler.start()
-    ms_dev, launches, stage, lookups, _, _, result, work = timed_loop(args.steps, False)
+    ms_dev, launches, stage, lookups, _, _, result, work, (tensor_flops, exact_buckets, fp64_buckets) = timed_loop(args.steps, False)
     timed_loop(max(1, min(args.warmup, 2)), True)
-    ms_e2e, _, stage_e2e, _, h2d, d2h, result_e2e, _ = timed_loop(args.steps, True)
+    ms_e2e, _, stage_e2e, _, h2d, d2h, result_e2e, _, _ = timed_loop(args.steps, True)
     clocks = sampler.stop() if rank == 0 else None  # sampled across both timed loops (HBM-resident and end-to-end)
+
+    # time to the planted motif on N GPUs: round-robin trial shards (every rank takes part)
+    ttm_multi = None
+    if not args.no_extras and cfg["t"] <= 100 and world > 1:
+        ttm_multi = time_to_motif_sharded(pm, ctx, cfg, dist, rank, world, torch.device("cuda", local_rank), all_gather_merge)
 
     if rank != 0:
         if dist is not None:
@@ -318,26 +358,56 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
     mean_ms = sum(ms_dev) / len(ms_dev)
     value = m_total / (mean_ms * 1e-3)
     mean_e2e = sum(ms_e2e) / len(ms_e2e)
-    hbm_peak, sm_max_mhz, peak_kind = measured_peaks()
-    # EM kernel roofline: FP32-pipe bound.  achieved = E-step lookup-adds executed per
-    # launch / mean launch duration (CUDA events on the launching stream, inside the timed steps).
+    hbm_peak, sm_max_mhz, peak_kind, bf16_peak = measured_peaks()
+    # EM stage = the dominant kernel.  Its time per step comes from CUDA events on the launching stream
+    # inside the timed steps (stage 3 brackets the tensor-core launch, the compaction of the buckets it flagged and
+    # their re-run on the pair kernel).  Two readings of the same time:
+    #  * tensor: dense tcgen05.mma FLOPs the kernel issued (2 M N K per instruction, counted by the library from its
+    #    block table) against the measured bf16 GEMM peak -- how busy the tensor pipe is;
+    #  * algorithmic: SURVEY 8(d) W_EM lookup-adds (what the reference computes) against the FP32-add peak -- the
+    #    figure round 1 reported for the shared-memory kernel, kept for continuity.
     em_launches = args.steps * max(1, -(-(end - begin + 1) // 32768))
     em_ms = stage[3] / max(1, args.steps)
     fp32_peak_tflops = 148 * 128 * sm_max_mhz * 1e6 / 1e12
-    achieved_tflops = (work / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 else None
-    estep_tflops = (lookups / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 else None
+    algo_tflops = (work / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 else None
+    tensor_tflops = (tensor_flops / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 and tensor_flops else None
     x = ss.total_lmers(l)
     hb_bytes = (-(-t * cfg["n"] // 4) + 8 * x) * (end - begin + 1)
     hb_ms = (stage[0] + stage[1] + stage[2]) / max(1, args.steps)
+    on_tensor = tensor_tflops is not None
+    kernel = "em_refine_tc_kernel" if on_tensor else "em_refine_pair_kernel"
+    traffic, traffic_src = recorded_traffic(kernel, args.config if not args.trials else None)
+    roofline = {
+        "bound": "tensor" if on_tensor else "fp32", "kernel": kernel,
+        "achieved": tensor_tflops if on_tensor else algo_tflops,
+        "peak": bf16_peak if on_tensor else fp32_peak_tflops, "unit": "TFLOP/s",
+        "frac": (tensor_tflops / bf16_peak) if on_tensor else ((algo_tflops / fp32_peak_tflops) if algo_tflops else None),
+        "traffic": traffic, "traffic_source": traffic_src,
+        "launch_ms": em_ms / max(1, em_launches // args.steps),
+        "peak_source": (f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst figure: the step lasts about a millisecond)" if on_tensor
+                        else f"148 SM x 128 FP32 lanes x {sm_max_mhz:.0f} MHz ({peak_kind} clocks), adds not FMAs"),
+        "work": ("dense MMA FLOPs issued: per 128-bucket tile and pass 2*128*columns*K, three bf16 log-odds terms in the E-step "
+                 "GEMM (one in the MAX passes), two bf16 responsibility terms in the M-step GEMM" if on_tensor
+                 else "SURVEY 8(d) W_EM = sum_b (2 I_b+1) x l + 4 (I_b+1) x FP32 ops (E- and M-step), measured I_b"),
+        "algorithmic": {"w_em_tflops": algo_tflops, "fp32_add_peak": fp32_peak_tflops,
+                        "frac_of_fp32_add_peak": (algo_tflops / fp32_peak_tflops) if algo_tflops else None,
+                        "estep_only_tflops": (lookups / args.steps) / (em_ms * 1e-3) / 1e12 if em_ms > 0 else None,
+                        "note": "SURVEY 8(d) W_EM lookup-adds per second against 148 SM x 128 lanes x clock; the one-hot GEMM "
+                                "performs these adds on the tensor pipe, so this fraction is not bounded by 1 in principle"},
+        "buckets_refined_again": {"pair_kernel": exact_buckets // args.steps, "fp64_kernel": fp64_buckets // args.steps,
+                                  "of": result.buckets_enriched},
+    }
+    config = workload_config(cfg, m_total, world, args.scaling)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"], "trials_per_step_per_gpu": m_per_gpu, "trials_per_step": m_total,
-                   "instance_seed": INSTANCE_SEED, "run_seed": RUN_SEED, "early_stop": False,
-                   "parallelism": f"trials sharded over {world} GPU(s), one all_gather of the best record",
-                   "l2": "256 MiB flush between timed steps (untimed)",
-                   "timing": "CUDA events on the launching stream per step, max over ranks"},
+        "ms_per_step": mean_ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": config,
+        "notes": {"trials_per_step_per_gpu": m_per_gpu if args.scaling == "weak" else None,
+                  "dtype": "EM sums: bf16 x 3 split operands on tcgen05 with FP32 accumulation (FP32-equivalent); model update FP32; "
+                           "decisions within the FP32 error re-run on FP64-assisted kernels; everything else integer",
+                  "parallelism": f"trials sharded over {world} GPU(s), one all_gather of the best record",
+                  "l2": "256 MiB flush between timed steps (untimed)",
+                  "timing": "CUDA events on the launching stream per step, max over ranks"},
         "result": {"consensus": result.consensus.decode(), "score": result.score, "best_trial": result.best_trial,
                    "planted_motif": motif, "recovered": result.consensus.decode() == motif,
                    "buckets_enriched": result.buckets_enriched, "within_d": result.within_d},
@@ -347,20 +417,8 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "stage_ms_per_step": {name: stage[i] / args.steps for i, name in
                               enumerate(["keys", "sort", "enrich", "em", "reduce", "score", "upload", "d2h"])},
-        "roofline": {"bound": "fp32", "kernel": "em_refine_pair_kernel",
-                     "achieved": achieved_tflops, "peak": fp32_peak_tflops,
-                     "unit": "TFLOP/s", "frac": (achieved_tflops / fp32_peak_tflops) if achieved_tflops else None,
-                     # dram__bytes_read+write of one launch from the ncu --set full capture in profiles/ (C1 only):
-                     # the kernel's working set is shared memory + L1/L2-resident tables
-                     "traffic": 857088 if args.config == "c1" and not args.trials else None,
-                     "traffic_source": "profiles/r1_em_refine_pair_ncu_full.txt (ncu, dram bytes per launch)",
-                     "launch_ms": em_ms / max(1, em_launches // args.steps),
-                     "work": "SURVEY 8(d) W_EM = sum_b (2 I_b+1) x l + 4 (I_b+1) x FP32 ops (E- and M-step), measured I_b",
-                     "estep_only_achieved": estep_tflops,
-                     "smem_lookup_ceiling": 148 * 32 * sm_max_mhz * 1e6 * 2 / 1e12,
-                     "frac_of_smem_ceiling": (achieved_tflops / (148 * 32 * sm_max_mhz * 1e6 * 2 / 1e12)) if achieved_tflops else None,
-                     "peak_source": f"148 SM x 128 FP32 lanes x {sm_max_mhz:.0f} MHz ({peak_kind} clocks), adds not FMAs"},
-        "roofline_hash_bucket": {"bound": "hbm", "kernels": "project_keys+radix_sort+enrich",
+        "roofline": roofline,
+        "roofline_hash_bucket": {"bound": "hbm", "kernels": "hash_bucket_fused (t=20 configs) | project_keys+radix_sort+enrich",
                                  "achieved": (hb_bytes / (hb_ms * 1e-3) / 1e9) if hb_ms > 0 else None, "peak": hbm_peak,
                                  "unit": "GB/s", "frac": (hb_bytes / (hb_ms * 1e-3) / 1e9 / hbm_peak) if hb_ms > 0 else None,
                                  "note": f"algorithmic bytes ceil(t*n/4)+8x per trial; peak {peak_kind}; at t=20 the "
@@ -368,8 +426,10 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "clocks": clocks,
     }
 
-    if not args.no_extras and cfg["t"] <= 100:
+    if not args.no_extras and cfg["t"] <= 100 and world == 1:
         line["time_to_motif"] = time_to_motif(pm, ctx, cfg)
+    if ttm_multi is not None:
+        line["time_to_motif"] = ttm_multi
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)
         if "time_to_motif" in line:
@@ -383,13 +443,17 @@ def time_to_motif(pm, ctx, cfg):
     """Wall time from run() entry until the trial T* after which the running best consensus equals
     the planted motif, over several instance seeds, batches of 16 trials."""
     rows = []
+    # batch = trials per call.  A 128-bucket tile of the tensor-core EM kernel takes about a millisecond however few
+    # tiles there are, so one call over all of C1's 172 trials (138 tiles, one wave of the 148 SMs) costs the same as
+    # a call over 32: the whole budget in one batch is the fastest way to the motif.  n = 1000: 64 trials (~285 tiles).
+    batch = cfg["m"] if cfg["n"] <= 600 else 64
     for inst_seed in (42, 1, 2, 3, 4):
         bases, offs, motif, _ = pm.generate_planted(cfg["t"], cfg["n"], cfg["l"], cfg["d"], inst_seed)
         ctx.set_sequences(bases, offs)
         t0 = time.perf_counter()
         found_at, first = None, 1
         while first <= cfg["m"] and found_at is None:
-            last = min(cfg["m"], first + 15)
+            last = min(cfg["m"], first + batch - 1)
             try:
                 r = ctx.run(per_trial=False, l=cfg["l"], d=cfg["d"], k=cfg["k"], s=cfg["s"], m=cfg["m"], seed=RUN_SEED,
                             early_stop=0, trial_begin=first, trial_end=last)
@@ -402,7 +466,51 @@ def time_to_motif(pm, ctx, cfg):
                      "ms": 1e3 * (time.perf_counter() - t0)})
     hit = [r for r in rows if r["found"]]
     return {"runs": rows, "ms_median": statistics.median(r["ms"] for r in hit) if hit else None,
-            "note": "wall ms incl. host, batches of 16 trials, stop at the first batch whose best == planted motif"}
+            "batch_trials": batch,
+            "note": f"wall ms incl. host, batches of {batch} trials, stop at the first batch whose best == planted motif"}
+
+
+def time_to_motif_sharded(pm, ctx, cfg, dist, rank, world, device, all_gather_merge):
+    """time_to_motif on N GPUs.  The planted motif usually appears within the first few trials, so contiguous shards
+    would leave every GPU but the first idle: trials are dealt round-robin (trial_stride = N), 16 per rank and round,
+    and the ranks exchange their best record after every round (one all_gather of ~300 bytes)."""
+    import numpy as np
+    import torch
+    rows = []
+    per_round = 16
+    t, l, m = cfg["t"], cfg["l"], cfg["m"]
+    for inst_seed in (42, 1, 2, 3, 4):
+        bases, offs, motif, _ = pm.generate_planted(t, cfg["n"], l, cfg["d"], inst_seed)
+        ctx.set_sequences(bases, offs)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        found_at, base = None, 0
+        while base < m and found_at is None:
+            begin, end = base + rank + 1, min(m, base + per_round * world)
+            out = pm.RunResult()
+            pos = np.zeros(t, dtype=np.int32)
+            if begin <= end:
+                cfg_c = pm.default_config(l=l, d=cfg["d"], k=cfg["k"], s=cfg["s"], m=m, seed=RUN_SEED, early_stop=0,
+                                          trial_begin=begin, trial_end=end, trial_stride=world)
+                rc = pm.lib().pm_run(ctx._h, C.byref(cfg_c), C.byref(out), pos.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     None, None, None, None)
+                if rc not in (0, 7):
+                    raise pm.PmError(rc, pm.lib().pm_last_error().decode())
+            try:
+                merged, _ = all_gather_merge(out, pos, t, l, False, device=device)
+                if merged.consensus.decode() == motif:
+                    found_at = int(merged.best_trial)
+            except pm.PmError:
+                pass  # no rank enriched a bucket in this round
+            base += per_round * world
+        torch.cuda.synchronize()
+        rows.append({"instance_seed": inst_seed, "found": found_at is not None, "t_star": found_at,
+                     "ms": 1e3 * (time.perf_counter() - t0)})
+    hit = [r for r in rows if r["found"]]
+    return {"runs": rows, "ms_median": statistics.median(r["ms"] for r in hit) if hit else None, "n_gpus": world,
+            "note": f"wall ms incl. host on rank 0; round-robin shards over {world} GPUs, rounds of {per_round} trials per GPU, "
+                    "one all_gather per round; stop at the first round whose merged best == planted motif"}
 
 
 def cpu_time_to_motif(cfg, ttm, baseline):

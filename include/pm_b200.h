@@ -108,6 +108,9 @@ typedef struct pm_run_result {
     int64_t h2d_bytes;        /* bytes this call copied host->device ... */
     int64_t d2h_bytes;        /* ... and device->host */
     int64_t em_work;          /* SURVEY §8(d) W_EM: sum_b (2 I_b+1) x l + 4 (I_b+1) x  (E- and M-step work) */
+    int64_t em_tensor_flops;  /* dense tcgen05.mma FLOPs the tensor-core EM kernel issued (2 M N K per instruction) */
+    int64_t em_exact_buckets; /* buckets refined again by the pair kernel (flagged by the tensor-core kernel) ... */
+    int64_t em_fp64_buckets;  /* ... and by the FP64 kernel (stop decisions near tol, candidates of near-equal expectation) */
 } pm_run_result;
 
 /* --------------------------------------------------------------------------------------------

@@ -93,6 +93,7 @@ class RunResult(C.Structure):
         ("within_d", C.c_int32), ("total_distance", C.c_int32),
         ("stage_ms", C.c_double * 8), ("gpu_launches", C.c_int64), ("em_lookup_adds", C.c_int64),
         ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("em_work", C.c_int64),
+        ("em_tensor_flops", C.c_int64), ("em_exact_buckets", C.c_int64), ("em_fp64_buckets", C.c_int64),
     ]
 
     def as_dict(self):

@@ -102,6 +102,8 @@ struct pm_ctx {
     int max_tile_seqs = 0;  // most sequences any tile of the class-group index holds
     // tensor-core EM kernel (pm_em_tc.cuh): block list of one sweep for the current (set, l)
     int tc_l = -1, tc_n_blocks = 0, tc_e_positions = 0;
+    int64_t tc_g1_flops = 0, tc_g2_flops = 0;  // per tile and pass: GEMM1 with ONE log-odds term, GEMM2 with both P terms
+    bool tc_used = false;                      // the last launch_em went through the tensor-core kernel
     std::vector<k::TcBlock> h_tc_blocks;
     k::TcBlock* d_tc_blocks = nullptr;
     int64_t em_exact[6] = {0, 0, 0, 0, 0, 0};  // last refine/run: buckets the tensor-core kernel handed to the pair kernel
@@ -840,11 +842,18 @@ int launch_em_f64(pm_ctx* c, int l, int max_iters, double tol, const k::WorkDesc
 
 // ---- tensor-core EM kernel (pm_em_tc.cuh) ------------------------------------------------------------------
 // PM_B200_EM_TC (test/tuning knob): 0 keeps every bucket on the pair kernel, 2 uses the tensor-core kernel even for
-// a handful of buckets (default: from 32 buckets on; below that a 128-row tile is mostly empty)
-bool em_tc_enabled(unsigned int n_work_bound) {
+// a handful of buckets.  Default: the tensor-core kernel from kTcMinWork buckets on -- a 128-bucket tile takes about a
+// millisecond of sequential passes however few tiles there are, while the pair kernel refines ~4,000 buckets per
+// millisecond, so smaller batches are faster there.  The count is only known on the device: the kernel itself hands
+// a small batch over (TcExtra.min_work).
+constexpr unsigned int kTcMinWork = 4096;
+int em_tc_mode() {
     const char* env = std::getenv("PM_B200_EM_TC");
-    const int v = env ? std::atoi(env) : 1;
-    return v >= 2 || (v == 1 && n_work_bound >= 32);
+    return env ? std::atoi(env) : 1;
+}
+bool em_tc_enabled(unsigned int n_work_bound) {
+    const int v = em_tc_mode();
+    return v >= 2 || (v == 1 && n_work_bound >= kTcMinWork);
 }
 
 int tc_kc_for(int l) { return std::max(8, 4 * ((l + 3) / 4)); }
@@ -919,6 +928,14 @@ int build_tc_blocks(pm_ctx* c, int l) {
         }
     }
     c->tc_n_blocks = static_cast<int>(c->h_tc_blocks.size());
+    c->tc_g1_flops = 0;
+    c->tc_g2_flops = 0;
+    for (const k::TcBlock& B : c->h_tc_blocks) {
+        for (const k::TcSeg& sg : B.seg) {
+            c->tc_g1_flops += 2LL * k::kTcRows * sg.n * (4 * KC);
+            c->tc_g2_flops += 2LL * 2 * k::kTcRows * ((sg.valid + 15) / 16 * 16) * (4 * KC);
+        }
+    }
     c->tc_e_positions = ru(c->max_seq_len + k::kTcEPad, 32);
     PM_TRY(get_buf(c, S_TC_BLOCKS, c->h_tc_blocks.size(), &c->d_tc_blocks));
     PM_TRY(h2d(c, c->d_tc_blocks, c->h_tc_blocks.data(), sizeof(k::TcBlock) * c->h_tc_blocks.size()));
@@ -977,6 +994,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     p.out_map = nullptr;
     p.theta_in = theta_in;
     p.flag_exact = nullptr;
+    c->tc_used = false;
     const k::WorkDesc* const work_all = work;  // the TC stage below narrows p.work to the buckets it flagged
 
     const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs;
@@ -997,6 +1015,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
             x.tie_delta = 1e-3f;
             x.ll_margin = 1e-2f;
             x.stats = d_scal + 4;
+            x.min_work = em_tc_mode() >= 2 ? 0u : kTcMinWork;
             unsigned int* d_cnt = reinterpret_cast<unsigned int*>(d_scal + 3);  // zeroed by the caller with the other scalars
             k::WorkDesc* d_list;
             unsigned int* d_map;
@@ -1007,6 +1026,7 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
             const unsigned int grid = std::max(1u, std::min(static_cast<unsigned int>(c->sm_count), tiles));
             kern<<<grid, k::kTcThreads, smem, c->stream>>>(p, x);
             PM_TRY(check_launch(c, "em_refine_tc"));
+            c->tc_used = true;
             const unsigned int cgrid = std::max(1u, std::min(1024u, (n_work_bound + 255) / 256));
             tc_compact_kernel<<<cgrid, 256, 0, c->stream>>>(x.out_flag, work, n_work_dev, n_work_host, d_list, d_map, d_cnt);
             PM_TRY(check_launch(c, "tc_compact"));
@@ -1533,6 +1553,7 @@ int refine_common(pm_ctx* c, int l, const int32_t* members, const int64_t* mem_o
     if (ll_trace) PM_TRY(d2h(c, ll_trace, o.ll, sizeof(double) * nb * static_cast<size_t>(max_iters)));
     PM_CUDA(cudaStreamSynchronize(c->stream));
     if (!exact) {
+        if ((scal[4] | scal[5] | scal[6] | scal[7]) == 0) scal[3] = 0;  // a small batch handed over wholesale
         c->em_exact[0] = static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
         for (int r = 0; r < 4; ++r) c->em_exact[1 + r] = static_cast<int64_t>(scal[4 + r]);
         c->em_exact[5] = static_cast<int64_t>(scal[2] & 0xFFFFFFFFULL);
@@ -1969,9 +1990,16 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     if ((scal[1] & 0xFFFFFFFFULL) != 0) {
         return set_error(PM_ERR_NUMERICAL_UNDERFLOW, "all window weights vanished in some sequence");
     }
+    const bool tc_bypassed = (scal[4] | scal[5] | scal[6] | scal[7]) == 0 && (scal[3] & 0xFFFFFFFFULL) != 0;
+    if (tc_bypassed) {  // a small batch handed over wholesale: not "refined again", and no tensor work
+        scal[3] = 0;
+        c->tc_used = false;
+    }
     c->em_exact[0] += static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
     for (int r = 0; r < 4; ++r) c->em_exact[1 + r] += static_cast<int64_t>(scal[4 + r]);
     c->em_exact[5] += static_cast<int64_t>(scal[2] & 0xFFFFFFFFULL);
+    out->em_exact_buckets += static_cast<int64_t>(scal[3] & 0xFFFFFFFFULL);
+    out->em_fp64_buckets += static_cast<int64_t>(scal[2] & 0xFFFFFFFFULL);
     out->em_lookup_adds += static_cast<int64_t>(scal[0]) * c->x * l;
     {
         // W_EM = sum_b (2 I_b + 1) x l lookup-adds + 4 (I_b + 1) x; scal[0] = sum_b (I_b + 1)
@@ -1979,6 +2007,12 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         for (unsigned int nr : n_rec) n_buckets += nr;
         const int64_t s_iters1 = static_cast<int64_t>(scal[0]);
         out->em_work += (2 * s_iters1 - n_buckets) * c->x * l + 4 * s_iters1 * c->x;
+        if (c->tc_used) {
+            // passes of a tile (pm_em_tc.cuh): I EM passes and the final E-step with three log-odds terms, min(I, 2) MAX
+            // passes with one; GEMM2 in the I EM passes
+            const int64_t I = cfg->max_em_iters, tiles = (n_buckets + k::kTcRows - 1) / k::kTcRows;
+            out->em_tensor_flops += tiles * (c->tc_g1_flops * (3 * (I + 1) + std::min<int64_t>(I, 2)) + c->tc_g2_flops * I);
+        }
     }
 
     // Trials whose best bucket the FP32 expectation cannot separate from another bucket of the same score: every such
@@ -2234,6 +2268,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     out->gpu_launches = c->launches - launches0;
     out->h2d_bytes = c->h2d_bytes - h2d0;
     out->d2h_bytes = c->d2h_bytes - d2h0;
+    out->em_fp64_buckets += st.exact_refines;
     out->found = st.have_best ? 1 : 0;
     if (!st.have_best) {
         out->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -2379,6 +2414,9 @@ int pm_run_multi(const int* devices, int n_devices, int strided, const pm_run_co
         out->gpu_launches += p.res.gpu_launches;
         out->em_lookup_adds += p.res.em_lookup_adds;
         out->em_work += p.res.em_work;
+        out->em_tensor_flops += p.res.em_tensor_flops;
+        out->em_exact_buckets += p.res.em_exact_buckets;
+        out->em_fp64_buckets += p.res.em_fp64_buckets;
         out->h2d_bytes += p.res.h2d_bytes;
         out->d2h_bytes += p.res.d2h_bytes;
         for (int j = 0; j < 8; ++j) out->stage_ms[j] = std::max(out->stage_ms[j], p.res.stage_ms[j]);

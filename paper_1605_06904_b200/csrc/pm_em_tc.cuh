@@ -42,7 +42,7 @@ constexpr int kTcMaxIters = 8;      // no early exit for a tile: larger budgets 
 constexpr int kTcMaxL = 20;         // K = 4 * KC <= 80
 constexpr int kTcEPad = 96;         // zero one-hot codes behind every sequence (pad windows read them)
 
-enum : unsigned { kTcFlagConv = 1u, kTcFlagRange = 2u, kTcFlagTie = 4u, kTcFlagBad = 8u };
+enum : unsigned { kTcFlagConv = 1u, kTcFlagRange = 2u, kTcFlagTie = 4u, kTcFlagBad = 8u, kTcFlagSmall = 16u };
 
 // One S/P block of a sweep: up to NBLK columns (a multiple of 32) of ONE sequence.  A column is a window; a
 // block consists of one or two MMA segments, each a run of windows of one parity.
@@ -70,6 +70,8 @@ struct TcExtra {
     float tie_delta;        // argmax runner-up margin (natural-log units)
     float ll_margin;        // likelihood gains below tol + margin are not decided here
     unsigned long long* stats;  // [4] flagged counts by kind (conv, range, tie, bad)
+    unsigned int min_work;      // fewer work items than this: hand every bucket to the pair kernel (a tile's ~1 ms of
+                                // sequential passes is a latency floor that a few hundred buckets do not amortise)
 };
 
 // ---------------------------------------------------------------------------------------------------------
@@ -343,6 +345,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
     extern __shared__ __align__(128) unsigned char smem[];
     const int t = p.t, l = p.l;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        const unsigned int n_all = p.n_work_dev ? *p.n_work_dev : p.n_work;
+        if (n_all < x.min_work) {  // small batch: nothing is decided here
+            for (unsigned int i = blockIdx.x * blockDim.x + tid; i < n_all; i += gridDim.x * blockDim.x) x.out_flag[i] = kTcFlagSmall;
+            return;
+        }
+    }
     const int EB = x.e_positions * 8;  // bytes per one-hot array
     unsigned char* Ebuf = smem;        // [2 sequences][2 parities][EB]
     float* mprev = reinterpret_cast<float*>(Ebuf + 4 * static_cast<size_t>(EB));  // [t][128]

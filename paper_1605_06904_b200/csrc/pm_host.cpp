@@ -475,6 +475,9 @@ int pm_merge_results(const pm_run_result* parts, const int32_t* const* parts_pos
         acc.gpu_launches += p.gpu_launches;
         acc.em_lookup_adds += p.em_lookup_adds;
         acc.em_work += p.em_work;
+        acc.em_tensor_flops += p.em_tensor_flops;
+        acc.em_exact_buckets += p.em_exact_buckets;
+        acc.em_fp64_buckets += p.em_fp64_buckets;
         acc.h2d_bytes += p.h2d_bytes;
         acc.d2h_bytes += p.d2h_bytes;
         for (int j = 0; j < 8; ++j) acc.stage_ms[j] = std::max(acc.stage_ms[j], p.stage_ms[j]);

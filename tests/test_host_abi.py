@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol(pm):
 def test_struct_layouts_match_header(pm):
     # sizes computed from the header's field lists (natural alignment, LP64)
     assert C.sizeof(pm.RunConfig) == 16 + 8 + 8 + 8 + 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8  # + trial_stride, exact_best
-    assert C.sizeof(pm.RunResult) == 32 + 8 + 8 + 8 + 24 + 8 + 8 + 8 + 8 + 8 + 8 + 64 + 16 + 16 + 8
+    assert C.sizeof(pm.RunResult) == 32 + 8 + 8 + 8 + 24 + 8 + 8 + 8 + 8 + 8 + 8 + 64 + 16 + 16 + 8 + 24
 
 
 def test_no_gpu_means_loud_failure_not_fallback(pm):
