@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
     __shared__ double th[4 * 32];     // theta[r][c] at c * 4 + r, c = 0 background
     __shared__ double D[4 * 32];      // log max(theta[r][c+1],1e-9) - log max(theta[r][0],1e-9) at c * 4 + r
     __shared__ double lbg[4];
-    __shared__ double cnt[4 * 32 * 2];  // M-step partial sums: [cell][half]
+    __shared__ double cnt[4 * 32];                        // M-step counts, cell c * 4 + r
+    __shared__ double part[(kF64Threads / 32) * 32 * 4];  // per-warp partial counts
     __shared__ double red[kF64Threads];
     __shared__ int prof[4 * 32];
     __shared__ int s_pos;
@@ -165,24 +166,45 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
             }
             if (final_pass) break;
 
-            // ---- M-step (refine.hpp:227-237): cell (c, r) sums z over the windows that show r at column c; two
-            // threads per cell (even / odd sequences), fixed order
+            // ---- M-step (refine.hpp:227-237): counts[c][r] = sum of z over the windows that show r at column c.
+            // Warp w takes the sequences i = w, w + 8, ...; lane = motif column, four accumulators (one per symbol);
+            // the eight per-warp partials are added in warp order: fixed shape, deterministic.
             __syncthreads();
-            if (tid < 8 * l) {
-                const int cell = tid >> 1, half = tid & 1;
-                const int c = cell >> 2, r = cell & 3;
-                double acc = 0.0;
-                for (int i = half; i < t; i += 2) {
+            {
+                const int warp = tid >> 5, lane = tid & 31;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                for (int i = warp; i < t; i += kF64Threads / 32) {
                     const uint64_t* __restrict__ wp = p.words + p.word_off[i];
                     const int W = p.seq_len[i] - l + 1;
                     const double* zi = z + p.win_off[i];
+                    // lane's column of window j is base j + lane: one symbol stream per lane, read word by word
+                    const int q0 = lane;  // first base this lane looks at
+                    uint64_t word = wp[q0 >> 5];
+                    int in_word = q0 & 31;
                     for (int j = 0; j < W; ++j) {
-                        const int q = j + c;
-                        const unsigned sym = static_cast<unsigned>(wp[q >> 5] >> (62 - 2 * (q & 31))) & 3u;
-                        if (sym == static_cast<unsigned>(r)) acc += zi[j];
+                        const double zj = zi[j];
+                        const unsigned sym = static_cast<unsigned>(word >> (62 - 2 * in_word)) & 3u;
+                        if (++in_word == 32) {
+                            in_word = 0;
+                            word = wp[((q0 + j + 1) >> 5)];
+                        }
+                        a0 += sym == 0u ? zj : 0.0;
+                        a1 += sym == 1u ? zj : 0.0;
+                        a2 += sym == 2u ? zj : 0.0;
+                        a3 += sym == 3u ? zj : 0.0;
                     }
                 }
-                cnt[cell * 2 + half] = acc;
+                if (lane < l) {
+                    double* out = part + (warp * 32 + lane) * 4;
+                    out[0] = a0, out[1] = a1, out[2] = a2, out[3] = a3;
+                }
+            }
+            __syncthreads();
+            if (tid < 4 * l) {
+                const int c = tid >> 2, r = tid & 3;
+                double sum = 0.0;
+                for (int w = 0; w < kF64Threads / 32; ++w) sum += part[(w * 32 + c) * 4 + r];
+                cnt[tid] = sum;
             }
             __syncthreads();
             ++iterations;
@@ -192,11 +214,11 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
                 if (tid == 0) {
                     for (int r = 0; r < 4; ++r) {
                         double b = p.tot_sym[r];
-                        for (int c = 0; c < l; ++c) b -= cnt[(c * 4 + r) * 2] + cnt[(c * 4 + r) * 2 + 1];
+                        for (int c = 0; c < l; ++c) b -= cnt[c * 4 + r];
                         raw[r] = fmax(b, 0.0);
                     }
                 } else {
-                    for (int r = 0; r < 4; ++r) raw[r] = cnt[((tid - 1) * 4 + r) * 2] + cnt[((tid - 1) * 4 + r) * 2 + 1];
+                    for (int r = 0; r < 4; ++r) raw[r] = cnt[(tid - 1) * 4 + r];
                 }
                 double sum = 0.0;
                 for (int r = 0; r < 4; ++r) sum += raw[r];

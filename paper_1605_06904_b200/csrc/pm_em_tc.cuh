@@ -777,21 +777,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         st.second = -INFINITY;
                         st.best_j = 0;
                     }
-#ifdef PM_TC_TIMING
-                    const bool trace = blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 4) && tile == 0 && (ps == 5 || ps == 0) && n >= 10 && n < 13;
-                    long long tr[8];
-                    int trn = 0;
-                    if (trace) tr[trn++] = clock64();
-#endif
                     {
                         TC_T0();
                         tc_wait(&s_full[blk & 1], (blk >> 1) & 1);
                         TC_ACC(ts_s);
                     }
                     tc_fence_after();
-#ifdef PM_TC_TIMING
-                    if (trace) tr[trn++] = clock64();
-#endif
                     const uint32_t tB = tS + (blk & 1) * NBLK;
                     const int half = B.ncols >> 1;
                     const int c_begin = wg * half, c_end = c_begin + half;
@@ -808,9 +799,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             uint32_t r[32];
                             tc_ld32(tB + cc, r);
                             tc_wait_ld();
-#ifdef PM_TC_TIMING
-                            if (trace && trn < 7) tr[trn++] = clock64();
-#endif
                             if (em_pass) {
                                 uint32_t o[32];
                                 tc_em_chunk<false>(r, o, 16, ref2, st);
@@ -823,9 +811,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                                 tc_final_chunk<false>(r, 16, j, st);
                                 tc_final_chunk<false>(r + 16, 16, j + 32, st);
                             }
-#ifdef PM_TC_TIMING
-                            if (trace && trn < 7) tr[trn++] = clock64();
-#endif
                         }
 #pragma unroll 1
                         for (; cc < vend; cc += 16, j += 32) {  // at most one full chunk and the tail (dead chunks are skipped)
@@ -848,14 +833,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(&p_full[blk & 1]);
-#ifdef PM_TC_TIMING
-                    if (trace) {
-                        tr[trn++] = clock64();
-                        printf("[trace] warp %d pass %d block %d ncols %d:", warp, ps, n, (int)B.ncols);
-                        for (int q = 1; q < trn; ++q) printf(" +%lld", tr[q] - tr[q - 1]);
-                        printf("  (start %lld)\n", tr[0]);
-                    }
-#endif
 
                     if (pending) fold_pending();  // the previous sequence's counts: its GEMM2 finished long ago
 
