@@ -162,6 +162,13 @@ void pm_ctx_destroy(pm_ctx* ctx);
  * Copies the ASCII bases host->device and packs them there; errors: empty set/sequence
  * (InvalidParams), symbol outside ACGT (UnknownSymbol). */
 int pm_ctx_set_sequences(pm_ctx* ctx, const char* bases, const int64_t* offs, int t);
+/* generate_planted (planted.hpp:38-101) ON THE DEVICE, straight into this context: the reference's mt19937_64 stream
+ * (one CTA, 156-way parallel twists) and its contractual draw order, byte-identical to pm_generate_planted for the same
+ * seed; the ASCII bases never cross PCIe on the way in.  Optional outputs (NULL to skip): bases_out t*n chars, motif l
+ * chars, positions t 1-based starts.  A seed whose stream makes the reference redraw a bounded value (p < 1e-16 per
+ * draw) is refused with PM_ERR_UNSUPPORTED rather than generated differently. */
+int pm_ctx_generate_planted(pm_ctx* ctx, int t, int n, int l, int d, uint64_t seed, char* bases_out, char* motif,
+                            int32_t* positions);
 int pm_ctx_num_sequences(const pm_ctx* ctx);
 int64_t pm_ctx_total_lmers(const pm_ctx* ctx, int l);               /* sequence.hpp:113-120; <0 if some n_i < l */
 int pm_ctx_packed_words(pm_ctx* ctx, uint64_t* words_out, int64_t* word_off_out /* t+1 */, int64_t cap_words);

@@ -107,7 +107,7 @@ EXPORTS = [
     "pm_version", "pm_last_error", "pm_default_config", "pm_splitmix64", "pm_derive_seed", "pm_sample_plan",
     "pm_sample_plan_stream", "pm_trial_plan", "pm_validate_plan", "pm_generate_planted", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
-    "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_num_sequences",
+    "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_generate_planted", "pm_ctx_num_sequences",
     "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
     "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_refine_exact",
     "pm_init_model", "pm_em_step", "pm_em_step_exact", "pm_expectation", "pm_score",
@@ -331,6 +331,17 @@ class Context:
         _check(lib().pm_ctx_set_sequences(self._h, bases, _p(offs, C.c_int64), len(offs) - 1))
         self.t = len(offs) - 1
         self.offs = offs
+
+    def generate_planted(self, t, n, l, d, seed):
+        """pm_ctx_generate_planted: the planted instance is generated on the device and becomes this context's sequence
+        set.  Returns (bases, offs, motif, positions) like the host generator."""
+        bases = C.create_string_buffer(t * n)
+        motif = C.create_string_buffer(l + 1)
+        pos = np.zeros(t, dtype=np.int32)
+        _check(lib().pm_ctx_generate_planted(self._h, t, n, l, d, C.c_uint64(seed), bases, motif, _p(pos, C.c_int32)))
+        self.t = t
+        self.offs = np.arange(t + 1, dtype=np.int64) * n
+        return bases.raw[: t * n], self.offs, motif.raw[:l].decode(), pos.tolist()
 
     def total_lmers(self, l):
         return int(lib().pm_ctx_total_lmers(self._h, l))

@@ -30,6 +30,7 @@
 #include "pm_em_pair.cuh"
 #include "pm_em_tc.cuh"
 #include "pm_em_f64.cuh"
+#include "pm_planted.cuh"
 #include "pm_hash_fused.cuh"
 
 using namespace pm;
@@ -63,7 +64,7 @@ enum Slot {
     S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
     S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE,
     // the FP64 path has its own scratch: run() calls it while a batch's buffers are still live
-    S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
+    S_DRAWS, S_PLANT_OUT, S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
 };
 
 }  // namespace
@@ -1209,8 +1210,12 @@ void pm_ctx_destroy(pm_ctx* c) {
     delete c;
 }
 
-int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t) {
-    clear_error();
+}  // extern "C"
+
+namespace {
+// SequenceSet ctor + 2-bit encoding.  ascii_on_device: the bases already sit in the context's device ASCII buffer
+// (pm_ctx_generate_planted wrote them there); `bases` is then the host copy the class-group index is built from.
+int load_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t, bool ascii_on_device) {
     if (c == nullptr || bases == nullptr || offs == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
     if (t < 1) return set_error(PM_ERR_INVALID_PARAMS, "a sequence set needs at least one sequence");
     for (int i = 0; i < t; ++i) {
@@ -1257,7 +1262,7 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     PM_TRY(ensure(c, &c->d_tot_sym, &c->cap_tot_sym, sizeof(unsigned long long) * 8));
     PM_TRY(ensure(c, &c->d_win_off, &c->cap_win_off, sizeof(int64_t) * (static_cast<size_t>(t) + 1)));
     PM_TRY(ensure(c, &c->d_seq_logw, &c->cap_seq_logw, sizeof(double) * static_cast<size_t>(t)));
-    PM_TRY(h2d(c, d_ascii, bases + base0, static_cast<size_t>(total_bases)));
+    if (!ascii_on_device) PM_TRY(h2d(c, d_ascii, bases + base0, static_cast<size_t>(total_bases)));
     PM_TRY(h2d(c, d_offs, rel.data(), sizeof(int64_t) * rel.size()));
     PM_TRY(h2d(c, c->d_word_off, word_off.data(), sizeof(int64_t) * word_off.size()));
     PM_TRY(h2d(c, c->d_seq_len, len.data(), sizeof(int32_t) * len.size()));
@@ -1295,6 +1300,65 @@ int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int 
     c->total_words = total_words;
     c->max_seq_len = *std::max_element(len.begin(), len.end());
     return PM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int pm_ctx_set_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t) {
+    clear_error();
+    return load_sequences(c, bases, offs, t, false);
+}
+
+int pm_ctx_generate_planted(pm_ctx* c, int t, int n, int l, int d, uint64_t seed, char* bases_out, char* motif,
+                            int32_t* positions) {
+    clear_error();
+    if (c == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null context");
+    if (t < 1) return set_error(PM_ERR_INVALID_PARAMS, "need at least one sequence, got t=" + std::to_string(t));
+    if (l < 1 || l > n) {
+        return set_error(PM_ERR_INVALID_PARAMS, "need 1 <= l <= n, got l=" + std::to_string(l) + ", n=" + std::to_string(n));
+    }
+    if (d < 0 || d >= l) {
+        return set_error(PM_ERR_INVALID_PARAMS, "need 0 <= d < l, got d=" + std::to_string(d) + ", l=" + std::to_string(l));
+    }
+    if (l > PM_MAX_L) return set_error(PM_ERR_UNSUPPORTED, "l exceeds this build's limit of 31");
+    PM_CUDA(cudaSetDevice(c->device));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t per_seq = static_cast<int64_t>(n) + (n - l + 1 > 1 ? 1 : 0) + 2 * d;
+    const int64_t n_draws = l + static_cast<int64_t>(t) * per_seq;
+    const int64_t total_bases = static_cast<int64_t>(t) * n;
+    uint64_t* d_draws;
+    char* d_ascii;
+    unsigned char* d_out;  // [0..3] rejected flag, [8..40) motif, [64..) positions
+    PM_TRY(get_buf(c, S_DRAWS, static_cast<size_t>(n_draws), &d_draws));
+    PM_TRY(get_buf(c, S_ASCII, static_cast<size_t>(total_bases), &d_ascii));
+    PM_TRY(get_buf(c, S_PLANT_OUT, 64 + sizeof(int32_t) * static_cast<size_t>(t), &d_out));
+    PM_CUDA(cudaMemsetAsync(d_out, 0, 64, c->stream));
+    k::mt64_stream_kernel<<<1, k::kMtThreads, 0, c->stream>>>(seed, n_draws, d_draws);
+    PM_TRY(check_launch(c, "mt64_stream"));
+    k::planted_build_kernel<<<static_cast<unsigned>(std::min(t, 4 * c->sm_count)), 256, 0, c->stream>>>(
+        d_draws, t, n, l, d, d_ascii, reinterpret_cast<char*>(d_out + 8), reinterpret_cast<int32_t*>(d_out + 64),
+        reinterpret_cast<unsigned int*>(d_out));
+    PM_TRY(check_launch(c, "planted_build"));
+    // the host keeps a copy of the bases: the class-group index of the EM kernels is built there, and callers get the
+    // instance back like from pm_generate_planted
+    std::vector<unsigned char> head(64 + sizeof(int32_t) * static_cast<size_t>(t));
+    std::vector<char> host_bases(static_cast<size_t>(total_bases));
+    PM_TRY(d2h(c, head.data(), d_out, head.size()));
+    PM_TRY(d2h(c, host_bases.data(), d_ascii, host_bases.size()));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    unsigned int rejected = 0;
+    std::memcpy(&rejected, head.data(), sizeof(rejected));
+    if (rejected != 0) {
+        return set_error(PM_ERR_UNSUPPORTED, "seed " + std::to_string(seed) + " makes the reference redraw a bounded value "
+                         "(probability < 1e-16 per draw): generate this instance with pm_generate_planted");
+    }
+    if (motif) std::memcpy(motif, head.data() + 8, static_cast<size_t>(l));
+    if (positions) std::memcpy(positions, head.data() + 64, sizeof(int32_t) * static_cast<size_t>(t));
+    if (bases_out) std::memcpy(bases_out, host_bases.data(), host_bases.size());
+    std::vector<int64_t> offs(static_cast<size_t>(t) + 1);
+    for (int i = 0; i <= t; ++i) offs[static_cast<size_t>(i)] = static_cast<int64_t>(i) * n;
+    return load_sequences(c, host_bases.data(), offs.data(), t, true);
 }
 
 int pm_ctx_num_sequences(const pm_ctx* c) { return c ? c->t : 0; }

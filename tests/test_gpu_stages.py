@@ -232,6 +232,30 @@ def test_stage_exports_init_model_em_step_expectation(pm, ctx, golden, example, 
         assert e.value.kind == kind
 
 
+def test_planted_instances_generated_on_the_device(pm, ctx, golden):
+    """pm_ctx_generate_planted (planted.hpp:38-101 on the device): same bytes, motif and positions as the reference for
+    every pinned instance, the set is loaded in the context, and a config-5-sized instance equals the host generator."""
+    import hashlib
+    for p in golden["planted"]:
+        bases, offs, motif, pos = ctx.generate_planted(p["t"], p["n"], p["l"], p["d"], p["seed"])
+        assert (motif, pos, hashlib.sha256(bases).hexdigest()) == (p["motif"], p["positions"], p["sha256"]), p
+        assert ctx.total_lmers(p["l"]) == p["t"] * (p["n"] - p["l"] + 1)
+    # the loaded set is what the hashing stage sees
+    h = [x for x in golden["hash"] if x["instance"] == [20, 600, 15, 4, 42] and x["trial"] == 1 and x["k"] == 7][0]
+    ctx.generate_planted(20, 600, 15, 4, 42)
+    assert sha(ctx.hash_keys(15, h["kept"]).astype("<u8").tobytes()) == h["keys_sha256"]
+    assert ctx.symbol_counts() == [bytes(pm.generate_planted(20, 600, 15, 4, 42)[0]).count(c) for c in (b"A", b"C", b"T", b"G")]
+    want = pm.generate_planted(2000, 1000, 15, 4, 42)
+    got = ctx.generate_planted(2000, 1000, 15, 4, 42)
+    assert got[0] == want[0] and got[2:] == want[2:]
+    n_eq_l = ctx.generate_planted(3, 8, 8, 2, 9)  # n == l: no start draw at all
+    assert n_eq_l[0] == pm.generate_planted(3, 8, 8, 2, 9)[0] and n_eq_l[3] == [1, 1, 1]
+    for bad in ((0, 10, 3, 1), (2, 10, 11, 1), (2, 10, 3, 3)):
+        with pytest.raises(pm.PmError) as e:
+            ctx.generate_planted(*bad, 1)
+        assert e.value.kind == "InvalidParamsError"
+
+
 def test_run_multi_equals_single_context(pm, ctx, golden, instance):
     """pm_run_multi over a device list (contexts may share a GPU): contiguous and round-robin shards give the
     single-context result, per-trial bucket counts and early stop included."""
