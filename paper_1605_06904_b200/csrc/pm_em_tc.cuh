@@ -16,7 +16,7 @@
 // memory: D as three bf16 terms (hi + mid + lo = 24 significant bits, what FP32 holds), P as two bf16 terms
 // written IN PLACE over the S block it was computed from; accumulation is FP32 in tensor memory.
 //
-// Roles (320 threads): warps 0-7 = two warpgroups of "softmax" threads, thread = bucket row, the warpgroups
+// Roles (384 threads): warps 0-7 = two warpgroups of "softmax" threads, thread = bucket row, the warpgroups
 // split the columns of every block; warp 8 lane 0 issues every tcgen05.mma; warp 9 expands the next sequence
 // into the one-hot arrays.  mbarriers connect them (full/empty pairs), tcgen05.commit signals MMA completion.
 //
@@ -36,7 +36,7 @@ namespace k {
 
 constexpr int kTcRows = 128;        // buckets per CTA tile = MMA M
 constexpr int kTcSoftWarps = 8;     // two warpgroups
-constexpr int kTcThreads = 320;     // + MMA warp + producer warp
+constexpr int kTcThreads = 384;     // + a third warpgroup: MMA warp, producer warp, two idle warps (it gives its registers away)
 constexpr int kTcMaxSeqs = 64;      // previous maxima [t][128] live in shared memory
 constexpr int kTcMaxIters = 8;      // no early exit for a tile: larger budgets use the pair kernel
 constexpr int kTcMaxL = 20;         // K = 4 * KC <= 80
@@ -180,6 +180,13 @@ __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint
         float2 w0 = make_float2(__uint_as_float(r[k2]), __uint_as_float(r[k2 + 1]));
         float2 w1 = make_float2(__uint_as_float(r[k2 + 2]), __uint_as_float(r[k2 + 3]));
         if (kMasked) {
+            if (k2 >= nvalid) {  // a dead quad (the columns are the same for every row: a uniform branch)
+                o[k2 >> 1] = 0u;
+                o[(k2 >> 1) + 1] = 0u;
+                o[8 + (k2 >> 1)] = 0u;
+                o[8 + (k2 >> 1) + 1] = 0u;
+                continue;
+            }
             if (k2 >= nvalid) w0.x = -INFINITY;
             if (k2 + 1 >= nvalid) w0.y = -INFINITY;
             if (k2 + 2 >= nvalid) w1.x = -INFINITY;
@@ -221,36 +228,25 @@ __device__ __forceinline__ void tc_max_chunk(const uint32_t* __restrict__ r, int
     }
 }
 
-// final pass: maximum (mxa), its window, and the runner-up weight
+// final pass: maximum, its window and the runner-up weight, without branches (the rows of a warp are different
+// buckets: a data-dependent branch is taken by some lane in nearly every chunk).  The column number within the chunk
+// rides in the low four mantissa bits of the weight -- a perturbation below 16 ulp that the tie margin of the caller
+// accounts for -- so the running maximum carries its own position; st.best_j is the chunk's first window.
+constexpr float kTcFinalUlpMargin = 4e-6f;  // 2 x 15 ulp of a perturbed weight, relative
 template <bool kMasked>
 __device__ __forceinline__ void tc_final_chunk(const uint32_t* __restrict__ r, int nvalid, int j0, TcSeqState& st) {
-    // a chunk whose maximum is below the running runner-up changes nothing
-    float cma = -INFINITY, cmb = -INFINITY;
+    const float m_in = st.mxa;
 #pragma unroll
-    for (int k2 = 0; k2 < 16; k2 += 4) {
-        float w0 = __uint_as_float(r[k2]), w1 = __uint_as_float(r[k2 + 1]), w2 = __uint_as_float(r[k2 + 2]), w3 = __uint_as_float(r[k2 + 3]);
-        if (kMasked) {
-            if (k2 >= nvalid) w0 = -INFINITY;
-            if (k2 + 1 >= nvalid) w1 = -INFINITY;
-            if (k2 + 2 >= nvalid) w2 = -INFINITY;
-            if (k2 + 3 >= nvalid) w3 = -INFINITY;
-        }
-        cma = fmaxf(cma, fmaxf(w0, w1));
-        cmb = fmaxf(cmb, fmaxf(w2, w3));
+    for (int k2 = 0; k2 < 16; ++k2) {
+        float w = __uint_as_float((r[k2] & 0xFFFFFFF0u) | static_cast<uint32_t>(15 - k2));
+        if (kMasked && k2 >= nvalid) w = -INFINITY;
+        st.second = fmaxf(st.second, fminf(w, st.mxa));
+        st.mxa = fmaxf(st.mxa, w);
     }
-    if (fmaxf(cma, cmb) > st.second) {
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) {
-            const float w = (!kMasked || k2 < nvalid) ? __uint_as_float(r[k2]) : -INFINITY;
-            if (w > st.mxa) {
-                st.second = st.mxa;
-                st.mxa = w;
-                st.best_j = j0 + 2 * k2;
-            } else {
-                st.second = fmaxf(st.second, w);
-            }
-        }
-    }
+    st.best_j = st.mxa != m_in ? j0 : st.best_j;
+}
+__device__ __forceinline__ int tc_final_window(const TcSeqState& st) {
+    return st.best_j + 2 * (15 - static_cast<int>(__float_as_uint(st.mxa) & 15u));
 }
 
 __device__ __forceinline__ void tc_ld4(uint32_t taddr, uint32_t* r) {
@@ -402,7 +398,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
     const int n_passes = tc_num_passes(p.max_iters);
     const int NB = x.n_blocks;
 
-    if (warp == 9) {
+    // Register budget by role.  The register file is per sub-partition, 3 warps x 168 registers at launch: the third
+    // warpgroup keeps 72 per thread and the softmax warpgroups take 216 (2 x 216 + 72 = 3 x 168, the pool is what the
+    // CTA was launched with), which holds a chunk of S, the outgoing P chunk and the count accumulators without spills.
+    // Each setmaxnreg sits inside its role's branch so that the assembler can tell which limit the code below runs under.
+    if (warp >= 10) {
+        // idle: these warps only complete the third warpgroup (setmaxnreg is a warpgroup-wide instruction)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    } else if (warp == 9) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
         // ================= producer: one-hot codes of the next sequence =================
         // The arrays depend on the sequence only, so the producer simply cycles through the set; every sweep of
         // every tile consumes the sequences in the same order.
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             }
         }
     } else if (warp == 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
         // ================= MMA issuer: the warp stays converged, one elected lane issues =================
         {
             constexpr uint32_t idesc_base = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kTcRows >> 4) << 24);
@@ -558,6 +563,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
         __syncwarp();
     } else {
         // ================= softmax warpgroups: thread = bucket row, warpgroup = column half =================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
         const int row = tid & 127, wg = tid >> 7;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint32_t tD = tmem + lane_base + cD, tO = tmem + lane_base + cO, tS = tmem + lane_base + cS;
@@ -565,8 +571,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
         constexpr float kLn2 = 0.6931471805599453f;
         double sum_logw = 0.0;
         for (int i = 0; i < t; ++i) sum_logw += p.seq_logw[i];
-        double lbg_tot[4];  // log of the global symbol frequencies (theta0's background column)
-        for (int r = 0; r < 4; ++r) lbg_tot[r] = log(fmax(p.tot_sym[r] / p.tot_bases, 1e-9));
 
         unsigned int blk = 0, oq = 0, xq = 0;
         long long ts_s = 0, ts_o = 0, ts_u = 0, ts_kind[3] = {0, 0, 0}, ts_close = 0;
@@ -602,7 +606,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
 #pragma unroll
                     for (int r = 0; r < 4; ++r) acc[4 * c + r] = static_cast<float>((cnt8[c] >> (8 * r)) & 255u) * inv_n;
                 }
-                for (int r = 0; r < 4; ++r) lbg[r] = lbg_tot[r];
+                // log of the global symbol frequencies (theta0's background column)
+                for (int r = 0; r < 4; ++r) lbg[r] = log(fmax(p.tot_sym[r] / p.tot_bases, 1e-9));
             }
 
             for (int ps = 0; ps < n_passes; ++ps) {
@@ -725,9 +730,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 double ll = 0.0;
                 float ref2 = 0.f;
                 TcSeqState st = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), -INFINITY, -INFINITY, -INFINITY, 0};
-                uint32_t prof8[KC];  // final sweep, warpgroup 0: symbol counts of the argmax rows (one byte per symbol)
-#pragma unroll
-                for (int c = 0; c < KC; ++c) prof8[c] = 0;
                 bool pending = false;   // the previous sequence's O block has not been folded into acc yet
                 float pend_inv = 0.f;
                 unsigned int pend_oq = 0;
@@ -839,7 +841,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     if (B.last) {
                         TC_T0();
                         // ---- close the sequence: both column halves -> maximum, normaliser, likelihood term
-                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), fmaxf(st.mxa, st.mxb), st.second, __int_as_float(st.best_j));
+                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), fmaxf(st.mxa, st.mxb), st.second,
+                                                  __int_as_float(final_sweep ? tc_final_window(st) : 0));
                         xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = mine;
                         tc_named_sync();
                         const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
@@ -865,12 +868,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             // smallest offset in the reference, refine.hpp:311-316: decided by the exact kernel)
                             const float sec = fmaxf(fmaxf(a4.z, b4.z), fminf(a4.y, b4.y));
                             const int bj = a4.y >= b4.y ? __float_as_int(a4.w) : __float_as_int(b4.w);
-                            const float delta2 = (x.tie_delta + 1e-5f * fabsf(M * kLn2)) * kLog2e;
+                            // the weights compared here carry their column number in the low mantissa bits
+                            const float delta2 = (x.tie_delta + 1e-5f * fabsf(M * kLn2)) * kLog2e + kTcFinalUlpMargin * fabsf(M);
                             if (!(M - sec > delta2)) flags |= kTcFlagTie;
                             if (live && p.out_pos) p.out_pos[static_cast<int64_t>(wi) * t + i] = bj + 1;
-                            const uint64_t v = load_window(p.words + smeta[4 * i], bj);
-#pragma unroll
-                            for (int c = 0; c < KC; ++c) prof8[c] += 1u << (8 * (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u));
+                            // the references in mprev have served their purpose: the slot keeps the argmax for the profile below
+                            mprev[i * kTcRows + row] = __int_as_float(bj);
                         }
                         TC_ACC(ts_close);
                     }
@@ -895,6 +898,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     }
                 } else if (final_sweep && wg == 0 && live) {
                     // ---- score / consensus over the argmax rows (scoring.hpp:84-126)
+                    uint32_t prof8[KC];  // symbol counts of the argmax rows, one byte per symbol
+#pragma unroll
+                    for (int c = 0; c < KC; ++c) prof8[c] = 0;
+                    for (int i = 0; i < t; ++i) {
+                        const uint64_t v = load_window(p.words + smeta[4 * i], __float_as_int(mprev[i * kTcRows + row]));
+#pragma unroll
+                        for (int c = 0; c < KC; ++c) prof8[c] += 1u << (8 * (static_cast<unsigned>(v >> (62 - 2 * c)) & 3u));
+                    }
                     int score = 0;
                     unsigned long long cons = 0ULL;
 #pragma unroll
