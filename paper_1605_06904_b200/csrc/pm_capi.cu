@@ -2073,10 +2073,10 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         const int64_t s_iters1 = static_cast<int64_t>(scal[0]);
         out->em_work += (2 * s_iters1 - n_buckets) * c->x * l + 4 * s_iters1 * c->x;
         if (c->tc_used) {
-            // passes of a tile (pm_em_tc.cuh): I EM passes and the final E-step with three log-odds terms, min(I, 2) MAX
-            // passes with one; GEMM2 in the I EM passes
+            // passes of a tile (pm_em_tc.cuh): I EM passes and the final E-step with three log-odds terms; GEMM2 in the
+            // I EM passes
             const int64_t I = cfg->max_em_iters, tiles = (n_buckets + k::kTcRows - 1) / k::kTcRows;
-            out->em_tensor_flops += tiles * (c->tc_g1_flops * (3 * (I + 1) + std::min<int64_t>(I, 2)) + c->tc_g2_flops * I);
+            out->em_tensor_flops += tiles * (c->tc_g1_flops * 3 * (I + 1) + c->tc_g2_flops * I);
         }
     }
 

@@ -165,12 +165,12 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32])
 // ---- per-chunk work of a softmax thread: 16 columns (= 16 windows of one parity) of its row ------------------
 struct TcSeqState {
     float2 sum2a, sum2b;  // partial sums of e (EM pass): four independent chains
-    float mxa, mxb;       // running maximum of the weights: two chains (final pass: mxa only)
+    float mxa;            // final pass: running maximum of the weights
     float second;         // final pass: runner-up weight
     int best_j;           // final pass: window of the maximum
 };
 
-// EM pass: e = 2^(w - ref), running sum and maximum, e as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM
+// EM pass: e = 2^(w - ref), running sum, e as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM
 template <bool kMasked>
 __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint32_t* __restrict__ o, int nvalid, float ref2,
                                             TcSeqState& st) {
@@ -192,8 +192,6 @@ __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint
             if (k2 + 2 >= nvalid) w1.x = -INFINITY;
             if (k2 + 3 >= nvalid) w1.y = -INFINITY;
         }
-        st.mxa = fmaxf(st.mxa, fmaxf(w0.x, w0.y));
-        st.mxb = fmaxf(st.mxb, fmaxf(w1.x, w1.y));
         const float2 a0 = f2_add(w0, nref), a1 = f2_add(w1, nref);
         const float2 e0 = make_float2(fast_ex2(a0.x), fast_ex2(a0.y));  // 2^-inf = 0 for masked columns
         const float2 e1 = make_float2(fast_ex2(a1.x), fast_ex2(a1.y));
@@ -208,23 +206,6 @@ __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint
         o[(k2 >> 1) + 1] = h1;
         o[8 + (k2 >> 1)] = tc_pack_bf16(l0.x, l0.y);
         o[8 + (k2 >> 1) + 1] = tc_pack_bf16(l1.x, l1.y);
-    }
-}
-
-// MAX pass: running maximum only
-template <bool kMasked>
-__device__ __forceinline__ void tc_max_chunk(const uint32_t* __restrict__ r, int nvalid, TcSeqState& st) {
-#pragma unroll
-    for (int k2 = 0; k2 < 16; k2 += 4) {
-        float w0 = __uint_as_float(r[k2]), w1 = __uint_as_float(r[k2 + 1]), w2 = __uint_as_float(r[k2 + 2]), w3 = __uint_as_float(r[k2 + 3]);
-        if (kMasked) {
-            if (k2 >= nvalid) w0 = -INFINITY;
-            if (k2 + 1 >= nvalid) w1 = -INFINITY;
-            if (k2 + 2 >= nvalid) w2 = -INFINITY;
-            if (k2 + 3 >= nvalid) w3 = -INFINITY;
-        }
-        st.mxa = fmaxf(st.mxa, fmaxf(w0, w1));
-        st.mxb = fmaxf(st.mxb, fmaxf(w2, w3));
     }
 }
 
@@ -271,33 +252,29 @@ __device__ __forceinline__ void tc_split3(float x, uint32_t& hi, uint32_t& mid, 
 }
 
 
-// A tile is refined in PASSES over the whole sequence set.  EM iteration `it` (0-based) is one EM pass (E-step fused
-// with the M-step counts); the first two iterations are preceded by a MAX pass (GEMM1 + a per-sequence maximum, no
-// exponentials), because theta0 (floored columns) and theta1 put the per-sequence maxima hundreds of units away from
-// any reference known beforehand; from the third iteration on the previous iteration's maximum is the reference.
-// The last pass is the final E-step (refine.hpp:306).  Every role decodes the same list.
-enum : int { kTcPassMax = 0, kTcPassEm = 1, kTcPassFinal = 2 };
+// A tile is refined in PASSES over the whole sequence set: EM iteration `it` (0-based) is one EM pass (E-step fused
+// with the M-step counts), the last pass is the final E-step (refine.hpp:306).  Every role decodes the same list.
+//
+// The exponentials of an EM pass are taken relative to ONE reference per bucket and pass, kTcRefBelow under the upper
+// bound ub = sum_c max_r D[c][r] of every window weight of the model: e = 2^(w - ub + 108) <= 2^108 cannot overflow
+// (nor can a sequence's sum, or the FP32 count accumulators), and a sequence whose best window lies up to
+// ~210 below ub -- seven columns at the 1e-9 floor -- still has its leading terms 24 binades above the FP32
+// underflow threshold; relative precision does not depend on the scale.  A sequence below that range (its sum under
+// kTcMinSum) flags the bucket for the exact kernel.  This replaces the separate per-sequence maximum passes
+// (GEMM1 + a max scan of S) that the first two iterations needed to find a reference.
+enum : int { kTcPassEm = 1, kTcPassFinal = 2 };
+constexpr float kTcRefBelow = 108.f;                 // log2 units
+constexpr float kTcMinSum = 7.888609052210118e-31f;  // 2^-100
 struct TcPass {
     int kind, it;
-    bool new_model;  // theta -> log-odds terms are rebuilt before this pass
+    bool new_model;  // theta -> log-odds terms are rebuilt before this pass (always: every pass has its own model)
 };
-__device__ __forceinline__ int tc_num_passes(int max_iters) { return max_iters + min(max_iters, 2) + 1; }
+__device__ __forceinline__ int tc_num_passes(int max_iters) { return max_iters + 1; }
 __device__ __forceinline__ TcPass tc_pass(int ps, int max_iters) {
-    const int pre = min(max_iters, 2);
     TcPass r;
-    if (ps < 2 * pre) {
-        r.it = ps >> 1;
-        r.kind = (ps & 1) ? kTcPassEm : kTcPassMax;
-        r.new_model = !(ps & 1);
-    } else if (ps < max_iters + pre) {
-        r.it = ps - pre;
-        r.kind = kTcPassEm;
-        r.new_model = true;
-    } else {
-        r.it = max_iters;
-        r.kind = kTcPassFinal;
-        r.new_model = true;
-    }
+    r.it = ps;
+    r.kind = ps < max_iters ? kTcPassEm : kTcPassFinal;
+    r.new_model = true;
     return r;
 }
 
@@ -305,7 +282,7 @@ __device__ __forceinline__ TcPass tc_pass(int ps, int max_iters) {
 __host__ __device__ inline size_t tc_smem_bytes(int t, int n_blocks, int e_positions) {
     size_t b = 0;
     b += static_cast<size_t>(4) * e_positions * 8;                 // E0/E1 of two sequences
-    b += static_cast<size_t>(t) * kTcRows * 4;                       // previous maxima (log2 units)
+    b += static_cast<size_t>(t) * kTcRows * 4;                       // argmax of every sequence (final pass)
     b += static_cast<size_t>(2) * 2 * kTcRows * 16;                  // partner exchange, double-buffered
     b += static_cast<size_t>(n_blocks) * sizeof(TcBlock);
     b += static_cast<size_t>(t) * 16 + 16;                           // per-sequence metadata (+ win_off[t])
@@ -350,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
     }
     const int EB = x.e_positions * 8;  // bytes per one-hot array
     unsigned char* Ebuf = smem;        // [2 sequences][2 parities][EB]
-    float* mprev = reinterpret_cast<float*>(Ebuf + 4 * static_cast<size_t>(EB));  // [t][128]
+    float* mprev = reinterpret_cast<float*>(Ebuf + 4 * static_cast<size_t>(EB));  // [t][128]: the final pass's argmax per sequence
     float4* xch = reinterpret_cast<float4*>(mprev + static_cast<size_t>(t) * kTcRows);  // [2][2][128]
     TcBlock* blocks = reinterpret_cast<TcBlock*>(xch + 2 * 2 * kTcRows);
     int* smeta = reinterpret_cast<int*>(blocks + x.n_blocks);  // [t][4]: first word (global index), windows, first flat index, bases
@@ -453,8 +430,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             long long tm_p = 0, tm_e = 0, tm_d = 0;
             const long long tm_begin = clock64();
 
-            // terms: 3 = full precision; the MAX passes only need a reference within a few units: the leading term
-            auto issue_g1 = [&](const TcBlock& B, unsigned int buf, unsigned int sq, bool one_term) {
+            auto issue_g1 = [&](const TcBlock& B, unsigned int buf, unsigned int sq) {
                 const uint32_t tS = tmem + cS + buf * NBLK;
 #pragma unroll 1
                 for (int sgi = 0; sgi < 2; ++sgi) {
@@ -466,12 +442,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     if (tc_elect()) {
 #pragma unroll
                         for (int kb = 0; kb < KC / 4; ++kb) tc_mma(d, tmem + cD + 8 * kb, lo + 2 * kb, hi1, idesc, kb != 0);
-                        if (!one_term) {
 #pragma unroll
-                            for (int term = 1; term < 3; ++term) {
+                        for (int term = 1; term < 3; ++term) {
 #pragma unroll
-                                for (int kb = 0; kb < KC / 4; ++kb) tc_mma(d, tmem + cD + term * 2 * KC + 8 * kb, lo + 2 * kb, hi1, idesc, true);
-                            }
+                            for (int kb = 0; kb < KC / 4; ++kb) tc_mma(d, tmem + cD + term * 2 * KC + 8 * kb, lo + 2 * kb, hi1, idesc, true);
                         }
                     }
                     __syncwarp();
@@ -497,7 +471,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
                         TC_ACC(tm_e);
                     }
-                    issue_g1(blocks[0], blk & 1, sq_g1, pass.kind == kTcPassMax);
+                    issue_g1(blocks[0], blk & 1, sq_g1);
                     if (blocks[0].last) ++sq_g1;
                     bool o_acc = false;
 #pragma unroll 1
@@ -510,7 +484,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                                 tc_wait(&e_full[sq_g1 & 1], (sq_g1 >> 1) & 1);
                                 TC_ACC(tm_e);
                             }
-                            issue_g1(B1, (blk + 1) & 1, sq_g1, pass.kind == kTcPassMax);
+                            issue_g1(B1, (blk + 1) & 1, sq_g1);
                             if (B1.last) ++sq_g1;
                         }
                         {
@@ -581,6 +555,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             const WorkDesc wd = live ? p.work[wi] : WorkDesc{0, 0, 0, 0};
             float acc[4 * HP];       // my columns' expected counts (EM sweeps) / theta0 counts
             unsigned flags = 0;
+            float ref2 = 0.f;  // reference of the current pass's exponentials (log2 units)
             double prev_ll = 0.0, expct = 0.0;
             double lbg[4];           // natural logs of the current background column
 
@@ -612,7 +587,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
 
             for (int ps = 0; ps < n_passes; ++ps) {
                 const TcPass pass = tc_pass(ps, p.max_iters);
-                const bool final_sweep = pass.kind == kTcPassFinal, max_pass = pass.kind == kTcPassMax, em_pass = pass.kind == kTcPassEm;
+                const bool final_sweep = pass.kind == kTcPassFinal, em_pass = pass.kind == kTcPassEm;
                 // ---- theta of this iteration -> log-odds terms in tensor memory.  Iteration 0: acc holds theta0 itself;
                 // otherwise acc holds the expected counts of the previous EM pass (M-step, refine.hpp:227-269).
                 if (pass.new_model) {
@@ -656,7 +631,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     // per column: write_column (refine.hpp:256-269), expectation = sum_c max_r theta[r][c]
                     // (refine.hpp:130-136) and the log-odds D[c][r] = log2 max(theta,1e-9) - log2 max(bg,1e-9) as three
                     // bf16 terms.  FP32 throughout: the counts are FP32 sums; log2f is accurate to 1 ulp (2e-6 at |D| = 20).
-                    float ex_part = 0.f;
+                    float ex_part = 0.f, ub_part = 0.f;
                     uint32_t dcol[3][2 * HP];
                     float lbg2[4];
 #pragma unroll
@@ -691,6 +666,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                                 p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + (c_lo + c + 1)] = static_cast<double>(v[r]);
                         }
                         if (col_live) ex_part += mx;
+                        ub_part += fmaxf(fmaxf(d2[0], d2[1]), fmaxf(d2[2], d2[3]));  // dead columns: all zero
                         uint32_t h[4], m[4], lw[4];
 #pragma unroll
                         for (int r = 0; r < 4; ++r) tc_split3(d2[r], h[r], m[r], lw[r]);
@@ -707,14 +683,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         for (int q = 0; q < 2 * HP; q += 4) tc_st4(tD + term * 2 * KC + 2 * c_lo + q, &dcol[term][q]);
                     }
                     tc_wait_st();
-                    // expectation: partner exchange
-                    reinterpret_cast<double*>(&xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row])[0] = static_cast<double>(ex_part);
+                    // expectation and the weight bound: partner exchange
+                    xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = make_float4(ex_part, ub_part, 0.f, 0.f);
                     tc_fence_before();
                     tc_named_sync();
                     {
-                        const double oex = reinterpret_cast<const double*>(&xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row])[0];
+                        const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
                         ++xq;
-                        expct = wg == 0 ? static_cast<double>(ex_part) + oex : oex + static_cast<double>(ex_part);
+                        expct = wg == 0 ? static_cast<double>(ex_part) + static_cast<double>(oth.x) : static_cast<double>(oth.x) + static_cast<double>(ex_part);
+                        ref2 = (wg == 0 ? ub_part + oth.y : oth.y + ub_part) - kTcRefBelow;  // same value in both partners
                     }
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(&d_full[0]);
@@ -728,8 +705,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 const long long ts_pass0 = clock64();
 #endif
                 double ll = 0.0;
-                float ref2 = 0.f;
-                TcSeqState st = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), -INFINITY, -INFINITY, -INFINITY, 0};
+                TcSeqState st = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), -INFINITY, -INFINITY, 0};
                 bool pending = false;   // the previous sequence's O block has not been folded into acc yet
                 float pend_inv = 0.f;
                 unsigned int pend_oq = 0;
@@ -771,11 +747,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     const TcBlock B = blocks[n];
                     const int i = B.seq;
                     if (B.first) {
-                        ref2 = mprev[i * kTcRows + row];  // this sequence's maximum in the MAX pass / previous iteration
                         st.sum2a = make_float2(0.f, 0.f);
                         st.sum2b = make_float2(0.f, 0.f);
                         st.mxa = -INFINITY;
-                        st.mxb = -INFINITY;
                         st.second = -INFINITY;
                         st.best_j = 0;
                     }
@@ -806,9 +780,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                                 tc_em_chunk<false>(r, o, 16, ref2, st);
                                 tc_em_chunk<false>(r + 16, o + 16, 16, ref2, st);
                                 tc_st32(tB + cc, o);
-                            } else if (max_pass) {
-                                tc_max_chunk<false>(r, 16, st);
-                                tc_max_chunk<false>(r + 16, 16, st);
                             } else {
                                 tc_final_chunk<false>(r, 16, j, st);
                                 tc_final_chunk<false>(r + 16, 16, j + 32, st);
@@ -824,8 +795,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                                 uint32_t o[16];
                                 tc_em_chunk<true>(r, o, nv, ref2, st);
                                 tc_st16(tB + cc, o);
-                            } else if (max_pass) {
-                                tc_max_chunk<true>(r, nv, st);
                             } else {
                                 tc_final_chunk<true>(r, nv, j, st);
                             }
@@ -841,38 +810,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     if (B.last) {
                         TC_T0();
                         // ---- close the sequence: both column halves -> maximum, normaliser, likelihood term
-                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), fmaxf(st.mxa, st.mxb), st.second,
+                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), st.mxa, st.second,
                                                   __int_as_float(final_sweep ? tc_final_window(st) : 0));
                         xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = mine;
                         tc_named_sync();
                         const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
                         ++xq;
                         const float4 a4 = wg == 0 ? mine : oth, b4 = wg == 0 ? oth : mine;  // fixed order
-                        const float M = fmaxf(a4.y, b4.y);
-                        if (!(M > -INFINITY) || !(M < INFINITY)) flags |= kTcFlagBad;
-                        if (max_pass) {
-                            if (wg == 0) mprev[i * kTcRows + row] = M;
-                        } else if (em_pass) {
+                        if (em_pass) {
                             const float L = a4.x + b4.x;
-                            const float sh = M - ref2;
-                            if (!(sh > -86.f && sh < 86.f) || !(L > 0.f) || !(L < INFINITY)) flags |= kTcFlagRange;
+                            // below kTcMinSum the sequence's best window is more than ~208 under the bound: out of range
+                            if (!(L >= kTcMinSum) || !(L < INFINITY)) flags |= kTcFlagRange;
                             pend_inv = 1.f / L;
                             pend_oq = oq++;
                             pending = true;
                             if (wg == 0) {
-                                mprev[i * kTcRows + row] = M;
-                                ll += (static_cast<double>(ref2) + static_cast<double>(log2f(L))) * 0.6931471805599453;
+                                // log2 L = exponent + log2(mantissa): the absolute error stays at 1e-7 whatever the scale
+                                const uint32_t lb = __float_as_uint(L);
+                                const float mant = __uint_as_float((lb & 0x007FFFFFu) | 0x3F800000u);
+                                const int ex = static_cast<int>(lb >> 23) - 127;
+                                ll += ((static_cast<double>(ref2) + static_cast<double>(ex)) + static_cast<double>(log2f(mant))) * 0.6931471805599453;
                             }
                         } else if (wg == 0) {
                             // argmax with margin: the runner-up must lie tie_delta below the maximum (ties go to the
                             // smallest offset in the reference, refine.hpp:311-316: decided by the exact kernel)
+                            const float M = fmaxf(a4.y, b4.y);
+                            if (!(M > -INFINITY) || !(M < INFINITY)) flags |= kTcFlagBad;
                             const float sec = fmaxf(fmaxf(a4.z, b4.z), fminf(a4.y, b4.y));
                             const int bj = a4.y >= b4.y ? __float_as_int(a4.w) : __float_as_int(b4.w);
                             // the weights compared here carry their column number in the low mantissa bits
                             const float delta2 = (x.tie_delta + 1e-5f * fabsf(M * kLn2)) * kLog2e + kTcFinalUlpMargin * fabsf(M);
                             if (!(M - sec > delta2)) flags |= kTcFlagTie;
                             if (live && p.out_pos) p.out_pos[static_cast<int64_t>(wi) * t + i] = bj + 1;
-                            // the references in mprev have served their purpose: the slot keeps the argmax for the profile below
+                            // parked for the profile below
                             mprev[i * kTcRows + row] = __int_as_float(bj);
                         }
                         TC_ACC(ts_close);
@@ -947,7 +917,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             atomicAdd(p.phase_clk + 2, static_cast<unsigned long long>(ts_o));
             atomicAdd(p.phase_clk + 3, static_cast<unsigned long long>(ts_u));
             atomicAdd(p.phase_clk + 4, static_cast<unsigned long long>(ts_kind[kTcPassEm]));
-            atomicAdd(p.phase_clk + 5, static_cast<unsigned long long>(ts_kind[kTcPassMax]));
+            atomicAdd(p.phase_clk + 5, static_cast<unsigned long long>(ts_kind[0]));
             atomicAdd(p.phase_clk + 6, static_cast<unsigned long long>(ts_kind[kTcPassFinal]));
             atomicAdd(p.phase_clk + 7, static_cast<unsigned long long>(ts_close));
         }
