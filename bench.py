@@ -42,6 +42,9 @@ CONFIGS = {
     # large-scale sweep; k, s are what the reference derives for this size (k=l-d-1, s=ceil(2x/4^k)); m explicit
     "c5": dict(t=10000, n=1000, l=15, d=4, k=10, s=19, m=2, label="C5 planted (15,4) t=10000 n=1000 k=10 s=19",
                extrapolate_cpu=True),
+    # the same set with the t=20 configurations' k, s: every one of the 16,384 buckets is enriched (~600 members each)
+    "c5b": dict(t=10000, n=1000, l=15, d=4, k=7, s=4, m=1, label="C5b planted (15,4) t=10000 n=1000 k=7 s=4",
+                extrapolate_cpu=True),
 }
 INSTANCE_SEED = 42
 RUN_SEED = 7

@@ -20,7 +20,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("PM_B200_LIB") or os.path.join(PKG_DIR, "libpm_b200.so")  # override: instrumented builds
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = ["pm_capi.cu", "pm_host.cpp"]
-HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_em_tc.cuh", "pm_hash_fused.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
+HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_em_tc.cuh", "pm_em_f64.cuh", "pm_planted.cuh", "pm_hash_fused.cuh", "pm_hash_count.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

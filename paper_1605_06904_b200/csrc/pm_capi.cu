@@ -32,6 +32,7 @@
 #include "pm_em_f64.cuh"
 #include "pm_planted.cuh"
 #include "pm_hash_fused.cuh"
+#include "pm_hash_count.cuh"
 
 using namespace pm;
 
@@ -1946,6 +1947,89 @@ int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
     return PM_OK;
 }
 
+// Large sets with a dense table of at most 2^20 entries: device-wide counting sort (pm_hash_count.cuh) -- when the
+// mean bucket size x / 4^k is below the threshold s, i.e. when enriched buckets are the exception (10,000 sequences,
+// k = 10, s = 19: 1 % of the l-mers are members).  When nearly every l-mer is a member of an enriched bucket (the same
+// set with k = 7, s = 4: 16,384 buckets of ~600) the contended cursor atomics and the per-bucket ordering cost more
+// than the three passes of the radix sort (measured 0.85 against 0.69 ms per trial), so that stays on the sort path.
+// PM_B200_COUNT_HASH: 0 never, 2 whenever the table fits (tests).
+bool count_hash_applies(const pm_ctx* c, int keybits, int thr) {
+    const char* env = std::getenv("PM_B200_COUNT_HASH");
+    const int mode = env != nullptr ? std::atoi(env) : 1;
+    if (mode == 0 || keybits > 20) return false;
+    return mode >= 2 || c->x < static_cast<int64_t>(thr) * (1LL << keybits);
+}
+
+// hash_trial + enriched_buckets of every trial of the batch.  *ok = false when some enriched bucket is too large for
+// the in-CTA ordering step (degenerate input): the caller then takes the radix-sort path.  One host sync per batch
+// (the size check) -- on this path a trial's EM stage takes seconds.
+int count_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keybits, int thr, unsigned int** members,
+                      Records* r, bool* ok) {
+    const int n = static_cast<int>(progs.size());
+    const int64_t tsize = 1LL << keybits;
+    r->cap_e = std::max<int64_t>(1, c->x / thr);
+    const size_t nrec = static_cast<size_t>(n) * static_cast<size_t>(r->cap_e);
+    PM_TRY(get_buf(c, S_REC_KEY, nrec, &r->key));
+    PM_TRY(get_buf(c, S_REC_START, nrec, &r->start));
+    PM_TRY(get_buf(c, S_REC_SIZE, nrec, &r->size));
+    PM_TRY(get_buf(c, S_NREC, static_cast<size_t>(n), &r->n_rec));
+    unsigned int* table;
+    unsigned int* slots;
+    const size_t table_words = static_cast<size_t>(n) * static_cast<size_t>(tsize);
+    PM_TRY(get_buf(c, S_COUNTS, table_words + 1, &table));  // + the largest enriched bucket of the batch
+    PM_TRY(get_buf(c, S_IDX_A, static_cast<size_t>(n) * static_cast<size_t>(c->x), &slots));
+    unsigned int* d_max = table + table_words;
+    PM_CUDA(cudaMemsetAsync(table, 0, (table_words + 1) * sizeof(unsigned int), c->stream));
+    k::CountParams p;
+    p.words = c->d_words;
+    p.word_off = c->d_word_off;
+    p.win_off = c->d_win_off;
+    p.t = c->t;
+    p.x = c->x;
+    p.uniform_w = c->uniform_w;
+    p.table_size = tsize;
+    p.table = table;
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((c->x + 255) / 256, 8LL * c->sm_count)));
+    for (int base = 0; base < n; base += k::kMaxConstPlans) {
+        const int cnt = std::min(k::kMaxConstPlans, n - base);
+        c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
+        ConstPlansUse plans_use(c->device, c->stream);
+        PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
+                                        0, cudaMemcpyHostToDevice, c->stream));
+        p.plan_base = base;
+        p.n_trials = cnt;
+        const dim3 grid(gx, static_cast<unsigned>(std::min(cnt, 64)));
+        k::count_hist_kernel<<<grid, 256, 0, c->stream>>>(p);
+        PM_TRY(check_launch(c, "count_hist"));
+        const int n_chunks = static_cast<int>((tsize + k::kCountChunk - 1) / k::kCountChunk);
+        uint2* partial;
+        PM_TRY(get_buf(c, S_DIGIT_TOT, static_cast<size_t>(cnt) * static_cast<size_t>(n_chunks), &partial));
+        const dim3 sgrid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(cnt));
+        k::count_partial_kernel<<<sgrid, k::kCountScanThreads, 0, c->stream>>>(
+            table + static_cast<size_t>(base) * static_cast<size_t>(tsize), tsize, thr, n_chunks, partial);
+        PM_TRY(check_launch(c, "count_partial"));
+        k::count_scan_kernel<<<sgrid, k::kCountScanThreads, 0, c->stream>>>(
+            table + static_cast<size_t>(base) * static_cast<size_t>(tsize), tsize, thr, r->cap_e, n_chunks, partial,
+            r->key + static_cast<size_t>(base) * static_cast<size_t>(r->cap_e),
+            r->start + static_cast<size_t>(base) * static_cast<size_t>(r->cap_e),
+            r->size + static_cast<size_t>(base) * static_cast<size_t>(r->cap_e), r->n_rec + base, d_max);
+        PM_TRY(check_launch(c, "count_scan"));
+        k::count_scatter_kernel<<<grid, 256, 0, c->stream>>>(p, slots);
+        PM_TRY(check_launch(c, "count_scatter"));
+    }
+    unsigned int h_max = 0;
+    PM_TRY(d2h(c, &h_max, d_max, sizeof(h_max)));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    *ok = h_max <= static_cast<unsigned int>(k::kCountMaxBucket);
+    if (!*ok) return PM_OK;
+    const unsigned ox = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(r->cap_e, 16LL * c->sm_count)));
+    k::count_order_kernel<<<dim3(ox, static_cast<unsigned>(std::min(n, 64))), k::kCountOrderThreads, 0, c->stream>>>(
+        slots, c->x, r->cap_e, n, r->start, r->size, r->n_rec);
+    PM_TRY(check_launch(c, "count_order"));
+    *members = slots;
+    return PM_OK;
+}
+
 template <typename KeyT>
 int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
               int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
@@ -1963,7 +2047,13 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         StageTimer tk(c, prof, 0);
         PM_TRY(get_buf(c, S_IDX_A, progs.size() * static_cast<size_t>(c->x), &srt.idx));
         PM_TRY(fused_hash_bucket(c, progs, 2 * params.k, params.s, srt.idx, &rec));
-    } else {
+    }
+    bool counted = false;
+    if (!fused && count_hash_applies(c, 2 * params.k, params.s)) {
+        StageTimer tk(c, prof, 0);
+        PM_TRY(count_hash_bucket(c, progs, 2 * params.k, params.s, &srt.idx, &rec, &counted));
+    }
+    if (!fused && !counted) {
         StageTimer tk(c, prof, 0);
         const size_t n = progs.size() * static_cast<size_t>(c->x);
         KeyT *ka, *kb;
@@ -1981,7 +2071,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     k::WorkDesc* work;
     {
         StageTimer te(c, prof, 2);
-        if (!fused) PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
+        if (!fused && !counted) PM_TRY(find_enriched<KeyT>(c, srt, n_trials, params.s, &rec));
         PM_TRY(get_buf(c, S_WORK_OFF, static_cast<size_t>(n_trials) + 1, &work_off));
         PM_TRY(get_buf(c, S_WORK, static_cast<size_t>(n_trials) * static_cast<size_t>(rec.cap_e), &work));
         k::work_scan_kernel<<<1, 1024, 0, c->stream>>>(rec.n_rec, n_trials, work_off);

@@ -233,37 +233,71 @@ def test_degenerate_shapes_match_oracle(ctx, best_oracle):
         assert abs(got["expectation"] - want["expectation"]) <= EXPECTATION_TOL
 
 
-def test_fused_hash_path_equals_sort_path(pm, best_oracle, instance):
+def test_fused_count_and_sort_bucketing_agree(pm, best_oracle, instance):
     """run() buckets each trial with the one-CTA shared-memory histogram kernel (csrc/pm_hash_fused.cuh) when
-    the dense table fits; PM_B200_FUSED_HASH=0 forces the radix-sort path.  Per-trial outcomes must be
-    identical, on the challenge instance and on low-complexity sets whose buckets hold hundreds of members
-    (cooperative ordering) or whose key space is smaller than the CTA (k <= 4)."""
+    the dense table fits one CTA, with the device-wide counting sort (csrc/pm_hash_count.cuh) when it does not and
+    4^k <= 2^20, and with the segmented radix sort otherwise; PM_B200_FUSED_HASH=0 with PM_B200_COUNT_HASH=2 / 0
+    force the later paths.  Per-trial outcomes must be identical, on the challenge instance and on low-complexity sets whose
+    buckets hold hundreds of members (cooperative ordering), whose key space is smaller than the CTA (k <= 4), or
+    whose largest bucket exceeds what the counting path orders in shared memory (it then falls back by itself)."""
     import os
     rng = np.random.default_rng(21)
     low = pmo.SeqSet.from_strings(["".join(rng.choice(list("AC"), 150, p=[0.9, 0.1])) for _ in range(6)])
     ragged = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(40, 200)))) for _ in range(9)])
+    mono = pmo.SeqSet.from_strings(["".join(rng.choice(list("AC"), 700, p=[0.97, 0.03])) for _ in range(8)])
     cases = [
         (instance(20, 600, 15, 4, 42)[0], dict(l=15, d=4, k=7, s=4, m=6, seed=7, early_stop=0)),
         (low, dict(l=9, d=2, k=6, s=3, m=4, seed=1, early_stop=0)),      # buckets of several hundred members
         (low, dict(l=9, d=2, k=8, s=40, m=3, seed=2, early_stop=0)),     # 4^8 keys, high threshold, r_cap truncation
         (ragged, dict(l=7, d=1, k=3, s=2, m=5, seed=3, early_stop=0)),   # 64 keys < 512 threads
         (ragged, dict(l=6, d=1, k=1, s=1, m=3, seed=4, early_stop=0)),   # 4 keys
+        (mono, dict(l=8, d=1, k=4, s=3, m=2, seed=5, early_stop=0)),     # one bucket of > 4096 members
     ]
+    modes = {"fused": {}, "count": {"PM_B200_FUSED_HASH": "0", "PM_B200_COUNT_HASH": "2"},
+             "sort": {"PM_B200_FUSED_HASH": "0", "PM_B200_COUNT_HASH": "0"}}
     for ss, kw in cases:
         res = {}
-        for flag in ("1", "0"):
-            os.environ["PM_B200_FUSED_HASH"] = flag
+        for name, env in modes.items():
+            os.environ.update(env)
             try:
                 with pm.Context(0) as c:
                     c.set_sequences(ss.bases, ss.offs)
-                    res[flag] = c.run(per_trial=True, **kw)
+                    res[name] = c.run(per_trial=True, **kw)
             finally:
-                os.environ.pop("PM_B200_FUSED_HASH", None)
-        a, b = res["1"], res["0"]
-        assert a["gpu_launches"] < b["gpu_launches"]  # the fused path really ran
-        for f in INT_FIELDS + ("expectation",):
-            assert a[f] == b[f], (kw, f)
-        for f in ("trial_buckets", "trial_score", "trial_key", "trial_expectation"):
-            assert (a[f] == b[f]).all(), (kw, f)
+                for key in env:
+                    os.environ.pop(key, None)
+        a = res["fused"]
+        assert a["gpu_launches"] < res["count"]["gpu_launches"]  # the fused path really ran
+        assert res["count"]["gpu_launches"] != res["sort"]["gpu_launches"]
+        for name in ("count", "sort"):
+            b = res[name]
+            for f in INT_FIELDS + ("expectation",):
+                assert a[f] == b[f], (kw, name, f)
+            for f in ("trial_buckets", "trial_score", "trial_key", "trial_expectation"):
+                assert (a[f] == b[f]).all(), (kw, name, f)
         want = best_oracle.run(ss, **kw)
         assert (a["score"], a["buckets_enriched"], a["trials_run"]) == (want["score"], want["buckets_enriched"], want["trials_run"])
+
+
+def test_large_scale_c5_counting_sort_equals_radix_sort(pm):
+    """BASELINE config 5 at full size through run(): one trial with the reference-derived k=10, s=19 (5,346 enriched
+    buckets of ~20 members) and one with k=7, s=4 (all 16,384 buckets enriched, ~600 members each: the M-step at
+    scale) -- the counting-sort bucketing against the radix-sort path, every per-trial outcome identical."""
+    import os
+    bases, offs, motif, _ = pm.generate_planted(10000, 1000, 15, 4, 42)
+    for k, s, n_enriched in ((10, 19, None), (7, 4, 16384)):
+        res = {}
+        for flag in ("2", "0"):
+            os.environ["PM_B200_COUNT_HASH"] = flag
+            try:
+                with pm.Context(0) as c:
+                    c.set_sequences(bases, offs)
+                    res[flag] = c.run(per_trial=True, l=15, d=4, k=k, s=s, m=1, seed=7, early_stop=0)
+            finally:
+                os.environ.pop("PM_B200_COUNT_HASH", None)
+        a, b = res["2"], res["0"]
+        for f in INT_FIELDS + ("expectation",):
+            assert a[f] == b[f], (k, s, f)
+        for f in ("trial_buckets", "trial_score", "trial_key", "trial_expectation"):
+            assert (a[f] == b[f]).all(), (k, s, f)
+        assert a["buckets_enriched"] > 5000 and (n_enriched is None or a["buckets_enriched"] == n_enriched)
