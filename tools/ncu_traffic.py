@@ -15,8 +15,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main():
     args = sys.argv[1:]
-    commit = subprocess.run(["git", "-C", REPO, "rev-parse", "--short", "HEAD"], capture_output=True, text=True).stdout.strip()
-    path = os.path.join(REPO, "profiles", "traffic.json")
+    commit = os.environ.get("PM_COMMIT") or subprocess.run(["git", "-C", REPO, "rev-parse", "--short", "HEAD"],
+                                                           capture_output=True, text=True).stdout.strip()
+    path = os.path.join(REPO, os.environ.get("PM_PROFILES_DST", "profiles"), "traffic.json")
     rec = {"captures": []}
     if os.path.exists(path):
         rec = json.load(open(path))
