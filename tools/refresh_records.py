@@ -84,15 +84,16 @@ def main():
         open(f"{DST}/{rep}_ncu_full.txt", "w").write(
             f"ncu --set full --clock-control none (tools/capture_profiles.sh), digest by tools/ncu_summary.py of {rep}.ncu-rep\n\n" + txt)
         pairs += [cfg, path]
-    if pairs:
+    if os.path.isdir(f"{SRC}/profiles_r2") and DST != f"{SRC}/profiles_r2":
+        # digests made on the GPU box (most reports are too large to bring back): they are the record
+        for name in sorted(os.listdir(f"{SRC}/profiles_r2")):
+            if name.endswith("_ncu_full.txt") or name == "traffic.json":
+                shutil.copy(f"{SRC}/profiles_r2/{name}", f"{DST}/{name}")
+    elif pairs:
         if os.path.exists(f"{DST}/traffic.json"):
             os.remove(f"{DST}/traffic.json")
         subprocess.run([sys.executable, "tools/ncu_traffic.py"] + pairs, check=True, stdout=subprocess.DEVNULL,
                        env=dict(os.environ, PM_PROFILES_DST=DST))
-    else:  # digests made on the GPU box (the reports themselves are too large to bring back)
-        for name in sorted(os.listdir(f"{SRC}/profiles_r2")) if os.path.isdir(f"{SRC}/profiles_r2") else []:
-            if name.endswith("_ncu_full.txt") or name == "traffic.json":
-                shutil.copy(f"{SRC}/profiles_r2/{name}", f"{DST}/{name}")
 
     fmt = lambda x: f"{x / 1000:.1f} k" if x >= 1000 else f"{x:.2f}"
     rows = ["| config | trials/s (HBM-resident) | e2e trials/s | EM share of step | roofline kernel | achieved / peak | frac | "
