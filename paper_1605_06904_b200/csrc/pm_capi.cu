@@ -1079,8 +1079,9 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
                 x.zcap = c->zlen;
                 x.wcap = stage_words;
                 if (big) PM_TRY(get_buf(c, S_MPREV, static_cast<size_t>(grid) * 2 * static_cast<size_t>(c->t), &x.mprev_g));
-                // third tier: stop decisions within the error of this kernel's likelihood go to the FP64 kernel
-                const bool tier3 = theta_in == nullptr && max_iters >= 3;
+                // third tier: stop decisions within the error of this kernel's likelihood, and argmax decisions between
+                // different windows whose FP64 weights agree to 1e-9, go to the FP64 kernel
+                const bool tier3 = theta_in == nullptr;
                 if (tier3) {
                     PM_TRY(get_buf(c, S_F64_FLAG, static_cast<size_t>(n_work_bound), &p.flag_exact));
                     PM_CUDA(cudaMemsetAsync(p.flag_exact, 0, static_cast<size_t>(n_work_bound), c->stream));

@@ -674,26 +674,41 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                 arg = s.best_j;  // the only window within delta of the maximum
                             } else if (!s.overflow) {
                                 const double* D = D64 + bb * TH;
-                                double bw = -INFINITY;
-                                int bj = 0x7fffffff;
-                                for (int e = lane; e < s.nnear; e += 32) {
-                                    const int j = my_near[e];
-                                    const double w = window_weight_rolled(D, load_window(wp, j), l);
+                                double bw = -INFINITY, sw = -INFINITY;  // best and runner-up weight, with their windows
+                                int bj = 0x7fffffff, sj = 0x7fffffff;
+                                auto offer = [&](double w, int j) {
                                     if (w > bw || (w == bw && j < bj)) {
+                                        sw = bw;
+                                        sj = bj;
                                         bw = w;
                                         bj = j;
+                                    } else if (w > sw || (w == sw && j < sj)) {
+                                        sw = w;
+                                        sj = j;
                                     }
+                                };
+                                for (int e = lane; e < s.nnear; e += 32) {
+                                    const int j = my_near[e];
+                                    offer(window_weight_rolled(D, load_window(wp, j), l), j);
                                 }
 #pragma unroll
                                 for (int o = 16; o > 0; o >>= 1) {
-                                    const double ow = __shfl_xor_sync(0xffffffffu, bw, o);
-                                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-                                    if (ow > bw || (ow == bw && oj < bj)) {
-                                        bw = ow;
-                                        bj = oj;
-                                    }
+                                    const double ow = __shfl_xor_sync(0xffffffffu, bw, o), osw = __shfl_xor_sync(0xffffffffu, sw, o);
+                                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o), osj = __shfl_xor_sync(0xffffffffu, sj, o);
+                                    offer(ow, oj);
+                                    offer(osw, osj);
                                 }
                                 arg = bj;
+                                // Two DIFFERENT l-mers whose weights lie closer than this kernel's theta can tell apart: the
+                                // comparison above is exact for the theta at hand, but theta carries the FP32 error of the
+                                // M-step sums (measured |d theta| <= 3.4e-7; typically ~1e-6 in a window weight), so which
+                                // window wins in the reference (refine.hpp:165-186, :311-316) is decided by the FP64 kernel.
+                                // (The same l-mer twice has bit-identical weights everywhere: the smaller offset wins, as
+                                // above.)  Not for large sets: an FP64 refinement of 10^7 windows takes seconds per bucket.
+                                if (!big && p.flag_exact != nullptr && lane == 0 && (bb == 0 || live1) && sj != 0x7fffffff &&
+                                    bw - sw <= 2e-6 + 1e-7 * fabs(bw) &&
+                                    ((load_window(wp, bj) ^ load_window(wp, sj)) >> (64 - 2 * l)) != 0ULL)
+                                    p.flag_exact[ois[bb]] = 1;
                             } else {
                                 float bw = s.best_w;
                                 int bj = s.best_j;
@@ -707,6 +722,8 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                     }
                                 }
                                 arg = bj;
+                                // more near-maximum windows than the list holds: FP32 cannot order them
+                                if (!big && p.flag_exact != nullptr && lane == 0 && (bb == 0 || live1)) p.flag_exact[ois[bb]] = 1;
                             }
                             if (p.out_pos && lane == 0 && (bb == 0 || live1)) p.out_pos[static_cast<int64_t>(ois[bb]) * t + i] = arg + 1;
                             if (lane < l) {

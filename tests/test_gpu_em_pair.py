@@ -80,6 +80,38 @@ def test_tensor_core_kernel_agrees_with_pair_kernel(pm, golden, instance):
         assert abs(a["expectation"] - x["expectation"]) <= EXPECTATION_TOL
 
 
+def test_tensor_core_kernel_on_random_shapes(pm, best_oracle):
+    """The tensor-core kernel forced on (PM_B200_EM_TC=2) across its four operand widths (l = 5 ... 20 -> K = 32, 48,
+    64, 80), ragged sequence lengths (segments that end in the middle of a chunk, blocks of every size), 2 ... 40
+    sequences and iteration budgets 1 ... 8, against the reference: discrete outputs strictly equal -- whatever the
+    kernel cannot decide with margin it hands to the exact kernels -- and theta / expectation within tolerance.  The
+    exponent range of its single per-bucket reference (108 binades under the weight bound) is exercised by theta0's
+    floored columns: buckets of one or two members."""
+    from oracle import pmo
+    rng = np.random.default_rng(1605)
+    os.environ["PM_B200_EM_TC"] = "2"
+    try:
+        total = handed = 0
+        for l, t, iters in ((5, 7, 5), (8, 2, 3), (11, 13, 5), (12, 40, 2), (13, 9, 8), (16, 21, 1), (17, 5, 5), (20, 30, 4)):
+            ss = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(l + 30, 420)))) for _ in range(t)])
+            kept = best_oracle.sample_plan(l, min(l - 1, 6), 100 + l)
+            en = best_oracle.enriched(ss, l, kept, 1, 4 * t)
+            en = en[:: max(1, len(en) // 150)][:150]
+            with pm.Context(0) as c:
+                c.set_sequences(ss.bases, ss.offs)
+                got = c.refine(l, [e["members"] for e in en], max_iters=iters)
+                handed += c.em_exact_counts()["total"]
+            for e, a in zip(en, got):
+                w = best_oracle.refine(ss, l, e["members"], e["key"], max_iters=iters)
+                assert (a["consensus"], a["score"], a["positions"], a["iterations"]) == (w.consensus, w.score, w.positions, w.iterations), (l, t, iters)
+                assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL
+                assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+            total += len(en)
+        assert total > 800 and handed < total // 2  # most buckets were decided on the tensor cores
+    finally:
+        os.environ.pop("PM_B200_EM_TC", None)
+
+
 def test_long_motifs_use_the_wide_flush_path(ctx, best_oracle):
     """l > 16 means more than eight column pairs: 32-value class flushes, l = 31 fills the whole 64-bit window."""
     import numpy as np
