@@ -91,6 +91,33 @@ def test_run_matches_oracle_on_small_and_ragged_sets(ctx, best_oracle):
         assert_same_result(got, want)
 
 
+def test_run_matches_reference_on_random_sets_through_every_em_tier(pm, best_oracle):
+    """run() against the reference on random sets -- larger than the ones above, ragged, 2 ... 24 sequences, l = 7 ... 18,
+    thresholds that enrich hundreds of buckets per trial -- with the tensor-core kernel forced on for every batch
+    (PM_B200_EM_TC=2), with its default size rule, and with the pair kernel alone (0): best trial, source bucket,
+    positions, score, consensus, iterations and the enriched-bucket count are the reference's in all three."""
+    import os
+    rng = np.random.default_rng(424242)
+    cases = []
+    for round_ in range(8):
+        t = int(rng.integers(2, 25))
+        l = int(rng.integers(7, 19))
+        strings = ["".join(rng.choice(list("ACGT"), int(rng.integers(l + 40, 360)))) for _ in range(t)]
+        k = int(rng.integers(4, min(l - 1, 8) + 1))
+        cases.append((pmo.SeqSet.from_strings(strings), dict(l=l, d=2, k=k, s=int(rng.integers(1, 4)), m=4, seed=100 + round_, early_stop=0)))
+    for ss, kw in cases:
+        want = best_oracle.run(ss, **kw)
+        for mode in ("2", "1", "0"):
+            os.environ["PM_B200_EM_TC"] = mode
+            try:
+                with pm.Context(0) as c:
+                    c.set_sequences(ss.bases, ss.offs)
+                    got = c.run(**kw)
+            finally:
+                os.environ.pop("PM_B200_EM_TC", None)
+            assert_same_result(got, want)
+
+
 def test_results_do_not_depend_on_batching_backend_or_workers(ctx, instance):
     # test_driver.cpp:124-151 (workers x backends) plus the GPU build's own knob (batch size)
     ss, _, _ = instance(8, 60, 9, 2, 1234)
