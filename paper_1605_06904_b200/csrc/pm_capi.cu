@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <limits>
 #include <map>
 #include <mutex>
@@ -115,6 +116,19 @@ struct pm_ctx {
     std::vector<k::TileDesc> h_tiles;
     std::vector<int> h_zoff, h_group_off;
     std::vector<uint16_t> h_entries;
+    // The class-group index of a small set is built on a worker thread while the first kernels of the run are already
+    // queued (it is only needed by the pair kernel, which follows the tensor-core kernel): see finish_class_groups()
+    struct ClsResult {
+        int zcap = 0, wcap = 0;
+        int64_t live_slots = 0;
+        size_t live_rows = 0;
+        bool built = false;  // false: a single sequence exceeds the z buffer (streaming kernel)
+    };
+    std::future<ClsResult> cls_job;
+    bool cls_pending = false;
+    bool cls_hint_small = false;  // known before the build ends: every sequence fits a tile of a small set
+    std::string cls_bases;        // the worker's copy of the ASCII input
+    std::vector<int64_t> cls_rel, cls_word_off;
     std::vector<double> h_logw;
     // window index space for the current l
     int win_l = 0;
@@ -244,12 +258,10 @@ int d2h(pm_ctx* c, void* dst, const void* src, size_t bytes) {
 // position is grouped per class into rows of 32 slots with pairwise distinct addresses mod 32, so
 // the M-step gather is free of bank conflicts.  A layout table like word_off, not arithmetic of
 // the path; it depends on the sequence set only (not on l, the plan or the bucket).
-int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel,
-                       const std::vector<int64_t>& word_off, int t) {
-    const int64_t total = rel[static_cast<size_t>(t)];
+// z slots per tile: one tile up to ~13.5k slots (3 CTAs/SM); above that, balanced tiles of at most ~12.6k slots
+// (two tiles for the n=1000 configs: 4 CTAs/SM, measured +5 % over one 84 KB tile)
+int64_t class_tile_cap(int64_t total, int t) {
     const int64_t single = k::kZPad + total + 32 * static_cast<int64_t>(t);
-    // one tile up to ~13.5k slots (3 CTAs/SM); above that, balanced tiles of at most ~12.6k slots
-    // (two tiles for the n=1000 configs: 4 CTAs/SM, measured +5 % over one 84 KB tile)
     int64_t cap = single;
     if (single > 13500) {
         const int64_t nt = (single + 12599) / 12600;
@@ -259,6 +271,16 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         const long v = std::atol(env);
         if (v >= 256 && v <= 48000) cap = v;
     }
+    return cap;
+}
+
+// host part: fills c->h_tiles / h_zoff / h_group_off / h_entries (no CUDA call: may run on a worker thread)
+pm_ctx::ClsResult class_groups_cpu(pm_ctx* c, const char* bases, const std::vector<int64_t>& rel,
+                                   const std::vector<int64_t>& word_off, int t) {
+    pm_ctx::ClsResult res;
+    const int64_t total = rel[static_cast<size_t>(t)];
+    const int64_t single = k::kZPad + total + 32 * static_cast<int64_t>(t);
+    const int64_t cap = class_tile_cap(total, t);
     // Sequences per tile: at most kPairMaxSeqs (the pair kernel keeps a tile's metadata in shared memory), and for
     // multi-tile sets a multiple of the ten warps of a CTA when ten or more fit (warp per sequence: a tile of
     // twelve leaves eight warps idle for half of the E-step).
@@ -357,7 +379,7 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
             live_slots += n;
             ++i;
         }
-        if (i == tile.seq_begin) return PM_OK;  // a single sequence exceeds the z buffer: streaming kernel
+        if (i == tile.seq_begin) return res;  // a single sequence exceeds the z buffer: streaming kernel
         tile.seq_end = i;
         tile.zlen = static_cast<int>(cursor);
         tile.word_begin = word_off[static_cast<size_t>(tile.seq_begin)];
@@ -387,25 +409,49 @@ int build_class_groups(pm_ctx* c, const char* bases, const std::vector<int64_t>&
         }
         tiles.push_back(tile);
     }
-    const size_t live_rows = entries.size() / 32;
+    res.live_rows = entries.size() / 32;
     for (int r = 0; r < 2 * 32; ++r) entries.push_back(static_cast<uint16_t>(32 + (r & 31)));  // rows the gather's prefetch may touch
-    PM_TRY(ensure(c, &c->d_cls_entries, &c->cap_cls_entries, sizeof(uint16_t) * std::max<size_t>(entries.size(), 1)));
-    PM_TRY(ensure(c, &c->d_cls_group_off, &c->cap_cls_group_off, sizeof(int) * group_off.size()));
+    res.zcap = zcap;
+    res.wcap = wcap;
+    res.live_slots = live_slots;
+    res.built = true;
+    return res;
+}
+
+// device part: uploads the tables and publishes the geometry in the context
+int class_groups_upload(pm_ctx* c, const pm_ctx::ClsResult& res, int t) {
+    if (!res.built) return PM_OK;
+    const std::vector<k::TileDesc>& tiles = c->h_tiles;
+    PM_TRY(ensure(c, &c->d_cls_entries, &c->cap_cls_entries, sizeof(uint16_t) * std::max<size_t>(c->h_entries.size(), 1)));
+    PM_TRY(ensure(c, &c->d_cls_group_off, &c->cap_cls_group_off, sizeof(int) * c->h_group_off.size()));
     PM_TRY(ensure(c, &c->d_seq_zoff, &c->cap_seq_zoff, sizeof(int) * static_cast<size_t>(t)));
     PM_TRY(ensure(c, &c->d_tiles, &c->cap_tiles, sizeof(k::TileDesc) * tiles.size()));
-    PM_TRY(h2d(c, c->d_cls_entries, entries.data(), sizeof(uint16_t) * entries.size()));
-    PM_TRY(h2d(c, c->d_cls_group_off, group_off.data(), sizeof(int) * group_off.size()));
-    PM_TRY(h2d(c, c->d_seq_zoff, zoff.data(), sizeof(int) * zoff.size()));
+    PM_TRY(h2d(c, c->d_cls_entries, c->h_entries.data(), sizeof(uint16_t) * c->h_entries.size()));
+    PM_TRY(h2d(c, c->d_cls_group_off, c->h_group_off.data(), sizeof(int) * c->h_group_off.size()));
+    PM_TRY(h2d(c, c->d_seq_zoff, c->h_zoff.data(), sizeof(int) * c->h_zoff.size()));
     PM_TRY(h2d(c, c->d_tiles, tiles.data(), sizeof(k::TileDesc) * tiles.size()));
-    // no sync here: the staging vectors belong to the context and pm_ctx_set_sequences synchronises once at its end
-    c->zlen = zcap;
+    // no sync here: the staging vectors belong to the context; the next upload starts with a stream synchronisation
+    c->zlen = res.zcap;
     c->max_tile_seqs = 0;
     for (const k::TileDesc& td : tiles) c->max_tile_seqs = std::max(c->max_tile_seqs, td.seq_end - td.seq_begin);
-    c->tile_words = wcap;
+    c->tile_words = res.wcap;
     c->n_tiles = static_cast<int>(tiles.size());
-    c->total_groups = static_cast<int>(live_rows);
-    c->group_fill = live_rows == 0 ? 0.0 : static_cast<double>(live_slots) / static_cast<double>(live_rows * 32);
+    c->total_groups = static_cast<int>(res.live_rows);
+    c->group_fill = res.live_rows == 0 ? 0.0 : static_cast<double>(res.live_slots) / static_cast<double>(res.live_rows * 32);
     return PM_OK;
+}
+
+// joins the worker of the last upload, if any, and uploads its tables
+int finish_class_groups(pm_ctx* c) {
+    if (!c->cls_pending) return PM_OK;
+    c->cls_pending = false;
+    pm_ctx::ClsResult res;
+    try {
+        res = c->cls_job.get();
+    } catch (const std::exception& e) {
+        return set_error(PM_ERR_OUT_OF_MEMORY, std::string("class-group build failed: ") + e.what());
+    }
+    return class_groups_upload(c, res, static_cast<int>(c->h_zoff.size()));
 }
 
 // PM_B200_HOST_TIMING=1: wall-clock marks of the host side of pm_run on stderr (where the GPU may sit idle)
@@ -999,8 +1045,16 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
     c->tc_used = false;
     const k::WorkDesc* const work_all = work;  // the TC stage below narrows p.work to the buckets it flagged
 
-    const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs;
-    const bool pair_small = pair_ok && !(c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords);
+    // the class-group index may still be under construction on the worker thread (finish_class_groups): the tensor-core
+    // stage only needs to know that the set is a small one the pair kernel will accept, which the upload already knew
+    bool pair_small;
+    if (c->cls_pending && c->cls_hint_small) {
+        pair_small = true;
+    } else {
+        PM_TRY(finish_class_groups(c));
+        pair_small = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs &&
+                     !(c->t > k::kPairMaxSeqs || c->total_words > k::kPairMaxWords);
+    }
     // Tensor-core kernel (pm_em_tc.cuh): 128 buckets per CTA.  It decides every bucket whose discrete outputs are clear
     // of the FP32 error of its sums and flags the rest, which the pair kernel below then refines into the same slots.
     if (pair_small && em_tc_enabled(n_work_bound) && theta_in == nullptr && l <= k::kTcMaxL && c->t <= k::kTcMaxSeqs &&
@@ -1040,6 +1094,8 @@ int launch_em(pm_ctx* c, int l, int max_iters, double tol, double z_eps, const k
         }
     }
 
+    PM_TRY(finish_class_groups(c));
+    const bool pair_ok = c->zlen > 0 && c->max_seq_len < 65536 && c->max_tile_seqs <= k::kPairMaxSeqs;
     if (pair_ok) {
         // two buckets per CTA in lockstep (pm_em_pair.cuh).  Small sets keep all per-sequence state and the whole
         // packed set in shared memory; large sets walk the tiles with per-tile state (C5: 1,000 tiles of 10).
@@ -1193,6 +1249,12 @@ int pm_ctx_create(int device, void* stream, pm_ctx** out) {
 
 void pm_ctx_destroy(pm_ctx* c) {
     if (c == nullptr) return;
+    if (c->cls_pending) {
+        try {
+            c->cls_job.get();
+        } catch (const std::exception&) {
+        }
+    }
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf& b : c->buf) {
@@ -1226,6 +1288,13 @@ int load_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t, boo
     }
     PM_CUDA(cudaSetDevice(c->device));
     HostMarks up_marks;
+    if (c->cls_pending) {  // the previous set's index build: its staging vectors are about to be reused
+        c->cls_pending = false;
+        try {
+            c->cls_job.get();
+        } catch (const std::exception&) {
+        }
+    }
     PM_CUDA(cudaStreamSynchronize(c->stream));
     up_marks.mark("upload: sync");
     c->t = 0;
@@ -1280,7 +1349,25 @@ int load_sequences(pm_ctx* c, const char* bases, const int64_t* offs, int t, boo
                                                                  c->d_seq_sym, c->d_tot_sym, c->d_tot_sym + 4);
     PM_TRY(check_launch(c, "encode"));
     up_marks.mark("h2d+encode issued");
-    PM_TRY(build_class_groups(c, bases + base0, rel, word_off, t));  // host index build overlaps the encode kernel
+    // The class-group index (host arithmetic over every base, ~0.1 ms for 12,000 bases) is only needed by the pair kernel.
+    // Small sets build it on a worker thread -- from a copy of the input, the caller's buffer is free after this call --
+    // while this thread goes on to sample plans and launch the hashing and tensor-core kernels; launch_em() joins it.
+    {
+        const int64_t cap = class_tile_cap(total_bases, t);
+        int64_t longest = 0;
+        for (int i = 0; i < t; ++i) longest = std::max<int64_t>(longest, len[static_cast<size_t>(i)]);
+        c->cls_hint_small = t <= k::kPairMaxSeqs && total_words <= k::kPairMaxWords && longest < 65536 &&
+                            k::kZPad + 31 + longest <= cap;
+        if (c->cls_hint_small && total_bases <= (1 << 20) && std::getenv("PM_B200_SYNC_CLASS_GROUPS") == nullptr) {
+            c->cls_bases.assign(bases + base0, static_cast<size_t>(total_bases));
+            c->cls_rel = rel;
+            c->cls_word_off = word_off;
+            c->cls_job = std::async(std::launch::async, [c, t]() { return class_groups_cpu(c, c->cls_bases.data(), c->cls_rel, c->cls_word_off, t); });
+            c->cls_pending = true;
+        } else {
+            PM_TRY(class_groups_upload(c, class_groups_cpu(c, bases + base0, rel, word_off, t), t));
+        }
+    }
     up_marks.mark("class groups");
     unsigned long long host_tot[5];
     PM_TRY(d2h(c, host_tot, c->d_tot_sym, sizeof(host_tot)));
