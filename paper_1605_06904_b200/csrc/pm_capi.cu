@@ -64,7 +64,7 @@ enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
     S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
-    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE,
+    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE, S_POS_BEST, S_HAM,
     // the FP64 path has its own scratch: run() calls it while a batch's buffers are still live
     S_DRAWS, S_PLANT_OUT, S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
 };
@@ -124,6 +124,9 @@ struct pm_ctx {
         size_t live_rows = 0;
         bool built = false;  // false: a single sequence exceeds the z buffer (streaming kernel)
     };
+    // pinned host staging for the per-batch read-back (copies into pageable memory block the host for ~10 us each)
+    void* h_pin = nullptr;
+    size_t h_pin_cap = 0;
     std::future<ClsResult> cls_job;
     bool cls_pending = false;
     bool cls_hint_small = false;  // known before the build ends: every sequence fits a tile of a small set
@@ -239,6 +242,23 @@ void collect_stage_times(pm_ctx* c, double* stage_ms) {
         c->ev_pool.push_back(m.b);
     }
     c->marks.clear();
+}
+
+// pinned host memory of at least `bytes` (grow-only; the previous batch's contents are gone)
+int get_pinned(pm_ctx* c, size_t bytes, void** out) {
+    if (bytes > c->h_pin_cap) {
+        if (c->h_pin != nullptr) {
+            PM_CUDA(cudaStreamSynchronize(c->stream));
+            PM_CUDA(cudaFreeHost(c->h_pin));
+            c->h_pin = nullptr;
+            c->h_pin_cap = 0;
+        }
+        const size_t cap = std::max<size_t>(bytes + bytes / 2, 1 << 16);
+        PM_CUDA(cudaHostAlloc(&c->h_pin, cap, cudaHostAllocDefault));
+        c->h_pin_cap = cap;
+    }
+    *out = c->h_pin;
+    return PM_OK;
 }
 
 int h2d(pm_ctx* c, void* dst, const void* src, size_t bytes) {
@@ -1267,6 +1287,7 @@ void pm_ctx_destroy(pm_ctx* c) {
     cudaFree(c->d_tot_sym);
     cudaFree(c->d_win_off);
     cudaFree(c->d_seq_logw);
+    if (c->h_pin) cudaFreeHost(c->h_pin);
     cudaFree(c->d_cls_entries);
     cudaFree(c->d_cls_group_off);
     cudaFree(c->d_seq_zoff);
@@ -1946,6 +1967,55 @@ __global__ void summarize_kernel(const int32_t* __restrict__ best_work, const in
     out[tr] = s;
 }
 
+// Per trial of the batch, for its best bucket: the positions (gathered next to each other so that one copy brings the
+// winner's along with the summaries) and the XOR/popcount scan of its consensus over every window (sequence.hpp:28-38,
+// oracle.hpp:101-115: total distance and the number of sequences with an occurrence within d).  With these the host
+// needs no second round trip for the batch winner's positions and none for the final scoring of the reported motif.
+__global__ void __launch_bounds__(256) trial_epilogue_kernel(const int32_t* __restrict__ best_work, int n_trials, int t, int l, int d,
+                                                            const uint64_t* __restrict__ cons, const int32_t* __restrict__ pos,
+                                                            const uint64_t* __restrict__ words, const int64_t* __restrict__ word_off,
+                                                            const int32_t* __restrict__ seq_len, int32_t* __restrict__ pos_best,
+                                                            int32_t* __restrict__ ham) {
+    __shared__ int s_within, s_total;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint64_t digit_mask = (0x5555555555555555ULL >> (64 - 2 * l)) << (64 - 2 * l);
+    for (int tr = blockIdx.x; tr < n_trials; tr += gridDim.x) {
+        const int w = best_work[tr];
+        if (threadIdx.x == 0) {
+            s_within = 0;
+            s_total = 0;
+        }
+        __syncthreads();
+        if (w >= 0) {
+            if (pos_best != nullptr && pos != nullptr) {
+                for (int i = threadIdx.x; i < t; i += blockDim.x)
+                    pos_best[static_cast<int64_t>(tr) * t + i] = pos[static_cast<int64_t>(w) * t + i];
+            }
+            const uint64_t cand = cons[w];
+            for (int i = warp; i < t; i += nwarps) {
+                const uint64_t* wp = words + word_off[i];
+                const int W = seq_len[i] - l + 1;
+                int best = 64;
+                for (int j = lane; j < W; j += 32) {
+                    const uint64_t xr = k::load_window(wp, j) ^ cand;
+                    best = min(best, __popcll((xr | (xr >> 1)) & digit_mask));
+                }
+                best = __reduce_min_sync(0xffffffffu, best);
+                if (lane == 0) {
+                    atomicAdd(&s_total, best);
+                    if (best <= d) atomicAdd(&s_within, 1);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ham[2 * tr] = s_within;
+            ham[2 * tr + 1] = s_total;
+        }
+        __syncthreads();
+    }
+}
+
 struct RunState {
     bool have_best = false;
     TrialSummary best{};
@@ -1955,6 +2025,8 @@ struct RunState {
     bool best_exact = false;            // best.expct is the FP64 kernel's value
     int32_t best_in_batch = -1;         // work item of the incumbent if it belongs to the batch being reduced
     int64_t exact_refines = 0;          // FP64 re-refinements this run needed
+    bool ham_valid = false;             // within_d / total_distance of the incumbent came back with its batch
+    int32_t within_d = 0, total_distance = 0;
 };
 
 // FP64 expectation (and score) of one member list: pm_em_f64.cuh through the stage path
@@ -2207,15 +2279,44 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
                                                                       o.cons, n_trials, d_tb);
         PM_TRY(check_launch(c, "summarize"));
     }
+    // every trial's best bucket: positions side by side and the XOR/popcount scan of its consensus; everything the
+    // host needs from this batch comes back through one pinned staging area behind a single synchronisation
+    const bool epi_pos = all_positions && static_cast<size_t>(n_trials) * static_cast<size_t>(c->t) * sizeof(int32_t) <= (8u << 20);
+    auto up16 = [](size_t v) { return (v + 15) & ~static_cast<size_t>(15); };
+    const size_t off_tb = 0, off_nrec = up16(off_tb + sizeof(TrialSummary) * tb.size()),
+                 off_scal = up16(off_nrec + sizeof(unsigned int) * n_rec.size()), off_ham = up16(off_scal + sizeof(scal)),
+                 off_pos = up16(off_ham + sizeof(int32_t) * 2 * static_cast<size_t>(n_trials)),
+                 pin_bytes = off_pos + (epi_pos ? sizeof(int32_t) * static_cast<size_t>(n_trials) * static_cast<size_t>(c->t) : 0);
+    unsigned char* pin;
+    PM_TRY(get_pinned(c, pin_bytes, reinterpret_cast<void**>(&pin)));
+    const int32_t* ham = reinterpret_cast<const int32_t*>(pin + off_ham);
+    const int32_t* pos_best = reinterpret_cast<const int32_t*>(pin + off_pos);
     {
+        StageTimer ts5(c, prof, 5);
+        int32_t* d_pos_best = nullptr;
+        int32_t* d_ham;
+        if (epi_pos) PM_TRY(get_buf(c, S_POS_BEST, static_cast<size_t>(n_trials) * static_cast<size_t>(c->t), &d_pos_best));
+        PM_TRY(get_buf(c, S_HAM, static_cast<size_t>(n_trials) * 2, &d_ham));
+        trial_epilogue_kernel<<<static_cast<unsigned>(std::min(n_trials, 8 * c->sm_count)), 256, 0, c->stream>>>(
+            best_work, n_trials, c->t, l, cfg->d, o.cons, epi_pos ? o.pos : nullptr, c->d_words, c->d_word_off, c->d_seq_len,
+            d_pos_best, d_ham);
+        PM_TRY(check_launch(c, "trial_epilogue"));
+        ts5.stop();
         StageTimer td(c, prof, 7);
-        PM_TRY(d2h(c, tb.data(), d_tb, sizeof(TrialSummary) * tb.size()));
-        PM_TRY(d2h(c, n_rec.data(), rec.n_rec, sizeof(unsigned int) * n_rec.size()));
-        PM_TRY(d2h(c, scal, d_scal, sizeof(scal)));
+        if (epi_pos) PM_TRY(d2h(c, pin + off_pos, d_pos_best, sizeof(int32_t) * static_cast<size_t>(n_trials) * static_cast<size_t>(c->t)));
+        PM_TRY(d2h(c, pin + off_ham, d_ham, sizeof(int32_t) * 2 * static_cast<size_t>(n_trials)));
+        PM_TRY(d2h(c, pin + off_tb, d_tb, sizeof(TrialSummary) * tb.size()));
+        PM_TRY(d2h(c, pin + off_nrec, rec.n_rec, sizeof(unsigned int) * n_rec.size()));
+        PM_TRY(d2h(c, pin + off_scal, d_scal, sizeof(scal)));
         td.stop();
         PM_CUDA(cudaStreamSynchronize(c->stream));
+        std::memcpy(tb.data(), pin + off_tb, sizeof(TrialSummary) * tb.size());
+        std::memcpy(n_rec.data(), pin + off_nrec, sizeof(unsigned int) * n_rec.size());
+        std::memcpy(scal, pin + off_scal, sizeof(scal));
     }
     host_mark("gpu-wait");
+    std::vector<int32_t> tb_dev_work(static_cast<size_t>(n_trials));
+    for (int i = 0; i < n_trials; ++i) tb_dev_work[static_cast<size_t>(i)] = tb[static_cast<size_t>(i)].work;
     collect_stage_times(c, out->stage_ms);
 #ifdef PM_TC_TIMING
     std::fprintf(stderr, "[tc clocks, CTA 0 softmax thread] total %llu  wait S %llu  wait O %llu  updates %llu | EM passes %llu  MAX passes %llu  final %llu | sequence close %llu\n",
@@ -2327,6 +2428,9 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     // Ascending-trial reduction, driver.hpp:195-208.
     const int perfect = l * c->t;
     int32_t new_best_work = -1;
+    int new_best_trial_idx = -1;  // index within the batch
+    std::vector<int32_t> dev_work(static_cast<size_t>(n_trials));  // the device's choice per trial (the FP64 settlement above may have moved s.work)
+    for (int i = 0; i < n_trials; ++i) dev_work[static_cast<size_t>(i)] = tb_dev_work[static_cast<size_t>(i)];
     for (int i = 0; i < n_trials; ++i) {
         const int64_t trial = first_trial + i * trial_stride;
         TrialSummary& s = tb[static_cast<size_t>(i)];
@@ -2374,6 +2478,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
             st->best_exact = tb_exact[static_cast<size_t>(i)] != 0;
             st->best_in_batch = s.work;
             new_best_work = s.work;
+            new_best_trial_idx = i;
         }
         if (cfg->early_stop && st->have_best && st->best.score == perfect) {
             *stop = true;
@@ -2383,7 +2488,19 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     // a later batch may have to re-refine the incumbent in FP64: keep its member list (this batch's buffers are reused)
     if (more_batches && st->best_in_batch >= 0) PM_TRY(fetch_members(c, work, srt.idx, st->best_in_batch, &st->best_members, nullptr));
     st->best_in_batch = -1;
-    if (new_best_work >= 0 && all_positions) {
+    const bool epi_hit = new_best_work >= 0 && dev_work[static_cast<size_t>(new_best_trial_idx)] == new_best_work;
+    if (new_best_work >= 0) {
+        st->ham_valid = epi_hit;
+        if (epi_hit) {
+            st->within_d = ham[2 * static_cast<size_t>(new_best_trial_idx)];
+            st->total_distance = ham[2 * static_cast<size_t>(new_best_trial_idx) + 1];
+        }
+    }
+    if (epi_hit && epi_pos) {
+        // the winner's positions came back with the summaries
+        st->positions.assign(pos_best + static_cast<int64_t>(new_best_trial_idx) * c->t,
+                             pos_best + static_cast<int64_t>(new_best_trial_idx + 1) * c->t);
+    } else if (new_best_work >= 0 && all_positions) {
         st->positions.resize(static_cast<size_t>(c->t));
         PM_TRY(d2h(c, st->positions.data(), o.pos + static_cast<size_t>(new_best_work) * static_cast<size_t>(c->t),
                    sizeof(int32_t) * static_cast<size_t>(c->t)));
@@ -2547,8 +2664,8 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
     {
         // XOR/popcount scoring of the reported consensus (north_star "Scoring")
         StageTimer tsc(c, cfg->profile != 0, 5);
-        int tot = 0, within = 0;
-        PM_TRY(pm_hamming_scan(c, out->consensus, cfg->l, cfg->d, nullptr, &tot, &within));
+        int tot = st.total_distance, within = st.within_d;
+        if (!st.ham_valid) PM_TRY(pm_hamming_scan(c, out->consensus, cfg->l, cfg->d, nullptr, &tot, &within));
         out->total_distance = tot;
         out->within_d = within;
     }
