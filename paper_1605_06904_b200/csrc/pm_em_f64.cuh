@@ -13,7 +13,7 @@
 namespace pm {
 namespace k {
 
-constexpr int kF64Threads = 256;
+constexpr int kF64Threads = 640;  // 20 warps: one per sequence of the t = 20 configurations (a flagged bucket is a latency problem)
 constexpr int kF64LlSeqs = 512;  // per-sequence likelihood terms kept in shared memory (added in sequence order)
 
 struct F64Extra {
@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
             }
             __syncthreads();
 
-            // ---- E-step (refine.hpp:165-201): warp w takes the sequences w, w + 8, ... (the same assignment as the M-step
+            // ---- E-step (refine.hpp:165-201): warp w takes the sequences w, w + 20, ... (the same assignment as the M-step
             // below), lanes stride over the windows; maxima and sums are reduced with shuffles in a fixed shape.  No
-            // block-wide barrier per sequence (a flagged bucket of the (15,4) set: ~0.9 -> ~0.55 ms).
+            // block-wide barrier per sequence (a flagged bucket of the (15,4) set: ~0.9 -> ~0.35 ms with 20 warps).
             {
                 const int warp = tid >> 5, lane = tid & 31;
                 double ll_w = 0.0;
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
             }
             __syncthreads();
             // the likelihood: per-sequence terms added in sequence order like the reference (refine.hpp:165-201) -- every
-            // thread adds the same list; beyond kF64LlSeqs sequences the eight per-warp sums are added in warp order
+            // thread adds the same list; beyond kF64LlSeqs sequences the per-warp sums are added in warp order
             double ll = 0.0;
             if (!final_pass) {
                 const int n_terms = t <= kF64LlSeqs ? t : kF64Threads / 32;
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
             if (final_pass) break;
 
             // ---- M-step (refine.hpp:227-237): counts[c][r] = sum of z over the windows that show r at column c.
-            // Warp w takes the sequences i = w, w + 8, ...; lane = motif column, four accumulators (one per symbol);
-            // the eight per-warp partials are added in warp order: fixed shape, deterministic.
+            // Warp w takes the sequences i = w, w + 20, ...; lane = motif column, four accumulators (one per symbol);
+            // the per-warp partials are added in warp order: fixed shape, deterministic.
             __syncthreads();
             {
                 const int warp = tid >> 5, lane = tid & 31;
