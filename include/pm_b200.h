@@ -169,6 +169,10 @@ int pm_ctx_set_sequences(pm_ctx* ctx, const char* bases, const int64_t* offs, in
  * draw) is refused with PM_ERR_UNSUPPORTED rather than generated differently. */
 int pm_ctx_generate_planted(pm_ctx* ctx, int t, int n, int l, int d, uint64_t seed, char* bases_out, char* motif,
                             int32_t* positions);
+/* Plans of trials first_trial, first_trial + stride, ... (n of them) sampled ON THE DEVICE from the reference's PRNG
+ * stream (driver.hpp:164-165, projection.hpp:210-226, rng.hpp:13-73): what pm_run uses for seed-derived plans of sets
+ * that take the one-CTA bucketing.  kept: n x k kept positions (1-based, ascending), identical to pm_trial_plan. */
+int pm_ctx_trial_plans(pm_ctx* ctx, int l, int k, uint64_t master, int64_t first_trial, int64_t stride, int n, int32_t* kept);
 int pm_ctx_num_sequences(const pm_ctx* ctx);
 int64_t pm_ctx_total_lmers(const pm_ctx* ctx, int l);               /* sequence.hpp:113-120; <0 if some n_i < l */
 int pm_ctx_packed_words(pm_ctx* ctx, uint64_t* words_out, int64_t* word_off_out /* t+1 */, int64_t cap_words);

@@ -20,7 +20,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("PM_B200_LIB") or os.path.join(PKG_DIR, "libpm_b200.so")  # override: instrumented builds
 CSRC = os.path.join(PKG_DIR, "csrc")
 SOURCES = ["pm_capi.cu", "pm_host.cpp"]
-HEADERS = ["pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_em_tc.cuh", "pm_em_f64.cuh", "pm_planted.cuh", "pm_hash_fused.cuh", "pm_hash_count.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
+HEADERS = ["pm_plans.cuh", "pm_kernels.cuh", "pm_em_smem.cuh", "pm_em_pair.cuh", "pm_em_tc.cuh", "pm_em_f64.cuh", "pm_planted.cuh", "pm_hash_fused.cuh", "pm_hash_count.cuh", "pm_internal.hpp", os.path.join(REPO_DIR, "include", "pm_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -108,7 +108,7 @@ EXPORTS = [
     "pm_sample_plan_stream", "pm_trial_plan", "pm_validate_plan", "pm_generate_planted", "pm_optimal_k", "pm_p_hat", "pm_binomial_lt", "pm_trials_for_tail",
     "pm_num_trials", "pm_bucket_threshold_for_windows", "pm_resolve_params", "pm_candidate_improves",
     "pm_merge_results", "pm_ctx_create", "pm_ctx_destroy", "pm_ctx_set_sequences", "pm_ctx_generate_planted", "pm_ctx_num_sequences",
-    "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
+    "pm_ctx_trial_plans", "pm_ctx_total_lmers", "pm_ctx_packed_words", "pm_ctx_symbol_counts", "pm_ctx_synchronize",
     "pm_ctx_launch_count", "pm_ctx_em_exact_counts", "pm_hash_keys", "pm_hash_trial", "pm_enriched_buckets", "pm_refine", "pm_refine_exact",
     "pm_init_model", "pm_em_step", "pm_em_step_exact", "pm_expectation", "pm_score",
     "pm_hamming_scan", "pm_median_string", "pm_run", "pm_run_host", "pm_run_multi",
@@ -372,6 +372,13 @@ class Context:
         return dict(zip(("total", "likelihood_gain", "range", "argmax_tie", "non_finite", "fp64"), out.tolist()))
 
     # ---- stages
+    def trial_plans_device(self, l, k, seed, first_trial, n, stride=1):
+        """Plans of n trials sampled on the device (pm_ctx_trial_plans): n x k kept positions."""
+        kept = np.zeros((n, k), dtype=np.int32)
+        _check(lib().pm_ctx_trial_plans(self._h, l, k, C.c_uint64(seed), C.c_int64(first_trial), C.c_int64(stride), n,
+                                         _p(kept, C.c_int32)))
+        return kept
+
     def hash_keys(self, l, kept):
         k = _i32(kept)
         x = max(self.total_lmers(l), 1)

@@ -34,6 +34,7 @@
 #include "pm_planted.cuh"
 #include "pm_hash_fused.cuh"
 #include "pm_hash_count.cuh"
+#include "pm_plans.cuh"
 
 using namespace pm;
 
@@ -64,7 +65,7 @@ enum Slot {
     S_KEYS_A, S_KEYS_B, S_IDX_A, S_IDX_B, S_COUNTS, S_REC_KEY, S_REC_START, S_REC_SIZE, S_NREC, S_WORK_OFF,
     S_WORK, S_OUT_SCORE, S_OUT_ITERS, S_OUT_EXP, S_OUT_CONS, S_OUT_POS, S_OUT_THETA, S_OUT_LL, S_BEST, S_TB,
     S_SCAL, S_MEMBERS, S_MPREV, S_DIGIT_TOT, S_ETILES, S_TMP_A, S_TMP_B, S_TMP_C, S_TMP_D, S_ASCII, S_OFFS,
-    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE, S_POS_BEST, S_HAM,
+    S_TC_BLOCKS, S_TC_FLAG, S_TC_WORK, S_TC_MAP, S_F64_Z, S_F64_FLAG, S_F64_WORK, S_F64_MAP, S_THETA_IN, S_NCLOSE, S_POS_BEST, S_HAM, S_PLANS, S_PLAN_KEPT,
     // the FP64 path has its own scratch: run() calls it while a batch's buffers are still live
     S_DRAWS, S_PLANT_OUT, S_X_MEMBERS, S_X_WORK, S_X_SCAL, S_X_SCORE, S_X_ITERS, S_X_EXP, S_X_CONS, S_X_POS, S_X_THETA, S_X_LL, S_X_THETA_IN, S_COUNT_
 };
@@ -2066,8 +2067,21 @@ bool fused_hash_applies(const pm_ctx* c, int keybits, int64_t cap_e) {
 }
 
 // hash_trial + enriched_buckets of every trial of the batch, one CTA per trial (pm_hash_fused.cuh)
+// plans of trials first, first + stride, ... sampled on the device (pm_plans.cuh) into S_PLANS; *fail (device) is
+// raised when a trial needed more PRNG outputs than the sampler holds
+int sample_plans_on_device(pm_ctx* c, int l, int kk, uint64_t master, int64_t first, int64_t stride, int n, k::PlanProg** d_progs,
+                           int32_t* d_kept, unsigned int** d_fail) {
+    unsigned char* raw;
+    PM_TRY(get_buf(c, S_PLANS, sizeof(k::PlanProg) * static_cast<size_t>(n) + 16, &raw));
+    *d_fail = reinterpret_cast<unsigned int*>(raw);
+    *d_progs = reinterpret_cast<k::PlanProg*>(raw + 16);
+    PM_CUDA(cudaMemsetAsync(*d_fail, 0, sizeof(unsigned int), c->stream));
+    k::plan_sample_kernel<<<(n + 63) / 64, 64, 0, c->stream>>>(master, first, stride, n, l, kk, *d_progs, d_kept, *d_fail);
+    return check_launch(c, "plan_sample");
+}
+
 int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keybits, int thr, unsigned int* members,
-                      Records* r) {
+                      Records* r, const k::PlanProg* d_progs = nullptr) {
     r->cap_e = std::max<int64_t>(1, c->x / thr);
     const int n = static_cast<int>(progs.size());
     const size_t nrec = static_cast<size_t>(n) * static_cast<size_t>(r->cap_e);
@@ -2094,10 +2108,15 @@ int fused_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
     p.n_rec = r->n_rec;
     for (int base = 0; base < n; base += k::kMaxConstPlans) {
         const int cnt = std::min(k::kMaxConstPlans, n - base);
-        c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
+        if (d_progs == nullptr) c->h2d_bytes += static_cast<int64_t>(sizeof(k::PlanProg)) * cnt;
         ConstPlansUse plans_use(c->device, c->stream);
-        PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
-                                        0, cudaMemcpyHostToDevice, c->stream));
+        if (d_progs != nullptr) {
+            PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, d_progs + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt), 0,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            PM_CUDA(cudaMemcpyToSymbolAsync(k::c_plans, progs.data() + base, sizeof(k::PlanProg) * static_cast<size_t>(cnt),
+                                            0, cudaMemcpyHostToDevice, c->stream));
+        }
         p.plan_base = base;
         p.n_trials = cnt;
         const unsigned grid = static_cast<unsigned>(std::min(cnt, 2 * c->sm_count));
@@ -2190,11 +2209,13 @@ int count_hash_bucket(pm_ctx* c, const std::vector<k::PlanProg>& progs, int keyb
     return PM_OK;
 }
 
+constexpr int kRetryWithHostPlans = -77;  // internal to pm_run / run_batch
+
 template <typename KeyT>
 int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, const std::vector<k::PlanProg>& progs,
               int64_t first_trial, pm_run_result* out, RunState* st, bool* stop, int64_t* trial_buckets,
               int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key, int64_t out_base,
-              bool more_batches, int64_t trial_stride) {
+              bool more_batches, int64_t trial_stride, bool device_plans) {
     const int n_trials = static_cast<int>(progs.size());
     st->best_in_batch = -1;
     const int l = cfg->l;
@@ -2203,10 +2224,15 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     Sorted<KeyT> srt;
     Records rec;
     const bool fused = fused_hash_applies(c, 2 * params.k, std::max<int64_t>(1, c->x / params.s));
+    unsigned int* d_plan_fail = nullptr;
+    if (device_plans && !fused) return set_error(PM_ERR_CUDA, "internal: device plans without the one-CTA bucketing");
     if (fused) {
         StageTimer tk(c, prof, 0);
         PM_TRY(get_buf(c, S_IDX_A, progs.size() * static_cast<size_t>(c->x), &srt.idx));
-        PM_TRY(fused_hash_bucket(c, progs, 2 * params.k, params.s, srt.idx, &rec));
+        k::PlanProg* d_progs = nullptr;
+        if (device_plans)  // the reference's PRNG stream, one thread per trial (pm_plans.cuh): nothing to sample or upload here
+            PM_TRY(sample_plans_on_device(c, l, params.k, cfg->seed, first_trial, trial_stride, n_trials, &d_progs, nullptr, &d_plan_fail));
+        PM_TRY(fused_hash_bucket(c, progs, 2 * params.k, params.s, srt.idx, &rec, d_progs));
     }
     bool counted = false;
     if (!fused && count_hash_applies(c, 2 * params.k, params.s)) {
@@ -2285,7 +2311,7 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     auto up16 = [](size_t v) { return (v + 15) & ~static_cast<size_t>(15); };
     const size_t off_tb = 0, off_nrec = up16(off_tb + sizeof(TrialSummary) * tb.size()),
                  off_scal = up16(off_nrec + sizeof(unsigned int) * n_rec.size()), off_ham = up16(off_scal + sizeof(scal)),
-                 off_pos = up16(off_ham + sizeof(int32_t) * 2 * static_cast<size_t>(n_trials)),
+                 off_fail = up16(off_ham + sizeof(int32_t) * 2 * static_cast<size_t>(n_trials)), off_pos = up16(off_fail + 16),
                  pin_bytes = off_pos + (epi_pos ? sizeof(int32_t) * static_cast<size_t>(n_trials) * static_cast<size_t>(c->t) : 0);
     unsigned char* pin;
     PM_TRY(get_pinned(c, pin_bytes, reinterpret_cast<void**>(&pin)));
@@ -2308,8 +2334,12 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         PM_TRY(d2h(c, pin + off_tb, d_tb, sizeof(TrialSummary) * tb.size()));
         PM_TRY(d2h(c, pin + off_nrec, rec.n_rec, sizeof(unsigned int) * n_rec.size()));
         PM_TRY(d2h(c, pin + off_scal, d_scal, sizeof(scal)));
+        if (d_plan_fail != nullptr) PM_TRY(d2h(c, pin + off_fail, d_plan_fail, sizeof(unsigned int)));
         td.stop();
         PM_CUDA(cudaStreamSynchronize(c->stream));
+        // a trial needed more PRNG outputs than the device sampler holds (probability ~1e-17 per trial): nothing of this
+        // batch has been consumed yet, the caller samples its plans on the host and runs it again
+        if (d_plan_fail != nullptr && *reinterpret_cast<const unsigned int*>(pin + off_fail) != 0) return kRetryWithHostPlans;
         std::memcpy(tb.data(), pin + off_tb, sizeof(TrialSummary) * tb.size());
         std::memcpy(n_rec.data(), pin + off_nrec, sizeof(unsigned int) * n_rec.size());
         std::memcpy(scal, pin + off_scal, sizeof(scal));
@@ -2530,6 +2560,25 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
 
 extern "C" {
 
+int pm_ctx_trial_plans(pm_ctx* c, int l, int k, uint64_t master, int64_t first_trial, int64_t stride, int n, int32_t* kept) {
+    clear_error();
+    if (c == nullptr || kept == nullptr) return set_error(PM_ERR_INVALID_PARAMS, "null argument");
+    if (l < 1 || l > 31 || k < 1 || k > l || n < 1 || stride < 1 || first_trial < 1)
+        return set_error(PM_ERR_INVALID_PARAMS, "device plans need 1 <= k <= l <= 31, n >= 1, stride >= 1, first_trial >= 1");
+    PM_CUDA(cudaSetDevice(c->device));
+    int32_t* d_kept;
+    PM_TRY(get_buf(c, S_PLAN_KEPT, static_cast<size_t>(n) * static_cast<size_t>(k), &d_kept));
+    k::PlanProg* d_progs;
+    unsigned int* d_fail;
+    PM_TRY(sample_plans_on_device(c, l, k, master, first_trial, stride, n, &d_progs, d_kept, &d_fail));
+    unsigned int fail = 0;
+    PM_TRY(d2h(c, kept, d_kept, sizeof(int32_t) * static_cast<size_t>(n) * static_cast<size_t>(k)));
+    PM_TRY(d2h(c, &fail, d_fail, sizeof(fail)));
+    PM_CUDA(cudaStreamSynchronize(c->stream));
+    if (fail != 0) return set_error(PM_ERR_UNSUPPORTED, "a trial needed more PRNG outputs than the device sampler holds");
+    return PM_OK;
+}
+
 int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* positions, int64_t* trial_buckets,
            int32_t* trial_best_score, double* trial_best_expectation, uint64_t* trial_best_key) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -2585,6 +2634,9 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         const int64_t n_plans = std::min(batch, n_mine - j0);
         std::vector<k::PlanProg> progs(static_cast<size_t>(n_plans));
         std::vector<int> plan_rc(static_cast<size_t>(n_plans), PM_OK);
+        // seed-derived plans of a set that takes the one-CTA bucketing are sampled on the device (pm_plans.cuh)
+        bool device_plans = cfg->forced_kept == nullptr && cfg->plans == nullptr && fused_hash_applies(c, 2 * params.k, cap_e) &&
+                            !(std::getenv("PM_B200_DEVICE_PLANS") != nullptr && std::atoi(std::getenv("PM_B200_DEVICE_PLANS")) == 0);
         auto make_range = [&](int64_t a, int64_t b) {
             if (cfg->forced_kept == nullptr && cfg->plans == nullptr && stride == 1) {
                 // the reference's stream, four trials' seed chains at a time (pm_host.cpp: trial_plans)
@@ -2615,6 +2667,7 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
         const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
         // ~0.3 us per plan (LazyMt64): threads only pay off for thousands of plans
         const int n_threads = static_cast<int>(std::min<int64_t>(std::min(8, hw), (n_plans + 1023) / 1024));
+        auto sample_on_host = [&]() {
         if (n_threads <= 1 || cfg->forced_kept != nullptr) {
             make_range(0, n_plans);
         } else {
@@ -2626,15 +2679,28 @@ int pm_run(pm_ctx* c, const pm_run_config* cfg, pm_run_result* out, int32_t* pos
             }
             for (std::thread& th : pool) th.join();
         }
+        };
+        if (!device_plans) sample_on_host();
         for (int rc_plan : plan_rc) {
             if (rc_plan != PM_OK) return set_error(rc_plan, "invalid projection plan for a trial");
         }
         host_mark("plans");
-        const int rc = key_bytes == 4
-                           ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride)
-                           : run_batch<uint64_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
-                                                 trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride);
+        auto run_it = [&]() {
+            return key_bytes == 4
+                       ? run_batch<uint32_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
+                                             trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride, device_plans)
+                       : run_batch<uint64_t>(c, cfg, params, progs, first, out, &st, &stop, trial_buckets, trial_best_score,
+                                             trial_best_expectation, trial_best_key, j0, j0 + n_plans < n_mine || cfg->exact_best != 0, stride, device_plans);
+        };
+        int rc = run_it();
+        if (rc == kRetryWithHostPlans) {
+            device_plans = false;
+            sample_on_host();
+            for (int rc_plan : plan_rc) {
+                if (rc_plan != PM_OK) return set_error(rc_plan, "invalid projection plan for a trial");
+            }
+            rc = run_it();
+        }
         if (rc != PM_OK) return rc;
     }
 

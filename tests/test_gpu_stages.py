@@ -232,6 +232,26 @@ def test_stage_exports_init_model_em_step_expectation(pm, ctx, golden, example, 
         assert e.value.kind == kind
 
 
+def test_trial_plans_sampled_on_the_device(pm, ctx):
+    """pm_run samples seed-derived plans on the device (csrc/pm_plans.cuh: splitmix64 seed, the first outputs of
+    mt19937_64 from its seeding chain, uniform_below with rejection, partial Fisher-Yates, sorted complement): the
+    same kept positions as the host's pm_trial_plan -- itself pinned to the reference's stream -- for every motif
+    length, k = 1 ... l, master seeds including 0 and 2^64-1, strided trials and trial numbers beyond 2^32."""
+    rng = np.random.default_rng(99)
+    cases = [(15, 7, 7, 1, 172, 1), (20, 7, 7, 1, 3421, 1), (31, 1, 0, 1, 40, 1), (31, 30, 2**64 - 1, 5, 33, 3),
+             (1, 1, 5, 1, 4, 1), (8, 8, 11, 2, 9, 1), (19, 6, 123456789, 2**33, 65, 7)]
+    for _ in range(12):
+        l = int(rng.integers(2, 32))
+        cases.append((l, int(rng.integers(1, l + 1)), int(rng.integers(0, 2**63)), int(rng.integers(1, 10**6)),
+                      int(rng.integers(1, 300)), int(rng.integers(1, 9))))
+    for l, k, seed, first, n, stride in cases:
+        got = ctx.trial_plans_device(l, k, seed, first, n, stride)
+        for i in (0, 1, n // 2, n - 1):
+            assert got[i].tolist() == pm.trial_plan(l, k, seed, first + i * stride), (l, k, seed, first, stride, i)
+        if n <= 200:
+            assert all(got[i].tolist() == pm.trial_plan(l, k, seed, first + i * stride) for i in range(n))
+
+
 def test_planted_instances_generated_on_the_device(pm, ctx, golden):
     """pm_ctx_generate_planted (planted.hpp:38-101 on the device): same bytes, motif and positions as the reference for
     every pinned instance, the set is loaded in the context, and a config-5-sized instance equals the host generator."""
