@@ -1943,50 +1943,79 @@ struct TrialSummary {  // device layout of S_TB: parallel arrays would need 6 co
 // kTieEps are re-refined in FP64 before they are compared (the reference compares doubles exactly, driver.hpp:131-133).
 constexpr double kTieEps = 5e-5;
 
-__global__ void summarize_kernel(const int32_t* __restrict__ best_work, const int32_t* __restrict__ n_close,
-                                 const k::WorkDesc* __restrict__ work, const int32_t* __restrict__ score,
-                                 const int32_t* __restrict__ iters, const double* __restrict__ expct,
-                                 const uint64_t* __restrict__ cons, int n_trials, TrialSummary* __restrict__ out) {
-    const int tr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (tr >= n_trials) return;
-    TrialSummary s;
-    s.work = best_work[tr];
-    s.n_close = n_close[tr];
-    if (s.work >= 0) {
-        s.score = score[s.work];
-        s.iters = iters[s.work];
-        s.expct = expct[s.work];
-        s.key = work[s.work].key;
-        s.cons = cons[s.work];
-    } else {
-        s.score = -1;
-        s.iters = 0;
-        s.expct = 0.0;
-        s.key = 0;
-        s.cons = 0;
-    }
-    out[tr] = s;
-}
-
-// Per trial of the batch, for its best bucket: the positions (gathered next to each other so that one copy brings the
-// winner's along with the summaries) and the XOR/popcount scan of its consensus over every window (sequence.hpp:28-38,
+// Per trial of the batch, one CTA: the trial's best bucket under candidate_improves (driver.hpp:127-135, :169-175:
+// lexicographic (score, expectation, smaller key) -- a strict total order within a trial, keys are unique), the number
+// of other buckets FP32 cannot separate from it, its summary record, its positions (gathered next to each other so that
+// one copy brings the winner's along) and the XOR/popcount scan of its consensus over every window (sequence.hpp:28-38,
 // oracle.hpp:101-115: total distance and the number of sequences with an occurrence within d).  With these the host
-// needs no second round trip for the batch winner's positions and none for the final scoring of the reported motif.
-__global__ void __launch_bounds__(256) trial_epilogue_kernel(const int32_t* __restrict__ best_work, int n_trials, int t, int l, int d,
-                                                            const uint64_t* __restrict__ cons, const int32_t* __restrict__ pos,
-                                                            const uint64_t* __restrict__ words, const int64_t* __restrict__ word_off,
-                                                            const int32_t* __restrict__ seq_len, int32_t* __restrict__ pos_best,
-                                                            int32_t* __restrict__ ham) {
-    __shared__ int s_within, s_total;
+// needs one read-back per batch and no second round trip for the winner's positions or the final scoring.
+__global__ void __launch_bounds__(256) trial_reduce_kernel(const unsigned int* __restrict__ work_off, const k::WorkDesc* __restrict__ work,
+                                                          const int32_t* __restrict__ score, const int32_t* __restrict__ iters,
+                                                          const double* __restrict__ expct, const uint64_t* __restrict__ cons,
+                                                          const int32_t* __restrict__ pos, int n_trials, int t, int l, int d,
+                                                          double tie_eps, const uint64_t* __restrict__ words,
+                                                          const int64_t* __restrict__ word_off, const int32_t* __restrict__ seq_len,
+                                                          int32_t* __restrict__ best_work, TrialSummary* __restrict__ out,
+                                                          int32_t* __restrict__ pos_best, int32_t* __restrict__ ham) {
+    __shared__ int s_within, s_total, s_best;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const uint64_t digit_mask = (0x5555555555555555ULL >> (64 - 2 * l)) << (64 - 2 * l);
     for (int tr = blockIdx.x; tr < n_trials; tr += gridDim.x) {
-        const int w = best_work[tr];
         if (threadIdx.x == 0) {
             s_within = 0;
             s_total = 0;
         }
+        if (warp == 0) {
+            const unsigned int b = work_off[tr], e = work_off[tr + 1];
+            int bi = -1, bs = -1;
+            double be = 0.0;
+            uint64_t bk = 0;
+            for (unsigned int w = b + lane; w < e; w += 32) {
+                const int sc = score[w];
+                const double ex = expct[w];
+                const uint64_t key = work[w].key;
+                if (bi < 0 || k::better(sc, ex, key, bs, be, bk)) {
+                    bi = static_cast<int>(w);
+                    bs = sc;
+                    be = ex;
+                    bk = key;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const double oe = __shfl_xor_sync(0xffffffffu, be, o);
+                const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                if (oi >= 0 && (bi < 0 || k::better(os, oe, ok, bs, be, bk))) {
+                    bi = oi;
+                    bs = os;
+                    be = oe;
+                    bk = ok;
+                }
+            }
+            // candidates the FP32 expectation cannot separate from the best (driver.hpp:131-133 compares doubles exactly)
+            int close = 0;
+            for (unsigned int w = b + lane; w < e; w += 32) {
+                if (static_cast<int>(w) != bi && score[w] == bs && fabs(expct[w] - be) <= tie_eps) ++close;
+            }
+            close = __reduce_add_sync(0xffffffffu, close);
+            if (lane == 0) {
+                s_best = bi;
+                best_work[tr] = bi;
+                TrialSummary sm;
+                sm.work = bi;
+                sm.n_close = close;
+                sm.score = bi >= 0 ? bs : -1;
+                sm.iters = bi >= 0 ? iters[bi] : 0;
+                sm.expct = bi >= 0 ? be : 0.0;
+                sm.key = bi >= 0 ? bk : 0;
+                sm.cons = bi >= 0 ? cons[bi] : 0;
+                out[tr] = sm;
+            }
+        }
         __syncthreads();
+        const int w = s_best;
         if (w >= 0) {
             if (pos_best != nullptr && pos != nullptr) {
                 for (int i = threadIdx.x; i < t; i += blockDim.x)
@@ -2282,8 +2311,6 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     if (all_positions) PM_TRY(get_buf(c, S_OUT_POS, nb * static_cast<size_t>(c->t), &o.pos));
     PM_TRY(get_buf(c, S_SCAL, 16, &d_scal));
     PM_TRY(get_buf(c, S_BEST, static_cast<size_t>(n_trials), &best_work));
-    int32_t* n_close;
-    PM_TRY(get_buf(c, S_NCLOSE, static_cast<size_t>(n_trials), &n_close));
     PM_TRY(get_buf(c, S_TB, static_cast<size_t>(n_trials), &d_tb));
     PM_CUDA(cudaMemsetAsync(d_scal, 0, sizeof(unsigned long long) * 16, c->stream));
     {
@@ -2295,18 +2322,8 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     std::vector<TrialSummary> tb(static_cast<size_t>(n_trials));
     std::vector<unsigned int> n_rec(static_cast<size_t>(n_trials));
     unsigned long long scal[16] = {0};
-    {
-        StageTimer tr(c, prof, 4);
-        const int warps_per_block = 8;
-        k::trial_best_kernel<<<(n_trials + warps_per_block - 1) / warps_per_block, warps_per_block * 32, 0, c->stream>>>(
-            work_off, work, o.score, o.expct, n_trials, best_work, kTieEps, n_close);
-        PM_TRY(check_launch(c, "trial_best"));
-        summarize_kernel<<<(n_trials + 127) / 128, 128, 0, c->stream>>>(best_work, n_close, work, o.score, o.iters, o.expct,
-                                                                      o.cons, n_trials, d_tb);
-        PM_TRY(check_launch(c, "summarize"));
-    }
-    // every trial's best bucket: positions side by side and the XOR/popcount scan of its consensus; everything the
-    // host needs from this batch comes back through one pinned staging area behind a single synchronisation
+    // per-trial reduction (trial_reduce_kernel); everything the host needs from this batch comes back through one
+    // pinned staging area behind a single synchronisation
     const bool epi_pos = all_positions && static_cast<size_t>(n_trials) * static_cast<size_t>(c->t) * sizeof(int32_t) <= (8u << 20);
     auto up16 = [](size_t v) { return (v + 15) & ~static_cast<size_t>(15); };
     const size_t off_tb = 0, off_nrec = up16(off_tb + sizeof(TrialSummary) * tb.size()),
@@ -2318,16 +2335,16 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     const int32_t* ham = reinterpret_cast<const int32_t*>(pin + off_ham);
     const int32_t* pos_best = reinterpret_cast<const int32_t*>(pin + off_pos);
     {
-        StageTimer ts5(c, prof, 5);
+        StageTimer ts4(c, prof, 4);
         int32_t* d_pos_best = nullptr;
         int32_t* d_ham;
         if (epi_pos) PM_TRY(get_buf(c, S_POS_BEST, static_cast<size_t>(n_trials) * static_cast<size_t>(c->t), &d_pos_best));
         PM_TRY(get_buf(c, S_HAM, static_cast<size_t>(n_trials) * 2, &d_ham));
-        trial_epilogue_kernel<<<static_cast<unsigned>(std::min(n_trials, 8 * c->sm_count)), 256, 0, c->stream>>>(
-            best_work, n_trials, c->t, l, cfg->d, o.cons, epi_pos ? o.pos : nullptr, c->d_words, c->d_word_off, c->d_seq_len,
-            d_pos_best, d_ham);
-        PM_TRY(check_launch(c, "trial_epilogue"));
-        ts5.stop();
+        trial_reduce_kernel<<<static_cast<unsigned>(std::min(n_trials, 8 * c->sm_count)), 256, 0, c->stream>>>(
+            work_off, work, o.score, o.iters, o.expct, o.cons, epi_pos ? o.pos : nullptr, n_trials, c->t, l, cfg->d, kTieEps,
+            c->d_words, c->d_word_off, c->d_seq_len, best_work, d_tb, d_pos_best, d_ham);
+        PM_TRY(check_launch(c, "trial_reduce"));
+        ts4.stop();
         StageTimer td(c, prof, 7);
         if (epi_pos) PM_TRY(d2h(c, pin + off_pos, d_pos_best, sizeof(int32_t) * static_cast<size_t>(n_trials) * static_cast<size_t>(c->t)));
         PM_TRY(d2h(c, pin + off_ham, d_ham, sizeof(int32_t) * 2 * static_cast<size_t>(n_trials)));

@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
         for (int i = 0; i < t; ++i) sum_logw += p.seq_logw[i];
 
         unsigned int blk = 0, oq = 0, xq = 0;
-        long long ts_s = 0, ts_o = 0, ts_u = 0, ts_kind[3] = {0, 0, 0}, ts_close = 0;
-        const long long ts_begin = clock64();
+        [[maybe_unused]] long long ts_s = 0, ts_o = 0, ts_u = 0, ts_kind[3] = {0, 0, 0}, ts_close = 0;
+        [[maybe_unused]] const long long ts_begin = clock64();
         for (unsigned int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
             const unsigned int wi = tile * kTcRows + row;
             const bool live = wi < n_work;

@@ -6,7 +6,7 @@
 //   enrich_kernel          run detection + stream compaction of buckets of size >= s  (projection.hpp:359-372)
 //   work_scan / build_work exclusive scan of per-trial bucket counts -> EM work list
 //   em_refine_kernel       one CTA per enriched bucket: init_model, EM, argmax, score (refine.hpp:90-326, scoring.hpp:84-126)
-//   trial_best_kernel      per-trial best candidate                                   (driver.hpp:169-175, :127-135)
+//   (trial_reduce_kernel, the per-trial best candidate, lives in pm_capi.cu next to its record type)
 //   hamming_scan_kernel    XOR/popcount distance of a candidate to every window       (sequence.hpp:28-38, oracle.hpp:101-115)
 //   score_kernel           profile score / consensus of a start vector                (scoring.hpp:84-126)
 //
@@ -853,54 +853,6 @@ __device__ __forceinline__ bool better(int sa, double ea, uint64_t ka, int sb, d
     if (sa != sb) return sa > sb;
     if (ea != eb) return ea > eb;
     return ka < kb;
-}
-
-__global__ void trial_best_kernel(const unsigned int* __restrict__ work_off, const WorkDesc* __restrict__ work,
-                                  const int32_t* __restrict__ score, const double* __restrict__ expct, int n_trials,
-                                  int32_t* __restrict__ best_work /* -1 if the trial has no bucket */, double tie_eps,
-                                  int32_t* __restrict__ n_close /* other buckets of the trial with the best score and an
-                                                                   expectation within tie_eps of the best */) {
-    const int lane = threadIdx.x & 31;
-    const int tr = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (tr >= n_trials) return;
-    const unsigned int b = work_off[tr], e = work_off[tr + 1];
-    int bi = -1, bs = -1;
-    double be = 0.0;
-    uint64_t bk = 0;
-    for (unsigned int w = b + lane; w < e; w += 32) {
-        const int s = score[w];
-        const double ex = expct[w];
-        const uint64_t key = work[w].key;
-        if (bi < 0 || better(s, ex, key, bs, be, bk)) {
-            bi = static_cast<int>(w);
-            bs = s;
-            be = ex;
-            bk = key;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-        const double oe = __shfl_xor_sync(0xffffffffu, be, o);
-        const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        if (oi >= 0 && (bi < 0 || better(os, oe, ok, bs, be, bk))) {
-            bi = oi;
-            bs = os;
-            be = oe;
-            bk = ok;
-        }
-    }
-    // candidates the FP32 expectation cannot separate from the best (driver.hpp:131-133 compares doubles exactly)
-    int close = 0;
-    for (unsigned int w = b + lane; w < e; w += 32) {
-        if (static_cast<int>(w) != bi && score[w] == bs && fabs(expct[w] - be) <= tie_eps) ++close;
-    }
-    close = __reduce_add_sync(0xffffffffu, close);
-    if (lane == 0) {
-        best_work[tr] = bi;
-        n_close[tr] = close;
-    }
 }
 
 // ---------------------------------------------------------------------------------------------

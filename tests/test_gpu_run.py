@@ -118,6 +118,32 @@ def test_run_matches_reference_on_random_sets_through_every_em_tier(pm, best_ora
             assert_same_result(got, want)
 
 
+def test_back_to_back_uploads_and_runs(pm, best_oracle):
+    """The upload builds the pair kernel's class-group index on a worker thread and run() samples its plans on the
+    device, both while other work is in flight: a context that is re-loaded and run over and over (the end-to-end
+    loop of bench.py), re-loaded before it ever ran, re-loaded with a large set in between (synchronous index build),
+    and destroyed with the build still pending, must give the reference's result every time."""
+    rng = np.random.default_rng(5150)
+    sets = []
+    for _ in range(6):
+        t = int(rng.integers(3, 21))
+        sets.append(pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), int(rng.integers(60, 500)))) for _ in range(t)]))
+    kw = dict(l=9, d=1, k=5, s=2, m=6, seed=11, early_stop=0)
+    want = [best_oracle.run(ss, **kw) for ss in sets]
+    big = pmo.SeqSet.from_strings(["".join(rng.choice(list("ACGT"), 300)) for _ in range(90)])  # t > 64: large-set path
+    want_big = best_oracle.run(big, **dict(kw, m=2))
+    with pm.Context(0) as c:
+        for round_ in range(3):
+            for ss, w in zip(sets, want):
+                assert_same_result(c.run_host(ss.bases, ss.offs, **kw), w)
+            c.set_sequences(sets[0].bases, sets[0].offs)   # replaced before anything ran on it
+            c.set_sequences(big.bases, big.offs)
+            assert_same_result(c.run(**dict(kw, m=2)), want_big)
+    for ss in sets[:3]:
+        with pm.Context(0) as c:
+            c.set_sequences(ss.bases, ss.offs)             # destroyed with the index build possibly still running
+
+
 def test_results_do_not_depend_on_batching_backend_or_workers(ctx, instance):
     # test_driver.cpp:124-151 (workers x backends) plus the GPU build's own knob (batch size)
     ss, _, _ = instance(8, 60, 9, 2, 1234)
