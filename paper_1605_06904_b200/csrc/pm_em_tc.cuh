@@ -133,13 +133,13 @@ __device__ __forceinline__ uint32_t tc_pack_bf16(float e0, float e1) {
     return d;
 }
 
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* r) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
                    "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                  : "r"(taddr));
 }
-__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t* r) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
                  "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
                  "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
@@ -164,17 +164,16 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32])
 
 // ---- per-chunk work of a softmax thread: 16 columns (= 16 windows of one parity) of its row ------------------
 struct TcSeqState {
-    float2 sum2a, sum2b;  // partial sums of e (EM pass): four independent chains
     float mxa;            // final pass: running maximum of the weights
     float second;         // final pass: runner-up weight
     int best_j;           // final pass: window of the maximum
 };
 
-// EM pass: e = 2^(w - ref), running sum, e as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM
+// EM pass: e = 2^S, as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM.  S already is weight minus reference
+// (the reference is folded into the log-odds terms, see the model update) and the normaliser comes out of GEMM2
+// (fold_pending): per pair of columns 2 ex2, 1 conversion, 2 to widen hi again, 1 residual, 1 conversion.
 template <bool kMasked>
-__device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint32_t* __restrict__ o, int nvalid, float ref2,
-                                            TcSeqState& st) {
-    const float2 nref = make_float2(-ref2, -ref2);
+__device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint32_t* __restrict__ o, int nvalid) {
 #pragma unroll
     for (int k2 = 0; k2 < 16; k2 += 4) {
         float2 w0 = make_float2(__uint_as_float(r[k2]), __uint_as_float(r[k2 + 1]));
@@ -187,16 +186,12 @@ __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint
                 o[8 + (k2 >> 1) + 1] = 0u;
                 continue;
             }
-            if (k2 >= nvalid) w0.x = -INFINITY;
             if (k2 + 1 >= nvalid) w0.y = -INFINITY;
             if (k2 + 2 >= nvalid) w1.x = -INFINITY;
             if (k2 + 3 >= nvalid) w1.y = -INFINITY;
         }
-        const float2 a0 = f2_add(w0, nref), a1 = f2_add(w1, nref);
-        const float2 e0 = make_float2(fast_ex2(a0.x), fast_ex2(a0.y));  // 2^-inf = 0 for masked columns
-        const float2 e1 = make_float2(fast_ex2(a1.x), fast_ex2(a1.y));
-        st.sum2a = f2_add(st.sum2a, e0);
-        st.sum2b = f2_add(st.sum2b, e1);
+        const float2 e0 = make_float2(fast_ex2(w0.x), fast_ex2(w0.y));  // 2^-inf = 0 for masked columns
+        const float2 e1 = make_float2(fast_ex2(w1.x), fast_ex2(w1.y));
         const uint32_t h0 = tc_pack_bf16(e0.x, e0.y), h1 = tc_pack_bf16(e1.x, e1.y);
         const float2 hf0 = make_float2(__uint_as_float(h0 << 16), __uint_as_float(h0 & 0xFFFF0000u));
         const float2 hf1 = make_float2(__uint_as_float(h1 << 16), __uint_as_float(h1 & 0xFFFF0000u));
@@ -555,7 +550,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
             const WorkDesc wd = live ? p.work[wi] : WorkDesc{0, 0, 0, 0};
             float acc[4 * HP];       // my columns' expected counts (EM sweeps) / theta0 counts
             unsigned flags = 0;
-            float ref2 = 0.f;  // reference of the current pass's exponentials (log2 units)
+            double ref_eff = 0.0;  // reference of the current pass's exponentials (log2 units), as GEMM1 subtracts it
             double prev_ll = 0.0, expct = 0.0;
             double lbg[4];           // natural logs of the current background column
 
@@ -629,10 +624,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         }
                     }
                     // per column: write_column (refine.hpp:256-269), expectation = sum_c max_r theta[r][c]
-                    // (refine.hpp:130-136) and the log-odds D[c][r] = log2 max(theta,1e-9) - log2 max(bg,1e-9) as three
-                    // bf16 terms.  FP32 throughout: the counts are FP32 sums; log2f is accurate to 1 ulp (2e-6 at |D| = 20).
+                    // (refine.hpp:130-136) and the log-odds D[c][r] = log2 max(theta,1e-9) - log2 max(bg,1e-9).  FP32
+                    // throughout: the counts are FP32 sums; log2f is accurate to 1 ulp (2e-6 at |D| = 20).
                     float ex_part = 0.f, ub_part = 0.f;
-                    uint32_t dcol[3][2 * HP];
+                    float dval[4 * HP];
                     float lbg2[4];
 #pragma unroll
                     for (int r = 0; r < 4; ++r) lbg2[r] = static_cast<float>(lbg[r] * 1.4426950408889634);
@@ -656,20 +651,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
 #pragma unroll
                             for (int r = 0; r < 4; ++r) v[r] = acc[4 * c + r];
                         }
-                        float d2[4];
                         float mx = 0.f;
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             mx = fmaxf(mx, v[r]);
-                            d2[r] = col_live ? log2f(fmaxf(v[r], 1e-9f)) - lbg2[r] : 0.f;
+                            dval[4 * c + r] = col_live ? log2f(fmaxf(v[r], 1e-9f)) - lbg2[r] : 0.f;
                             if (p.out_theta && live && col_live && final_sweep)
                                 p.out_theta[static_cast<int64_t>(wi) * 4 * (l + 1) + r * (l + 1) + (c_lo + c + 1)] = static_cast<double>(v[r]);
                         }
                         if (col_live) ex_part += mx;
-                        ub_part += fmaxf(fmaxf(d2[0], d2[1]), fmaxf(d2[2], d2[3]));  // dead columns: all zero
+                        ub_part += fmaxf(fmaxf(dval[4 * c], dval[4 * c + 1]), fmaxf(dval[4 * c + 2], dval[4 * c + 3]));  // dead columns: all zero
+                    }
+                    // expectation and the weight bound: partner exchange
+                    xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = make_float4(ex_part, ub_part, 0.f, 0.f);
+                    tc_named_sync();
+                    float qref;  // what every live column gives up so that GEMM1 delivers weight minus reference
+                    {
+                        const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
+                        ++xq;
+                        expct = wg == 0 ? static_cast<double>(ex_part) + static_cast<double>(oth.x) : static_cast<double>(oth.x) + static_cast<double>(ex_part);
+                        const float ub = wg == 0 ? ub_part + oth.y : oth.y + ub_part;  // same value in both partners
+                        // The reference of this pass's exponentials, kTcRefBelow under the bound, is folded into the
+                        // log-odds: every window has exactly l live columns, so taking ref / l off every entry makes
+                        // GEMM1 produce weight - ref itself (one subtraction per element less in the sweep).  The final
+                        // E-step only compares weights: the shift does not matter there.
+                        qref = (ub - kTcRefBelow) / static_cast<float>(l);
+                        ref_eff = static_cast<double>(l) * static_cast<double>(qref);
+                    }
+                    // three bf16 terms (hi + mid + lo = 24 significant bits) of D - ref / l
+                    uint32_t dcol[3][2 * HP];
+#pragma unroll
+                    for (int c = 0; c < HP; ++c) {
+                        const bool col_live = c_lo + c < l;
                         uint32_t h[4], m[4], lw[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) tc_split3(d2[r], h[r], m[r], lw[r]);
+                        for (int r = 0; r < 4; ++r) tc_split3(col_live ? dval[4 * c + r] - qref : 0.f, h[r], m[r], lw[r]);
                         dcol[0][2 * c] = h[0] | (h[1] << 16);
                         dcol[0][2 * c + 1] = h[2] | (h[3] << 16);
                         dcol[1][2 * c] = m[0] | (m[1] << 16);
@@ -683,16 +699,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         for (int q = 0; q < 2 * HP; q += 4) tc_st4(tD + term * 2 * KC + 2 * c_lo + q, &dcol[term][q]);
                     }
                     tc_wait_st();
-                    // expectation and the weight bound: partner exchange
-                    xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = make_float4(ex_part, ub_part, 0.f, 0.f);
                     tc_fence_before();
-                    tc_named_sync();
-                    {
-                        const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
-                        ++xq;
-                        expct = wg == 0 ? static_cast<double>(ex_part) + static_cast<double>(oth.x) : static_cast<double>(oth.x) + static_cast<double>(ex_part);
-                        ref2 = (wg == 0 ? ub_part + oth.y : oth.y + ub_part) - kTcRefBelow;  // same value in both partners
-                    }
                     __syncwarp();
                     if (lane == 0) tc_mbar_arrive(&d_full[0]);
 #pragma unroll
@@ -705,10 +712,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                 const long long ts_pass0 = clock64();
 #endif
                 double ll = 0.0;
-                TcSeqState st = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), -INFINITY, -INFINITY, 0};
+                TcSeqState st = {-INFINITY, -INFINITY, 0};
                 bool pending = false;   // the previous sequence's O block has not been folded into acc yet
-                float pend_inv = 0.f;
                 unsigned int pend_oq = 0;
+                // Folds the counts of the sequence whose GEMM2 has finished into acc.  Its normaliser needs no sum in the
+                // softmax threads: every window has a base under motif column 0, so the four symbol counts of that column
+                // add up to sum_j e_j = L -- read from the same accumulator (by both partners: four more columns), made of
+                // the very hi + lo terms the counts are made of, so the normalised counts of a column sum to one exactly.
                 auto fold_pending = [&]() {
                     {
                         TC_T0();
@@ -716,25 +726,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         TC_ACC(ts_o);
                     }
                     tc_fence_after();
-                    const uint32_t src = tO + (pend_oq & 1) * K + 4 * c_lo;
+                    const uint32_t base = tO + (pend_oq & 1) * K;
+                    const uint32_t src = base + 4 * c_lo;
+                    uint32_t r0[4];
+                    tc_ld4(base, r0);
+                    uint32_t r[4 * HP];
 #pragma unroll
                     for (int q = 0; q < 4 * HP; q += 16) {
                         if (q + 16 <= 4 * HP) {
-                            uint32_t r[16];
-                            tc_ld16(src + q, r);
-                            tc_wait_ld();
-#pragma unroll
-                            for (int e = 0; e < 16; ++e) acc[q + e] = fmaf(__uint_as_float(r[e]), pend_inv, acc[q + e]);
+                            tc_ld16(src + q, r + q);
                         } else {
 #pragma unroll
-                            for (int q4 = q; q4 < 4 * HP; q4 += 4) {
-                                uint32_t r[4];
-                                tc_ld4(src + q4, r);
-                                tc_wait_ld();
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) acc[q4 + e] = fmaf(__uint_as_float(r[e]), pend_inv, acc[q4 + e]);
-                            }
+                            for (int q4 = q; q4 < 4 * HP; q4 += 4) tc_ld4(src + q4, r + q4);
                         }
+                    }
+                    tc_wait_ld();
+                    const float L = (__uint_as_float(r0[0]) + __uint_as_float(r0[1])) + (__uint_as_float(r0[2]) + __uint_as_float(r0[3]));
+                    // below kTcMinSum the sequence's best window is more than ~208 under the bound: out of range
+                    if (!(L >= kTcMinSum) || !(L < INFINITY)) flags |= kTcFlagRange;
+                    const float inv = 1.f / L;
+#pragma unroll
+                    for (int e = 0; e < 4 * HP; ++e) acc[e] = fmaf(__uint_as_float(r[e]), inv, acc[e]);
+                    if (wg == 0) {
+                        // log2 L = exponent + log2(mantissa): the absolute error stays at 1e-7 whatever the scale
+                        const uint32_t lb = __float_as_uint(L);
+                        const float mant = __uint_as_float((lb & 0x007FFFFFu) | 0x3F800000u);
+                        const int ex = static_cast<int>(lb >> 23) - 127;
+                        ll += ((ref_eff + static_cast<double>(ex)) + static_cast<double>(log2f(mant))) * 0.6931471805599453;
                     }
                     tc_fence_before();
                     __syncwarp();
@@ -747,8 +765,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     const TcBlock B = blocks[n];
                     const int i = B.seq;
                     if (B.first) {
-                        st.sum2a = make_float2(0.f, 0.f);
-                        st.sum2b = make_float2(0.f, 0.f);
                         st.mxa = -INFINITY;
                         st.second = -INFINITY;
                         st.best_j = 0;
@@ -777,8 +793,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             tc_wait_ld();
                             if (em_pass) {
                                 uint32_t o[32];
-                                tc_em_chunk<false>(r, o, 16, ref2, st);
-                                tc_em_chunk<false>(r + 16, o + 16, 16, ref2, st);
+                                tc_em_chunk<false>(r, o, 16);
+                                tc_em_chunk<false>(r + 16, o + 16, 16);
                                 tc_st32(tB + cc, o);
                             } else {
                                 tc_final_chunk<false>(r, 16, j, st);
@@ -793,7 +809,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             tc_wait_ld();
                             if (em_pass) {
                                 uint32_t o[16];
-                                tc_em_chunk<true>(r, o, nv, ref2, st);
+                                tc_em_chunk<true>(r, o, nv);
                                 tc_st16(tB + cc, o);
                             } else {
                                 tc_final_chunk<true>(r, nv, j, st);
@@ -807,31 +823,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
 
                     if (pending) fold_pending();  // the previous sequence's counts: its GEMM2 finished long ago
 
-                    if (B.last) {
+                    if (B.last && em_pass) {
+                        // nothing to exchange: the normaliser comes out of GEMM2 (fold_pending)
+                        pend_oq = oq++;
+                        pending = true;
+                    } else if (B.last) {
                         TC_T0();
-                        // ---- close the sequence: both column halves -> maximum, normaliser, likelihood term
-                        float4 mine = make_float4((st.sum2a.x + st.sum2a.y) + (st.sum2b.x + st.sum2b.y), st.mxa, st.second,
-                                                  __int_as_float(final_sweep ? tc_final_window(st) : 0));
+                        // ---- close the sequence (final pass): both column halves -> maximum, its window, runner-up
+                        float4 mine = make_float4(0.f, st.mxa, st.second, __int_as_float(tc_final_window(st)));
                         xch[(xq & 1) * 2 * kTcRows + wg * kTcRows + row] = mine;
                         tc_named_sync();
                         const float4 oth = xch[(xq & 1) * 2 * kTcRows + (wg ^ 1) * kTcRows + row];
                         ++xq;
                         const float4 a4 = wg == 0 ? mine : oth, b4 = wg == 0 ? oth : mine;  // fixed order
-                        if (em_pass) {
-                            const float L = a4.x + b4.x;
-                            // below kTcMinSum the sequence's best window is more than ~208 under the bound: out of range
-                            if (!(L >= kTcMinSum) || !(L < INFINITY)) flags |= kTcFlagRange;
-                            pend_inv = 1.f / L;
-                            pend_oq = oq++;
-                            pending = true;
-                            if (wg == 0) {
-                                // log2 L = exponent + log2(mantissa): the absolute error stays at 1e-7 whatever the scale
-                                const uint32_t lb = __float_as_uint(L);
-                                const float mant = __uint_as_float((lb & 0x007FFFFFu) | 0x3F800000u);
-                                const int ex = static_cast<int>(lb >> 23) - 127;
-                                ll += ((static_cast<double>(ref2) + static_cast<double>(ex)) + static_cast<double>(log2f(mant))) * 0.6931471805599453;
-                            }
-                        } else if (wg == 0) {
+                        if (wg == 0) {
                             // argmax with margin: the runner-up must lie tie_delta below the maximum (ties go to the
                             // smallest offset in the reference, refine.hpp:311-316: decided by the exact kernel)
                             const float M = fmaxf(a4.y, b4.y);
@@ -839,7 +844,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                             const float sec = fmaxf(fmaxf(a4.z, b4.z), fminf(a4.y, b4.y));
                             const int bj = a4.y >= b4.y ? __float_as_int(a4.w) : __float_as_int(b4.w);
                             // the weights compared here carry their column number in the low mantissa bits
-                            const float delta2 = (x.tie_delta + 1e-5f * fabsf(M * kLn2)) * kLog2e + kTcFinalUlpMargin * fabsf(M);
+                            // and are weight minus reference; the relative part of the margin scales with the weight itself
+                            // (the accumulation error of GEMM1, ~1e-5 at these magnitudes, is far inside the absolute part)
+                            const float m_raw = M + static_cast<float>(ref_eff);
+                            const float delta2 = (x.tie_delta + 1e-5f * fabsf(m_raw * kLn2)) * kLog2e + kTcFinalUlpMargin * fabsf(M);
                             if (!(M - sec > delta2)) flags |= kTcFlagTie;
                             if (live && p.out_pos) p.out_pos[static_cast<int64_t>(wi) * t + i] = bj + 1;
                             // parked for the profile below
