@@ -171,7 +171,7 @@ struct TcSeqState {
 
 // EM pass: e = 2^S, as bf16 hi + lo pairs (8 + 8 words) for the M-step GEMM.  S already is weight minus reference
 // (the reference is folded into the log-odds terms, see the model update) and the normaliser comes out of GEMM2
-// (fold_pending): per pair of columns 2 ex2, 1 conversion, 2 to widen hi again, 1 residual, 1 conversion.
+// (fold_pending): per pair of columns 2 ex2, 1 byte permute + 2 masks for hi, 1 residual, 1 conversion for lo.
 template <bool kMasked>
 __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint32_t* __restrict__ o, int nvalid) {
 #pragma unroll
@@ -192,9 +192,12 @@ __device__ __forceinline__ void tc_em_chunk(const uint32_t* __restrict__ r, uint
         }
         const float2 e0 = make_float2(fast_ex2(w0.x), fast_ex2(w0.y));  // 2^-inf = 0 for masked columns
         const float2 e1 = make_float2(fast_ex2(w1.x), fast_ex2(w1.y));
-        const uint32_t h0 = tc_pack_bf16(e0.x, e0.y), h1 = tc_pack_bf16(e1.x, e1.y);
-        const float2 hf0 = make_float2(__uint_as_float(h0 << 16), __uint_as_float(h0 & 0xFFFF0000u));
-        const float2 hf1 = make_float2(__uint_as_float(h1 << 16), __uint_as_float(h1 & 0xFFFF0000u));
+        // hi = the upper 16 bits of e (a byte permute on the ALU pipe: the XU pipe, which the exponentials and the
+        // conversions share, is the scarce one), lo = bf16(e - hi): hi + lo carries 15-16 bits of e
+        const uint32_t h0 = __byte_perm(__float_as_uint(e0.x), __float_as_uint(e0.y), 0x7632);
+        const uint32_t h1 = __byte_perm(__float_as_uint(e1.x), __float_as_uint(e1.y), 0x7632);
+        const float2 hf0 = make_float2(__uint_as_float(__float_as_uint(e0.x) & 0xFFFF0000u), __uint_as_float(__float_as_uint(e0.y) & 0xFFFF0000u));
+        const float2 hf1 = make_float2(__uint_as_float(__float_as_uint(e1.x) & 0xFFFF0000u), __uint_as_float(__float_as_uint(e1.y) & 0xFFFF0000u));
         const float2 l0 = f2_fma(hf0, make_float2(-1.f, -1.f), e0);  // exact residuals
         const float2 l1 = f2_fma(hf1, make_float2(-1.f, -1.f), e1);
         o[k2 >> 1] = h0;
