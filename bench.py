@@ -69,6 +69,9 @@ def parse_args():
 # clocks: sampled with nvidia-smi DURING the timed region (B200_PROFILING.md recipe)
 # ------------------------------------------------------------------------------------------------
 class ClockSampler:
+    """nvidia-smi in loop mode, started BEFORE the warm-up (its first row takes ~100 ms) so that rows exist by the time
+    the timed region begins; only rows that arrived between mark_begin() and stop() are reported.  A C1 step is about a
+    millisecond, 20 of them with their L2 flushes ~50 ms: at one row per 10 ms that is a handful of samples."""
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -77,11 +80,12 @@ class ClockSampler:
         self.rows = []
         self.proc = None
         self.gpu_index = gpu_index
+        self.t_begin = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "25",
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits", "-lms", "10",
                  "-i", str(self.gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
@@ -89,9 +93,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
+
+    def mark_begin(self):
+        self.t_begin = time.perf_counter()
 
     def stop(self):
+        t_end = time.perf_counter()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -100,7 +108,9 @@ class ClockSampler:
                 self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        # a row describes the interval before it arrived: accept rows up to one period after the region's end
+        inside = [r for ts, r in self.rows if self.t_begin is None or (self.t_begin <= ts <= t_end + 0.02)]
+        for r in inside:
             if len(r) < 9:
                 continue
             try:
@@ -112,7 +122,7 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "rows_total": len(self.rows)}
 
 
 def measured_peaks():
@@ -339,10 +349,11 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         return per_step_ms, launches, stage, lookups, h2d, d2h, result, work, (tensor_flops, exact_buckets, fp64_buckets)
 
     ctx.set_sequences(ss.bases, ss.offs)
-    timed_loop(args.warmup, False)                      # warm-up (untimed)
     sampler = ClockSampler(local_rank)
     if rank == 0:
-        sampler.start()
+        sampler.start()                                 # running before the warm-up: rows exist when the timed region begins
+    timed_loop(args.warmup, False)                      # warm-up (untimed)
+    sampler.mark_begin()
     ms_dev, launches, stage, lookups, _, _, result, work, (tensor_flops, exact_buckets, fp64_buckets) = timed_loop(args.steps, False)
     timed_loop(max(1, min(args.warmup, 2)), True)
     ms_e2e, _, stage_e2e, _, h2d, d2h, result_e2e, _, _ = timed_loop(args.steps, True)

@@ -9,9 +9,9 @@ import subprocess
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(REPO, "paper_1605_06904_b200", "libpm_b200.so")
-WANT = ["em_refine_tc_kernelILi16", "em_refine_pair_kernelILi8", "em_refine_f64_kernel", "hash_bucket_fused_kernel",
+WANT = ["em_refine_tc_kernelILi16", "em_refine_pair_kernelILi8", "em_refine_f64_kernel", "hash_bucket_fused_kernel", "plan_sample_kernel", "trial_reduce_kernel",
         "count_hist_kernel", "count_scan_kernel", "count_scatter_kernel", "count_order_kernel", "encode_kernel",
-        "hamming_scan_kernel", "median_string_kernel", "trial_best_kernel", "mt64_stream_kernel",
+        "hamming_scan_kernel", "median_string_kernel", "mt64_stream_kernel",
         "radix_scatter_kernelIjLb0", "project_keys_kernelIj"]
 PAT = re.compile(r"\b(UTCHMMA|LDTM|STTM|UTCBAR|UBLKCP|SYNCS|USETMAXREG|FADD2|FMUL2|FFMA2|REDG|ATOMG|ATOMS|REDUX|MUFU\.EX2|F2FP|"
                  r"POPC|MATCH|ELECT|DADD|DFMA)\b")
@@ -30,7 +30,7 @@ def main():
         name = f.split("\n", 1)[0].strip()
         if not any(w in name for w in WANT):
             continue
-        dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip().split("(")[0]
+        dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip().replace("(anonymous namespace)", "{anonymous}").split("(")[0]
         lines = [ln for ln in f.split("\n") if re.search(r"/\*[0-9a-f]{4,}\*/", ln) and not re.match(r"\s*/\* 0x", ln)]
         cnt, sample = collections.Counter(), {}
         for ln in lines:
