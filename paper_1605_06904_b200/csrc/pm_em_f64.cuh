@@ -184,17 +184,26 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
                     const int q0 = lane;  // first base this lane looks at
                     uint64_t word = wp[q0 >> 5];
                     int in_word = q0 & 31;
-                    for (int j = 0; j < W; ++j) {
-                        const double zj = zi[j];
-                        const unsigned sym = static_cast<unsigned>(word >> (62 - 2 * in_word)) & 3u;
-                        if (++in_word == 32) {
-                            in_word = 0;
-                            word = wp[((q0 + j + 1) >> 5)];
+                    // eight responsibilities are fetched at a time (the loads were the latency of this loop: one L2 round
+                    // trip per window); they are added in window order, like the reference's sequential sums
+                    for (int j0 = 0; j0 < W; j0 += 8) {
+                        double zb[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) zb[u] = j0 + u < W ? zi[j0 + u] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (j0 + u >= W) break;
+                            const double zj = zb[u];
+                            const unsigned sym = static_cast<unsigned>(word >> (62 - 2 * in_word)) & 3u;
+                            if (++in_word == 32) {
+                                in_word = 0;
+                                word = wp[((q0 + j0 + u + 1) >> 5)];
+                            }
+                            a0 += sym == 0u ? zj : 0.0;
+                            a1 += sym == 1u ? zj : 0.0;
+                            a2 += sym == 2u ? zj : 0.0;
+                            a3 += sym == 3u ? zj : 0.0;
                         }
-                        a0 += sym == 0u ? zj : 0.0;
-                        a1 += sym == 1u ? zj : 0.0;
-                        a2 += sym == 2u ? zj : 0.0;
-                        a3 += sym == 3u ? zj : 0.0;
                     }
                 }
                 if (lane < l) {
