@@ -2412,10 +2412,17 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
     // gather them share a handful of synchronisations (a trial at a time cost ~0.6 ms each on the n = 1000 sets).
     std::vector<char> tb_exact(static_cast<size_t>(n_trials), 0);
     {
+        // Only a trial that can still become the incumbent needs it: in the ascending scan below the incumbent's score is
+        // the largest score seen so far, so a trial scoring less cannot improve on it whatever its expectation (its
+        // per-trial record is settled only when the caller asked for per-trial outputs).
+        const bool want_all = trial_best_score != nullptr || trial_best_expectation != nullptr || trial_best_key != nullptr;
+        int run_max = st->have_best ? st->best.score : -1;
         std::vector<int> need;
         for (int i = 0; i < n_trials; ++i) {
             const TrialSummary& s = tb[static_cast<size_t>(i)];
-            if (s.work >= 0 && s.n_close != 0) need.push_back(i);
+            if (s.work < 0) continue;
+            if (s.n_close != 0 && (want_all || s.score >= run_max)) need.push_back(i);
+            run_max = std::max(run_max, s.score);
         }
         if (!need.empty()) {
             std::vector<unsigned int> woff(static_cast<size_t>(n_trials) + 1);
