@@ -253,16 +253,23 @@ __device__ __forceinline__ void tc_split3(float x, uint32_t& hi, uint32_t& mid, 
 // A tile is refined in PASSES over the whole sequence set: EM iteration `it` (0-based) is one EM pass (E-step fused
 // with the M-step counts), the last pass is the final E-step (refine.hpp:306).  Every role decodes the same list.
 //
-// The exponentials of an EM pass are taken relative to ONE reference per bucket and pass, kTcRefBelow under the upper
-// bound ub = sum_c max_r D[c][r] of every window weight of the model: e = 2^(w - ub + 108) <= 2^108 cannot overflow
+// The exponentials of an EM pass are taken relative to ONE reference per bucket and pass, tc_ref_below(l) = 64 ... 108
+// under the upper bound ub = sum_c max_r D[c][r] of every window weight of the model: e = 2^(w - ub + 108) <= 2^108 cannot overflow
 // (nor can a sequence's sum, or the FP32 count accumulators), and a sequence whose best window lies up to
-// ~210 below ub -- seven columns at the 1e-9 floor -- still has its leading terms 24 binades above the FP32
+// offset + 100 below ub (l = 20: seven columns at the 1e-9 floor) still has its leading terms 24 binades above the FP32
 // underflow threshold; relative precision does not depend on the scale.  A sequence below that range (its sum under
 // kTcMinSum) flags the bucket for the exact kernel.  This replaces the separate per-sequence maximum passes
 // (GEMM1 + a max scan of S) that the first two iterations needed to find a reference.
 enum : int { kTcPassEm = 1, kTcPassFinal = 2 };
-constexpr float kTcRefBelow = 108.f;                 // log2 units
+constexpr float kTcRefBelow = 108.f;                 // log2 units, at l = 20 (tc_ref_below)
 constexpr float kTcMinSum = 7.888609052210118e-31f;  // 2^-100
+// How far under the bound the reference sits.  The FP32 accumulators of GEMM1 hold weight - reference, so their
+// rounding error (a few ulps of that magnitude) grows with the offset: measured max |d theta| against the reference on
+// random sets 1.7e-5 / 3.5e-5 / 7.6e-5 at 32 / 64 / 108.  What the offset buys is range -- a sequence whose best window
+// lies more than offset + 100 under the bound flags its bucket -- and the depth a sequence can sink to grows with the
+// motif length (one column at the 1e-9 floor costs 28): at l = 20 an offset of 64 flags 2.5 x as many buckets as 108,
+// at l <= 16 it flags fewer (better precision, fewer near-ties).  Hence 64 up to l = 16 and 11 more per extra column.
+__host__ __device__ inline float tc_ref_below(int l) { return l <= 16 ? 64.f : fminf(kTcRefBelow, 64.f + 11.f * static_cast<float>(l - 16)); }
 struct TcPass {
     int kind, it;
     bool new_model;  // theta -> log-odds terms are rebuilt before this pass (always: every pass has its own model)
@@ -674,11 +681,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                         ++xq;
                         expct = wg == 0 ? static_cast<double>(ex_part) + static_cast<double>(oth.x) : static_cast<double>(oth.x) + static_cast<double>(ex_part);
                         const float ub = wg == 0 ? ub_part + oth.y : oth.y + ub_part;  // same value in both partners
-                        // The reference of this pass's exponentials, kTcRefBelow under the bound, is folded into the
+                        // The reference of this pass's exponentials, tc_ref_below(l) under the bound, is folded into the
                         // log-odds: every window has exactly l live columns, so taking ref / l off every entry makes
                         // GEMM1 produce weight - ref itself (one subtraction per element less in the sweep).  The final
                         // E-step only compares weights: the shift does not matter there.
-                        qref = (ub - kTcRefBelow) / static_cast<float>(l);
+                        qref = (ub - tc_ref_below(l)) / static_cast<float>(l);
                         ref_eff = static_cast<double>(l) * static_cast<double>(qref);
                     }
                     // three bf16 terms (hi + mid + lo = 24 significant bits) of D - ref / l
@@ -745,7 +752,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) em_refine_tc_kernel(const EmPar
                     }
                     tc_wait_ld();
                     const float L = (__uint_as_float(r0[0]) + __uint_as_float(r0[1])) + (__uint_as_float(r0[2]) + __uint_as_float(r0[3]));
-                    // below kTcMinSum the sequence's best window is more than ~208 under the bound: out of range
+                    // below kTcMinSum the sequence's best window is more than offset + 100 under the bound: out of range
                     if (!(L >= kTcMinSum) || !(L < INFINITY)) flags |= kTcFlagRange;
                     const float inv = 1.f / L;
 #pragma unroll

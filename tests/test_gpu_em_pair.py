@@ -85,7 +85,7 @@ def test_tensor_core_kernel_on_random_shapes(pm, best_oracle):
     64, 80), ragged sequence lengths (segments that end in the middle of a chunk, blocks of every size), 2 ... 40
     sequences and iteration budgets 1 ... 8, against the reference: discrete outputs strictly equal -- whatever the
     kernel cannot decide with margin it hands to the exact kernels -- and theta / expectation within tolerance.  The
-    exponent range of its single per-bucket reference (108 binades under the weight bound) is exercised by theta0's
+    exponent range of its single per-bucket reference (64 ... 108 binades under the weight bound) is exercised by theta0's
     floored columns: buckets of one or two members."""
     from oracle import pmo
     rng = np.random.default_rng(1605)
@@ -107,7 +107,9 @@ def test_tensor_core_kernel_on_random_shapes(pm, best_oracle):
                 assert np.abs(a["theta"].astype(np.float64) - w.theta).max() <= THETA_TOL
                 assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
             total += len(en)
-        assert total > 800 and handed < total // 2  # most buckets were decided on the tensor cores
+        # buckets of one member put most columns of theta0 at the floor: many of them leave the exponent range of the
+        # kernel's single reference (64 binades under the bound for l <= 16) and are handed over -- not all of them
+        assert total > 800 and handed < 3 * total // 4
     finally:
         os.environ.pop("PM_B200_EM_TC", None)
 
