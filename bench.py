@@ -411,6 +411,20 @@ def run_b200_arm(args, cfg, rank, world, local_rank):
         "buckets_refined_again": {"pair_kernel": exact_buckets // args.steps, "fp64_kernel": fp64_buckets // args.steps,
                                   "of": result.buckets_enriched},
     }
+    if on_tensor:
+        # What actually bounds the tensor-core kernel: every pass reads the S block of every tile out of
+        # tensor memory, 4 bytes per (bucket, window column), at the measured 64 B/clk/SM of tcgen05.ld.
+        W = cfg["n"] - l + 1
+        ru = lambda v, m_: -(-v // m_) * m_
+        cols = t * ru(ru(-(-W // 2), 16) + ru(W // 2, 16), 32)
+        tiles = -(-result.buckets_enriched // 128)
+        passes = 5 + 1  # default max_em_iters EM passes + the final E-step
+        tmem_bytes = tiles * passes * 128 * cols * 4
+        tmem_peak = 148 * 64 * sm_max_mhz * 1e6 / 1e9  # GB/s
+        roofline["tmem_read"] = {"achieved": tmem_bytes / (em_ms * 1e-3) / 1e9 if em_ms > 0 else None, "peak": tmem_peak, "unit": "GB/s",
+                                 "frac": (tmem_bytes / (em_ms * 1e-3) / 1e9 / tmem_peak) if em_ms > 0 else None,
+                                 "note": "S blocks read by tcgen05.ld per step (tiles x 6 passes x 128 rows x padded window columns x 4 B) "
+                                         "over the EM stage time, against 148 SMs x 64 B/clk (measured tcgen05.ld rate) x clock"}
     config = workload_config(cfg, m_total, world, args.scaling)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
