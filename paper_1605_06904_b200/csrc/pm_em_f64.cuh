@@ -1,8 +1,10 @@
 // pm_em_f64.cuh — refine() of one bucket per CTA entirely in FP64, in the reference's own operation order where the
 // order is observable (refine.hpp:90-326): per-window weights are summed column by column, the per-sequence maximum
-// is exact, write_column sums its four entries in symbol order.  A warp takes a sequence; sums over its windows are
-// fixed-shape trees (per-lane strided partial sums, then shuffles: deterministic, a few ulps from the reference's
-// sequential sums); the per-sequence likelihood terms are added in sequence order like the reference.
+// is exact, write_column sums its four entries in symbol order, and every sum whose rounding reaches an output is one
+// chain in the reference's order: the exponentials of a sequence window by window, the background log term base by
+// base, the M-step counts window by window across the whole set, the likelihood sequence by sequence.  What remains
+// outside this kernel's control is the last bit of exp() and log() themselves (CUDA's against the host libm's).  A warp
+// takes a sequence in the E-step; the M-step is one warp (lane = column).
 //
 // Not a throughput kernel.  It settles what the FP32 kernels cannot: two candidates of equal score whose expectations
 // differ by less than the FP32 error (detail::candidate_improves compares doubles exactly, driver.hpp:127-135), and it
@@ -22,12 +24,28 @@ struct F64Extra {
     int steps_only;        // 1: run exactly max_iters em_step()s from theta_in, no stop test, no final E-step outputs
 };
 
+// v[0..n) added in index order by a whole warp; every lane returns the sum.  The lanes fetch 32 values at a time
+// (coalesced, two groups ahead) and hand them round with shuffles, so the chain waits on the adder, not on memory.
+// Entries past n are 0.0, and x + 0.0 == x.
+__device__ __forceinline__ double warp_chain_sum(const double* v, int n, int lane) {
+    double se = 0.0;
+    double cur = lane < n ? v[lane] : 0.0;
+    double nxt = 32 + lane < n ? v[32 + lane] : 0.0;
+    for (int g = 0; g < n; g += 32) {
+        const double nn = g + 64 + lane < n ? v[g + 64 + lane] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) se += __shfl_sync(0xffffffffu, cur, u);
+        cur = nxt;
+        nxt = nn;
+    }
+    return se;
+}
+
 __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmParams p, const F64Extra x) {
     __shared__ double th[4 * 32];     // theta[r][c] at c * 4 + r, c = 0 background
     __shared__ double D[4 * 32];      // log max(theta[r][c+1],1e-9) - log max(theta[r][0],1e-9) at c * 4 + r
     __shared__ double lbg[4];
     __shared__ double cnt[4 * 32];                        // M-step counts, cell c * 4 + r
-    __shared__ double part[(kF64Threads / 32) * 32 * 4];  // per-warp partial counts
     __shared__ double ll_seq[kF64LlSeqs];
     __shared__ int prof[4 * 32];
     const int tid = threadIdx.x;
@@ -108,20 +126,25 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
                         if (lane == 0) atomicExch(p.error_flag, 1u);
                     }
                     __syncwarp();
-                    double se = 0.0;
-                    for (int j = lane; j < W; j += 32) {
-                        const double e = exp(zi[j] - M);
-                        zi[j] = e;
-                        se += e;
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-                    const double S = se;
+                    for (int j = lane; j < W; j += 32) zi[j] = exp(zi[j] - M);
+                    __syncwarp();
+                    // sum_exp in window order (refine.hpp:191-194): one chain (warp_chain_sum), so
+                    // the responsibilities e / S round like the reference's
+                    const double S = warp_chain_sum(zi, W, lane);
+                    __syncwarp();
                     if (!final_pass) {
                         for (int j = lane; j < W; j += 32) zi[j] /= S;
                         // log P(S_i) = log prod theta_bg - log W + logsumexp (refine.hpp:200)
+                        // log_base: one term per base, in sequence order (refine.hpp:172-175)
                         double lb = 0.0;
-                        for (int r = 0; r < 4; ++r) lb += static_cast<double>(p.seq_sym[i * 4 + r]) * lbg[r];
+                        {
+                            const int len = p.seq_len[i];
+                            for (int q = 0; q < len; q += 32) {
+                                const uint64_t word = wp[q >> 5];
+                                const int m = min(32, len - q);
+                                for (int u = 0; u < m; ++u) lb += lbg[static_cast<unsigned>(word >> (62 - 2 * u)) & 3u];
+                            }
+                        }
                         const double term = lb - log(static_cast<double>(W)) + M + log(S);
                         if (t <= kF64LlSeqs) {
                             if (lane == 0) ll_seq[i] = term;
@@ -169,54 +192,53 @@ __global__ void __launch_bounds__(kF64Threads) em_refine_f64_kernel(const EmPara
             }
             if (final_pass) break;
 
-            // ---- M-step (refine.hpp:227-237): counts[c][r] = sum of z over the windows that show r at column c.
-            // Warp w takes the sequences i = w, w + 20, ...; lane = motif column, four accumulators (one per symbol);
-            // the per-warp partials are added in warp order: fixed shape, deterministic.
+            // ---- M-step (refine.hpp:227-237): counts[c][r] = sum of z over the windows that show r at column c, added in
+            // the reference's order -- sequence by sequence, window by window, ONE chain per cell carried across the
+            // sequences -- because the rounding of these sums is observable: saturated models (every column one symbol,
+            // the rest on the floor) have expectations that differ in the last bits only, and candidate_improves
+            // (driver.hpp:127-135) compares them exactly.  Four warps walk the set, one per symbol; lane = motif column.  The chain
+            // costs an FP64 add per window (~0.1 ms per pass on the (15,4) set): this kernel settles a handful of buckets
+            // per run, its latency is not the product's.
             __syncthreads();
-            {
-                const int warp = tid >> 5, lane = tid & 31;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                for (int i = warp; i < t; i += kF64Threads / 32) {
+            if (tid < 128) {
+                // warp r keeps the chains of symbol r; lane = motif column
+                const unsigned r = static_cast<unsigned>(tid >> 5);
+                const int lane = tid & 31;
+                const int col = min(lane, l - 1);  // lanes past the motif shadow its last column (their sums are dropped)
+                double a = 0.0;
+                for (int i = 0; i < t; ++i) {
                     const uint64_t* __restrict__ wp = p.words + p.word_off[i];
                     const int W = p.seq_len[i] - l + 1;
                     const double* zi = z + p.win_off[i];
-                    // lane's column of window j is base j + lane: one symbol stream per lane, read word by word
-                    const int q0 = lane;  // first base this lane looks at
-                    uint64_t word = wp[q0 >> 5];
-                    int in_word = q0 & 31;
-                    // eight responsibilities are fetched at a time (the loads were the latency of this loop: one L2 round
-                    // trip per window); they are added in window order, like the reference's sequential sums
-                    for (int j0 = 0; j0 < W; j0 += 8) {
-                        double zb[8];
+                    // The lane's column of windows g .. g+31 is the 32 bases from g + col: one 64-bit window, turned into a
+                    // match mask for this warp's symbol (bit 62-2u set iff window g+u shows r at the lane's column).  The
+                    // responsibilities come 32 at a time, two groups ahead, and go round the warp with shuffles; a step
+                    // is two shuffles, two selects and an add -- the loop waits on the adder only.  Responsibilities
+                    // past W are 0.0 (a + 0.0 == a), so the last group needs no special case.
+                    const uint64_t rpat = static_cast<uint64_t>(r) * 0x5555555555555555ULL;
+                    uint64_t v = load_window(wp, col);
+                    double cur = lane < W ? zi[lane] : 0.0;
+                    double nxt = 32 + lane < W ? zi[32 + lane] : 0.0;
+                    for (int g = 0; g < W; g += 32) {
+                        const double nn = g + 64 + lane < W ? zi[g + 64 + lane] : 0.0;
+                        const uint64_t v_next = g + 32 < W ? load_window(wp, g + 32 + col) : 0ULL;
+                        const uint64_t x = v ^ rpat;
+                        const uint64_t mt = ~(x | (x >> 1)) & 0x5555555555555555ULL;
+                        const unsigned mh = static_cast<unsigned>(mt >> 32), ml = static_cast<unsigned>(mt);
+                        const int cur_lo = __double2loint(cur), cur_hi = __double2hiint(cur);
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) zb[u] = j0 + u < W ? zi[j0 + u] : 0.0;
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            if (j0 + u >= W) break;
-                            const double zj = zb[u];
-                            const unsigned sym = static_cast<unsigned>(word >> (62 - 2 * in_word)) & 3u;
-                            if (++in_word == 32) {
-                                in_word = 0;
-                                word = wp[((q0 + j0 + u + 1) >> 5)];
-                            }
-                            a0 += sym == 0u ? zj : 0.0;
-                            a1 += sym == 1u ? zj : 0.0;
-                            a2 += sym == 2u ? zj : 0.0;
-                            a3 += sym == 3u ? zj : 0.0;
+                        for (int u = 0; u < 32; ++u) {
+                            // the addend is selected (z or 0.0) off the chain; the chain itself is one DADD per window
+                            const int zlo = __shfl_sync(0xffffffffu, cur_lo, u), zhi = __shfl_sync(0xffffffffu, cur_hi, u);
+                            const bool on = (u < 16 ? (mh & (1u << (30 - 2 * u))) : (ml & (1u << (62 - 2 * u)))) != 0u;
+                            a += __hiloint2double(on ? zhi : 0, on ? zlo : 0);
                         }
+                        cur = nxt;
+                        nxt = nn;
+                        v = v_next;
                     }
                 }
-                if (lane < l) {
-                    double* out = part + (warp * 32 + lane) * 4;
-                    out[0] = a0, out[1] = a1, out[2] = a2, out[3] = a3;
-                }
-            }
-            __syncthreads();
-            if (tid < 4 * l) {
-                const int c = tid >> 2, r = tid & 3;
-                double sum = 0.0;
-                for (int w = 0; w < kF64Threads / 32; ++w) sum += part[(w * 32 + c) * 4 + r];
-                cnt[tid] = sum;
+                if (lane < l) cnt[lane * 4 + r] = a;
             }
             __syncthreads();
             ++iterations;

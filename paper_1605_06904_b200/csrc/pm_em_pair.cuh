@@ -29,6 +29,14 @@ constexpr int kPairMaxWarps = 10;  // 12 was measured no faster and caps the ker
 constexpr int kPairMaxSeqs = 64;     // small sets: per-sequence state (previous maxima, metadata) lives in shared memory;
                                      // large sets: at most this many sequences per tile
 constexpr int kPairMaxWords = 2048;  // small sets: packed words of the whole set, staged once per CTA by one TMA bulk copy
+// Two different l-mers whose FP64 weights (under this kernel's theta) lie closer than this go to the FP64 kernel.  The
+// FP32 error of the M-step sums is ~1e-6 in a window weight.  EM amplifies an asymmetry eps between two equally good
+// windows of one sequence: the cells they touch move by eps / count, the weight gap by up to 2 l eps / count, the
+// responsibilities by a quarter of that -- a factor l / (2 count) per iteration, count being the column mass behind a
+// cell, which grows with the number of sequences t.  With t = 20 (every BASELINE configuration, verified trial by trial
+// against the reference) the factor is below one; with two or three sequences it reaches ~l/2, so the window widens as
+// 20 / t, up to ten times.  (A gap that EM has already blown up beyond the window cannot be seen from the final state.)
+constexpr double kPairTieAbs = 2e-6, kPairTieRel = 1e-7, kPairTieAmpMax = 10.0;
 constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
 
 // The per-sequence bookkeeping around the two hot loops is large straight-line code that every warp walks
@@ -705,10 +713,21 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                 // window wins in the reference (refine.hpp:165-186, :311-316) is decided by the FP64 kernel.
                                 // (The same l-mer twice has bit-identical weights everywhere: the smaller offset wins, as
                                 // above.)  Not for large sets: an FP64 refinement of 10^7 windows takes seconds per bucket.
-                                if (!big && p.flag_exact != nullptr && lane == 0 && (bb == 0 || live1) && sj != 0x7fffffff &&
-                                    bw - sw <= 2e-6 + 1e-7 * fabs(bw) &&
-                                    ((load_window(wp, bj) ^ load_window(wp, sj)) >> (64 - 2 * l)) != 0ULL)
-                                    p.flag_exact[ois[bb]] = 1;
+                                // The runner-up that matters is the best window showing ANOTHER l-mer: repeats of the winning
+                                // l-mer (homopolymer runs, tandem copies) tie exactly and must not hide it.
+                                if (!big && p.flag_exact != nullptr && (bb == 0 || live1) && sj != 0x7fffffff) {
+                                    const uint64_t bv = load_window(wp, bj) >> (64 - 2 * l);
+                                    double dw = -INFINITY;
+                                    for (int e = lane; e < s.nnear; e += 32) {
+                                        const uint64_t v = load_window(wp, my_near[e]);
+                                        if ((v >> (64 - 2 * l)) != bv) dw = fmax(dw, window_weight_rolled(D, v, l));
+                                    }
+#pragma unroll
+                                    for (int o = 16; o > 0; o >>= 1) dw = fmax(dw, __shfl_xor_sync(0xffffffffu, dw, o));
+                                    // count ~ t: the window is the FP32 one (2e-6) from t = 20 on and ten times that for t <= 2
+                                    const double amp = fmin(kPairTieAmpMax, fmax(1.0, 20.0 / static_cast<double>(t)));
+                                    if (lane == 0 && bw - dw <= amp * (kPairTieAbs + kPairTieRel * fabs(bw))) p.flag_exact[ois[bb]] = 1;
+                                }
                             } else {
                                 float bw = s.best_w;
                                 int bj = s.best_j;

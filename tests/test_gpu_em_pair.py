@@ -161,3 +161,63 @@ def test_large_set_path_with_frozen_buckets(ctx, best_oracle):
     got = ctx.refine(8, [e["members"] for e in en], max_iters=12)
     for a, w in zip(got, want):
         _check(a, w)
+
+
+def test_near_ties_behind_repeats_of_the_winning_lmer(pm, best_oracle):
+    """tests/golden/near_tie_cases.json: buckets of random two-sequence sets on which the reference's argmax
+    (refine.hpp:311-316) chooses between two DIFFERENT l-mers whose FP64 weights differ by 1e-10 .. 9e-8 -- in three of
+    them the winning l-mer also occurs two or three times in the sequence (bit-identical weights), which used to hide the
+    other l-mer from the near-tie test.  Every tier must hand these to the FP64 kernel and return the reference's
+    positions; the fixture's `want` is re-checked against the oracle."""
+    import json
+    from oracle import pmo
+    path = os.path.join(os.path.dirname(__file__), "golden", "near_tie_cases.json")
+    cases = json.load(open(path))["cases"]
+    assert len(cases) == 4
+    for cs in cases:
+        ss = pmo.SeqSet.from_strings(cs["strings"])
+        w = best_oracle.refine(ss, cs["l"], cs["members"], 0, max_iters=cs["max_iters"])
+        assert (w.consensus, w.score, list(w.positions), w.iterations) == \
+               (cs["want"]["consensus"], cs["want"]["score"], cs["want"]["positions"], cs["want"]["iterations"])
+        for mode in ("2", "1", "0"):
+            os.environ["PM_B200_EM_TC"] = mode
+            try:
+                with pm.Context(0) as c:
+                    c.set_sequences(ss.bases, ss.offs)
+                    a = c.refine(cs["l"], [cs["members"]], max_iters=cs["max_iters"])[0]
+                    assert c.em_exact_counts()["fp64"] == 1, (mode, cs["origin"])
+            finally:
+                os.environ.pop("PM_B200_EM_TC", None)
+            assert (a["consensus"], a["score"], list(a["positions"]), a["iterations"]) == \
+                   (w.consensus, w.score, list(w.positions), w.iterations), (mode, cs["origin"])
+            assert abs(a["expectation"] - w.expectation) <= EXPECTATION_TOL
+
+
+def test_run_decided_by_the_last_bit_of_saturated_expectations(pm, best_oracle):
+    """tests/golden/near_tie_cases.json `runs`: every trial's best bucket is a saturated model (each column one symbol,
+    the rest on the 1e-9 floor), so the expectations are 6 / (1 + 3e-9) up to the rounding of the M-step sums, and
+    candidate_improves (driver.hpp:127-135) compares them exactly: the reference's winner is trial 1 because trial 2's
+    expectation is one ulp smaller.  The FP64 kernel adds every observable sum in the reference's order
+    (csrc/pm_em_f64.cuh), so the per-trial expectations are bit-identical and so is the winner, through every tier."""
+    import json
+    from oracle import pmo
+    path = os.path.join(os.path.dirname(__file__), "golden", "near_tie_cases.json")
+    for cs in json.load(open(path))["runs"]:
+        ss = pmo.SeqSet.from_strings(cs["strings"])
+        want = best_oracle.run(ss, **cs["kw"])
+        for f, v in cs["want"].items():
+            assert (want[f].tolist() if hasattr(want[f], "tolist") else want[f]) == v, f
+        for mode in ("2", "1", "0"):
+            os.environ["PM_B200_EM_TC"] = mode
+            try:
+                with pm.Context(0) as c:
+                    c.set_sequences(ss.bases, ss.offs)
+                    got = c.run(per_trial=True, **cs["kw"])
+            finally:
+                os.environ.pop("PM_B200_EM_TC", None)
+            for f, v in cs["want"].items():
+                assert got[f] == v, (mode, f, got[f], v)  # the expectation too: exact
+            assert got["trial_buckets"].tolist() == cs["trial_buckets"]
+            assert got["trial_score"].tolist() == cs["trial_score"]
+            assert got["trial_key"].tolist() == cs["trial_key"]
+            assert got["trial_expectation"].tolist() == cs["trial_expectation"], mode
