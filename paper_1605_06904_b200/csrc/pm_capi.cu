@@ -2520,10 +2520,12 @@ int run_batch(pm_ctx* c, const pm_run_config* cfg, const pm_run_result& params, 
         if (s.work >= 0) {
             if (!st->have_best) {
                 improves = true;
-            } else if (s.score == st->best.score && s.expct != st->best.expct &&
-                       std::fabs(s.expct - st->best.expct) <= kTieEps) {
-                // equal score, expectations closer than the FP32 error: both in FP64 (bit-equal expectations are the
-                // same model -- identical member lists -- and stay an exact tie)
+            } else if (s.score == st->best.score && std::fabs(s.expct - st->best.expct) <= kTieEps &&
+                       (s.expct != st->best.expct || static_cast<double>(static_cast<float>(s.expct)) == s.expct)) {
+                // equal score, expectations closer than the FP32 error: both in FP64.  Bit-equal FP64 expectations are the
+                // same model -- identical member lists -- and stay an exact tie; bit-equal values that are FP32 numbers
+                // come from the tensor-core kernel, which rounds its expectation to FP32: different models can collide
+                // there (two saturated models 3e-14 apart in the reference), so those are settled too.
                 bool s_exact = tb_exact[static_cast<size_t>(i)] != 0;
                 if (!s_exact) {
                     std::vector<int32_t> mem;

@@ -33,9 +33,11 @@ constexpr int kPairMaxWords = 2048;  // small sets: packed words of the whole se
 // FP32 error of the M-step sums is ~1e-6 in a window weight.  EM amplifies an asymmetry eps between two equally good
 // windows of one sequence: the cells they touch move by eps / count, the weight gap by up to 2 l eps / count, the
 // responsibilities by a quarter of that -- a factor l / (2 count) per iteration, count being the column mass behind a
-// cell, which grows with the number of sequences t.  With t = 20 (every BASELINE configuration, verified trial by trial
-// against the reference) the factor is below one; with two or three sequences it reaches ~l/2, so the window widens as
-// 20 / t, up to ten times.  (A gap that EM has already blown up beyond the window cannot be seen from the final state.)
+// cell, which grows with the number of sequences t.  The window widens as 50 / t, up to ten times: 5e-6 at t = 20 (every
+// BASELINE configuration; the campaign found gaps of 1e-9 in the reference that this kernel saw as 2.7e-6 and 3.8e-6 at
+// t = 21 and 16 -- a theta cell of 0.03 carries ~6e-8 of absolute error, 2e-6 relative, once per differing column),
+// 2e-5 on sets of five sequences or fewer, where the amplification reaches ~l/2.  (A gap that EM has already blown up
+// beyond the window cannot be seen from the final state.)
 constexpr double kPairTieAbs = 2e-6, kPairTieRel = 1e-7, kPairTieAmpMax = 10.0;
 constexpr int kPairNearCap = 64;     // near-maximum windows re-evaluated in FP64, per warp and bucket
 
@@ -724,8 +726,8 @@ em_refine_pair_kernel(const EmParams p, const EmSmemExtra x) {
                                     }
 #pragma unroll
                                     for (int o = 16; o > 0; o >>= 1) dw = fmax(dw, __shfl_xor_sync(0xffffffffu, dw, o));
-                                    // count ~ t: the window is the FP32 one (2e-6) from t = 20 on and ten times that for t <= 2
-                                    const double amp = fmin(kPairTieAmpMax, fmax(1.0, 20.0 / static_cast<double>(t)));
+                                    // count ~ t: the window is 5e-6 at t = 20, the FP32 one (2e-6) from t = 50 on and ten times that for t <= 5
+                                    const double amp = fmin(kPairTieAmpMax, fmax(1.0, 50.0 / static_cast<double>(t)));
                                     if (lane == 0 && bw - dw <= amp * (kPairTieAbs + kPairTieRel * fabs(bw))) p.flag_exact[ois[bb]] = 1;
                                 }
                             } else {

@@ -115,7 +115,7 @@ def main():
     s = s[:a] + "<!-- r2-table-begin -->\n" + table + "\n" + s[b:]
     if "c1" in rec and "time_to_motif" in rec["c1"]:
         ttm = rec["c1"]["time_to_motif"]
-        s = re.sub(r"<!-- r2-ttm -->[^.]*\.", f"<!-- r2-ttm -->median {ttm['ms_median']:.2f} ms against {ttm.get('cpu_ms_median', 0):.0f} ms for the reference.", s)
+        s = re.sub(r"<!-- r2-ttm -->.*?for the reference\.(?:[0-9. a-z]*for the reference\.)*", f"<!-- r2-ttm -->median {ttm['ms_median']:.2f} ms against {ttm.get('cpu_ms_median', 0):.0f} ms for the reference.", s)
     open("DESIGN.md", "w").write(s)
     print(table)
 
